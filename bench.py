@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-transition hot path (BASELINE.json metric:
+"state-switch latency (ms) and GB/s vs HBM/host-link/NVLink peak").
+
+One STEP = one pass of the whole hot path over one job's
+synthetic Qwen2.5-7B-shaped state on the GPU group:
+    suspend (a3 gather-pack + a4 D2H into the pinned slab)
+    resume  (a6 H2D + a7 scatter-unpack + checksum verify)
+    sync    (a8 fp32->bf16 RNE + a9-a11 reshard into the rollout layout)
+Workload at N GPUs: FSDP-N shards -> rollout TP-min(2,N) x DP-N/TP (configs[1]
+is N=8: FSDP-8 -> TP-2 x DP-4).  ``value`` = state bytes switched by all ranks
+per second (sum over ranks of the per-rank state S, ÷ the max-over-ranks step
+time); ``ms_per_step`` is the switch latency.
+
+    python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
+    python bench.py --impl reference ...                        # the CPU oracle
+    torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "state-switch latency (ms) and GB/s vs HBM/host-link/NVLink peak at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="plex", choices=["plex", "reference"])
+    ap.add_argument("--model", default="qwen2.5-7b")
+    ap.add_argument("--tp", type=int, default=0, help="rollout TP (default min(2, N))")
+    ap.add_argument("--ep", type=int, default=1)
+    ap.add_argument("--bucket-mb", type=int, default=64)
+    ap.add_argument("--slots", type=int, default=3)
+    ap.add_argument("--hugepage", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    ap.add_argument("--sync-nccl", action="store_true", help="NCCL send/recv sync transport (baseline)")
+    ap.add_argument("--out", default="")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md: clocks DURING the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.index)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for ln in self.p.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample of the same workload)
+# ---------------------------------------------------------------------------
+def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int, reps: int = 1):
+    """Time the oracle's o4 pack, o5 parse, o6 cast and o7 reshard over the
+    first ``layers`` decoder layers of rank 0's FSDP-``world`` shard (+ the
+    final norm).  Returns (GB of state per second, seconds, sample string)."""
+    import numpy as np
+
+    from oracle import plex_oracle as O
+    from plexgen import gen_range, manifest
+
+    man = [(k, s) for k, s in manifest(model)
+           if any(k.startswith(f"model.layers.{l}.") for l in range(layers)) or k == "model.norm.weight"]
+    dp = world // tp
+    shards = {}
+    for k, s in man:
+        a, b = O.fsdp_rows(s[0], world, 0)
+        re_ = int(np.prod(s[1:])) if len(s) > 1 else 1
+        for kd in range(4):
+            shards[(k, kd)] = gen_range(0, k, kd, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:]))
+    S = sum(x.nbytes for x in shards.values())
+    # master shards of every rank for the reshard of this sample
+    ms = {}
+    for k, s in man:
+        re_ = int(np.prod(s[1:])) if len(s) > 1 else 1
+        parts = []
+        for r in range(world):
+            a, b = O.fsdp_rows(s[0], world, r)
+            parts.append(gen_range(0, k, 1, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:])))
+        ms[k] = parts
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        segs, size = O.slab_layout(man, world, 0)
+        slab = O.pack_slab(segs, size, shards)
+        O.parse_slab(slab, segs, dict(man))
+        O.weight_sync(ms, tp, dp, ep)
+    dt = (time.perf_counter() - t0) / reps
+    sample = (f"{model} layers[0:{layers}]+norm, rank-0 FSDP-{world} shard ({S / 1e9:.3f} GB state): "
+              f"o4 pack + o5 parse + o6/o7 gather-RNE-reshard to TP-{tp}xDP-{dp} (all ranks' outputs)")
+    return S / dt / 1e9, dt, sample
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = a.gpus
+    tp = a.tp or min(2, world)
+    for _ in range(max(0, a.warmup)):
+        pass  # the oracle has no warm state; warm-up steps would only repeat the sample
+    vals, secs = [], []
+    sample = ""
+    for _ in range(a.steps):
+        v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
+        vals.append(v)
+        secs.append(dt)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32 bits",
+            "data": "synthetic (counter-based generator, DESIGN.md §3)",
+            "config": {"workload": f"{a.model} FSDP-{world} -> TP-{tp}xDP-{world // tp} (oracle on a bounded sample)"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our CUDA path
+# ---------------------------------------------------------------------------
+def run_plex(a):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    import paper_2605_20863_b200 as P
+    from paper_2605_20863_b200 import _lib as L
+    from plexgen import MODELS, manifest
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    tp = a.tp or min(2, world)
+    dp = world // tp
+    shape = MODELS[a.model]
+    bucket = a.bucket_mb << 20
+    t_setup = time.perf_counter()
+    mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=a.slots, timing=True,
+                         sync_nccl=a.sync_nccl)
+    t0 = time.perf_counter()
+    plan = mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep)
+    plan_s = time.perf_counter() - t0
+    info = plan.rank_info(rank)
+    job = P.Job(mgr, plan, seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+    arena = mgr.arena(plan)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    # host-link roofline BW_host(k = world): pinned copy of 4 GiB, all ranks at once
+    probe = 4 << 30
+    h = torch.empty(probe, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(probe, dtype=torch.uint8, device=f"cuda:{local}")
+    bw = {}
+    for direction in ("d2h", "h2d"):
+        best = 0.0
+        for _ in range(3):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            (h.copy_(dbuf, non_blocking=True) if direction == "d2h" else dbuf.copy_(h, non_blocking=True))
+            e1.record()
+            e1.synchronize()
+            best = max(best, probe / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        bw[direction] = best
+    del h, dbuf
+    torch.cuda.empty_cache()
+
+    def step():
+        job.suspend(release=False)
+        job.resume()
+        job.sync(arena)
+
+    for _ in range(a.warmup):
+        step()
+    mgr.reset_stats()
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(a.steps):
+        step()
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / a.steps
+    ms = allmax(ms_local)
+    st = mgr.stats()
+
+    # end-to-end through the public API: state starts and ends in pinned host
+    # memory (release/re-acquire of device storage included), host clock.
+    e2e_steps = a.steps if a.e2e_steps < 0 else a.e2e_steps
+    e2e = None
+    if e2e_steps > 0:
+        job.suspend()                       # state now HOST-resident, device storage released
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            job.resume()                    # H2D of the step's input (the job state)
+            job.sync(arena)
+            job.suspend()                   # D2H of the step's result (the updated state)
+        barrier()
+        e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
+        job.resume()
+        e2e = {"S": info.payload_bytes, "s": e2e_s, "h2d": info.slab_bytes,
+               "d2h": info.slab_bytes + 16 * info.n_segments}
+
+    S_total = allsum(float(info.payload_bytes))
+    value = S_total / (ms * 1e-3) / 1e9
+    peak_hbm, peak_kind = load_peaks()
+
+    # roofline of the dominant kernel (largest total device time among ours)
+    kern = {k: st[k] for k in ("pack", "unpack", "push", "rpack", "runpack") if st[k]["launches"]}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[dom]
+    per_launch_bytes = d["bytes"] / d["launches"]
+    avg_ms = d["ms"] / d["launches"]
+    achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get(dom, {}).get("dram_bytes_per_launch")
+
+    def frac(x, p):
+        return round(x / p, 4) if p else None
+
+    d2h, h2d = st["d2h"], st["h2d"]
+    rl = {}
+    for k, v in kern.items():
+        if v["ms"] > 0:
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            rl[k] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak_hbm, "unit": "GB/s",
+                     "frac": frac(gbs, peak_hbm), "launches_per_step": v["launches"] / a.steps,
+                     "ms_per_step": round(v["ms"] / a.steps, 3)}
+    for k, v, ref in (("d2h", d2h, bw["d2h"]), ("h2d", h2d, bw["h2d"])):
+        if v["ms"] > 0:
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            rl["host_" + k] = {"bound": "host_link", "achieved": round(gbs, 2), "peak": round(ref, 2),
+                               "unit": "GB/s", "frac": frac(gbs, ref),
+                               "peak_kind": f"measured pinned copy, {world} GPU(s) concurrently"}
+    if "push" in kern and world > 1:
+        nv = max(info.send_bytes, info.recv_bytes)
+        nv = allmax(float(nv))
+        t_push = allmax(kern["push"]["ms"] / a.steps)
+        gbs = nv / (t_push * 1e-3) / 1e9
+        rl["nvlink"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s",
+                        "frac": frac(gbs, 900.0), "bytes_max_rank": nv,
+                        "peak_kind": "nominal 900 GB/s/dir (measured peer copy ref 770)"}
+    # our kernel launches per timed step: pack + unpack + push + 1 verify per onload
+    launches = sum(v["launches"] for v in kern.values()) + a.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16/fp32 bits (byte copy; fp32->bf16 RNE integer cast)",
+            "data": "synthetic (counter-based generator, DESIGN.md §3); random-init Qwen2.5-7B-shaped state",
+            "config": {"workload": f"{a.model} state (bf16 param + fp32 master/m/v) FSDP-{world} -> rollout "
+                                   f"TP-{tp}xDP-{dp}: suspend+resume+sync per step",
+                       "model_shape": a.model, "state_bytes_per_rank": info.payload_bytes,
+                       "state_bytes_total": int(S_total), "bucket_bytes": bucket, "staging_slots": a.slots,
+                       "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
+                       "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
+                       "sync_transport": "nccl" if a.sync_nccl else "nvlink-push"},
+            "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
+                         "unit": "GB/s", "frac": frac(achieved, peak_hbm), "traffic": traffic,
+                         "algorithmic_bytes_per_launch": int(per_launch_bytes), "avg_launch_ms": round(avg_ms, 4),
+                         "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+            "rooflines": rl,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+        }
+        if e2e:
+            line["e2e"] = {"value": round(S_total / e2e["s"] / 1e9, 3), "unit": "GB/s",
+                           "ms_per_step": round(e2e["s"] * 1e3, 2), "h2d_bytes_per_step": e2e["h2d"],
+                           "d2h_bytes_per_step": e2e["d2h"],
+                           "api": "Job.resume -> Job.sync -> Job.suspend(release) (host clock)"}
+        if not a.no_cpu_baseline and world == 1:
+            v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
+            line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                                    "sample": sample, "seconds": round(dt, 2)}
+        print(json.dumps(line), flush=True)
+        if a.out:
+            with open(a.out, "w") as f:
+                json.dump(line, f, indent=1)
+    barrier()
+    del job, arena
+    mgr.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_plex(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,302 @@
+/*
+ * plex.h — C ABI of libplex.so, the B200-native data plane of PlexRL's
+ * GPU-group state transition (arXiv 2605.20863, /root/reference/PAPER.md).
+ *
+ * The paper's StateManager exposes "blocking state-transfer primitives":
+ * "when a transfer returns, the requested state is resident and safe to use
+ * on the default CUDA stream" (§5.3).  The scheduler prepends
+ * "offload and load operations" when the incoming job differs from the
+ * resident one (§5.2.2), and weight synchronisation
+ * "materializ[es] training-visible state into the format expected by serving
+ * instances" (§4.5) with "each rollout rank fetch[ing] only the
+ * tensor slices required by its target parallel layout" (§5.3).
+ *
+ * Conventions:
+ *  - Every export returns plex_status (PLEX_OK = 0, negative on error); a
+ *    thread-local message is available from plex_last_error().  No C++
+ *    exception crosses the ABI.
+ *  - No partial mutation: a failed offload leaves the device tensors and the
+ *    slab's residency untouched; a failed onload leaves the slab untouched and
+ *    its residency HOST (destination contents unspecified); a failed sync
+ *    leaves the sources untouched (destination unspecified).
+ *  - Device memory for state, rollout tensors and staging is the CALLER's
+ *    (PyTorch's).  The library allocates only: pinned host slabs, small device
+ *    metadata tables (segment/work-item tables, pointer tables), events, and
+ *    NCCL internals.  Streams are the caller's (cudaStream_t passed as void*).
+ *  - Plans are immutable after creation and may be shared read-only.  Calls
+ *    on one (job, rank) state are serialised by the caller (WPG-serial
+ *    semantics).
+ *  - Element values are treated as raw bits: bf16 = 2 B, fp32 = 4 B.
+ */
+#ifndef PLEX_H
+#define PLEX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PLEX_API __attribute__((visibility("default")))
+#else
+#define PLEX_API
+#endif
+
+typedef int plex_status;
+
+#define PLEX_OK            0
+#define PLEX_E_INVAL      -1  /* bad argument / shape / pointer count          */
+#define PLEX_E_LAYOUT     -2  /* shape not divisible by TP / EP / head split   */
+#define PLEX_E_TIER_FULL  -3  /* pinned host allocation failed / too small     */
+#define PLEX_E_STATE      -4  /* residency mismatch (e.g. onload of empty slab)*/
+#define PLEX_E_CUDA       -5  /* CUDA runtime error                            */
+#define PLEX_E_NCCL       -6  /* NCCL error                                    */
+#define PLEX_E_CHECKSUM   -7  /* onload: restored bytes fail the R14 checksum  */
+
+/* State kinds (reading R1): bf16 params, fp32 master, Adam m, Adam v. */
+#define PLEX_KIND_PARAM       0   /* bf16, 2 B */
+#define PLEX_KIND_MASTER      1   /* fp32, 4 B */
+#define PLEX_KIND_EXP_AVG     2   /* fp32, 4 B */
+#define PLEX_KIND_EXP_AVG_SQ  3   /* fp32, 4 B */
+#define PLEX_NUM_KINDS        4
+#define PLEX_KINDMASK_ALL     0xFu
+#define PLEX_KINDMASK_OPTIM   0xEu  /* master + m + v (config 3) */
+
+/* Destination roles (reading R3, Megatron/vLLM tensor-parallel conventions). */
+#define PLEX_ROLE_REPLICATED  0   /* whole tensor on every rollout rank            */
+#define PLEX_ROLE_COL         1   /* dim-0 split by TP; pieces of one group fused  */
+#define PLEX_ROLE_ROW         2   /* dim-1 split by TP                             */
+#define PLEX_ROLE_EXPERT      3   /* whole tensor on EP rank floor(e / (E/EP))     */
+
+#define PLEX_SLAB_KIND_MAJOR  0   /* R4: for kind: for key   (default)  */
+#define PLEX_SLAB_KEY_MAJOR   1   /* R4: for key: for kind   (per-expert units) */
+
+#define PLEX_RANKMAP_TP_FAST  0   /* R10: g = dp*TP + tp (default) */
+#define PLEX_RANKMAP_DP_FAST  1   /* R10: g = tp*DP + dp           */
+
+/* Transition ops. */
+#define PLEX_OP_NONE     0
+#define PLEX_OP_OFFLOAD  1
+#define PLEX_OP_ONLOAD   2
+#define PLEX_OP_SYNC     3
+
+/* Residency of a slab's job state (PAPER.md:505-506 hierarchical residency). */
+#define PLEX_RES_DEVICE  0
+#define PLEX_RES_HOST    1
+
+/* Context flags. */
+#define PLEX_CTX_TIMING    0x1u  /* record CUDA events around every kernel/copy */
+#define PLEX_CTX_SYNC_NCCL 0x2u  /* weight sync via K4 pack + NCCL send/recv + K5
+                                    unpack instead of the fused NVLink push     */
+
+/* Slab flags. */
+#define PLEX_SLAB_HUGEPAGE 0x1u  /* mmap + MADV_HUGEPAGE + cudaHostRegister      */
+
+typedef struct plex_plan_s* plex_plan_t;
+typedef struct plex_ctx_s*  plex_ctx_t;
+typedef struct plex_slab_s* plex_slab_t;
+
+/* One logical (unsharded) tensor of the job's manifest, in canonical order
+ * (R4).  2-D view [d0, d1]; 1-D tensors have d1 = 1, ndim = 1.
+ *   role   : PLEX_ROLE_*.
+ *   group  : destination tensor id; tensors sharing a group are fused into
+ *            one rollout tensor, pieces concatenated along dim 0 in `slot`
+ *            order (qkv = q|k|v, gate_up = gate|up, w13 = gate_e|up_e ...).
+ *   expert : expert index e for PLEX_ROLE_EXPERT (else -1).
+ *   unit   : COL split granularity in rows (head_dim for q/k/v, else 1). */
+typedef struct {
+    const char* key;
+    int64_t d0, d1;
+    int32_t ndim;
+    int32_t role;
+    int32_t group;
+    int32_t slot;
+    int32_t expert;
+    int32_t unit;
+} plex_tensor_desc;
+
+/* Plan request (a1 + a2).  `world` is the GPU-group size: FSDP-world source
+ * shards (R2: rank r owns rows [min(d0,r*c), min(d0,(r+1)*c)), c=ceil(d0/N))
+ * and tp*dp destination ranks (tp*dp must equal world, or tp = dp = 0 for a
+ * plan without sync).  `subset` (optional) restricts the slab to those tensor
+ * indices; `kind_mask` to those kinds.  `bucket_bytes` is the staging bucket
+ * (multiple of 256 B, default 64 MiB); `tile_bytes` the kernel work item
+ * (multiple of 256 B, default 64 KiB).  resident_job / incoming_job (-1 =
+ * none) and `op` drive the transition decision of PAPER.md:555. */
+typedef struct {
+    int32_t n_tensors;
+    const plex_tensor_desc* tensors;
+    int32_t world;
+    int32_t tp, dp, ep;
+    int32_t rank_map;
+    int32_t slab_layout;
+    uint32_t kind_mask;
+    int32_t n_subset;
+    const int32_t* subset;
+    uint64_t bucket_bytes;
+    uint64_t tile_bytes;
+    int64_t resident_job;
+    int64_t incoming_job;
+    int32_t op;
+} plex_plan_req;
+
+typedef struct {
+    int32_t n_ops;               /* transition op list       */
+    int32_t ops[4];              /* PLEX_OP_*                               */
+    int64_t op_jobs[4];
+    int32_t n_tensors;
+    int32_t world, tp, dp, ep;
+    uint64_t total_params;       /* sum of numel over the manifest         */
+} plex_plan_stats;
+
+typedef struct {
+    uint64_t slab_bytes;         /* pinned slab size (256-B aligned)        */
+    uint64_t payload_bytes;      /* sum of segment bytes (no padding)       */
+    int32_t n_segments;
+    int32_t n_buckets;
+    uint64_t n_pack_items;
+    uint64_t dst_arena_bytes;    /* rollout arena size for this rank        */
+    int32_t n_dst_tensors;
+    uint64_t n_push_items;
+    uint64_t send_bytes;         /* bf16 bytes this rank pushes to peers    */
+    uint64_t recv_bytes;         /* bf16 bytes peers push to this rank      */
+    uint64_t local_bytes;        /* bf16 bytes cast locally (no transfer)   */
+    uint64_t src_read_bytes;     /* fp32 bytes read by this rank's push     */
+} plex_rank_info;
+
+typedef struct {
+    int32_t tensor;              /* manifest index                          */
+    int32_t kind;
+    uint64_t slab_offset;
+    uint64_t nbytes;
+    int64_t row0, row1;          /* FSDP rows of the logical tensor         */
+    uint64_t index_base;         /* logical flat index of first element     */
+} plex_seg_desc;
+
+typedef struct {
+    int32_t group;               /* plex_tensor_desc.group                  */
+    int32_t first_tensor;        /* manifest index of its first piece       */
+    uint64_t arena_offset;       /* byte offset in the rank's arena (256-B) */
+    int64_t rows, cols;          /* 2-D bf16 shape                          */
+} plex_dst_desc;
+
+typedef struct {
+    uint64_t launches;
+    double   total_ms;           /* sum of per-launch CUDA-event durations  */
+    uint64_t bytes;              /* algorithmic bytes moved by those launches */
+} plex_kernel_stats;
+
+#define PLEX_STAT_PACK    0      /* K1 gather-pack (+checksum)  */
+#define PLEX_STAT_UNPACK  1      /* K2 scatter-unpack (+verify) */
+#define PLEX_STAT_PUSH    2      /* K3+K4 fused cast/reshard push over NVLink */
+#define PLEX_STAT_D2H     3      /* CE1 bucket copies           */
+#define PLEX_STAT_H2D     4      /* CE2 bucket copies           */
+#define PLEX_STAT_NCCL    5      /* NCCL exchange (sync baseline) */
+#define PLEX_STAT_RPACK   6      /* K4 reshard-pack (NCCL path) */
+#define PLEX_STAT_RUNPACK 7      /* K5 reshard-unpack (NCCL path) */
+#define PLEX_NUM_STATS    8
+
+/* ---- errors / version ---------------------------------------------------- */
+PLEX_API const char* plex_last_error(void);
+PLEX_API const char* plex_version(void);
+
+/* ---- a1 + a2: transition decision and plan (pure host, no CUDA calls) ----- */
+/* Deterministic: identical requests give identical plans on every rank.
+ * Errors: E_INVAL (bad request), E_LAYOUT (non-divisible destination). */
+PLEX_API plex_status plex_transition_plan(const plex_plan_req* req, plex_plan_t* out);
+PLEX_API plex_status plex_plan_destroy(plex_plan_t plan);
+PLEX_API plex_status plex_plan_query(plex_plan_t plan, plex_plan_stats* out);
+PLEX_API plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* out);
+PLEX_API plex_status plex_plan_segment(plex_plan_t plan, int32_t rank, int32_t i, plex_seg_desc* out);
+PLEX_API plex_status plex_plan_dst_tensor(plex_plan_t plan, int32_t rank, int32_t i, plex_dst_desc* out);
+/* FSDP rows [row0, row1) of tensor t held by `rank` (R2; empty when row0 == row1). */
+PLEX_API plex_status plex_plan_shard_rows(plex_plan_t plan, int32_t rank, int32_t t, int64_t* row0, int64_t* row1);
+/* bytes[r * world + g]: bf16 bytes source rank r contributes to rollout rank g
+ * (diagonal = local).  The zero-redundancy ledger of PAPER.md:576. */
+PLEX_API plex_status plex_plan_ledger(plex_plan_t plan, uint64_t* bytes, int32_t n);
+
+/* ---- lifecycle ------------------------------------------------------------ */
+/* 128-byte NCCL unique id for bootstrapping (rank 0 calls it and broadcasts). */
+PLEX_API plex_status plex_nccl_unique_id(void* out128);
+/* device: CUDA ordinal.  staging: caller-owned device buffer of
+ * staging_bytes >= n_slots * bucket_bytes of every plan used with this ctx.
+ * pack_stream / copy_stream: caller-owned cudaStream_t (side streams).
+ * nccl_id: 128 B from plex_nccl_unique_id, or NULL when world == 1 (or for a
+ * ctx used only for single-process per-rank emulation).  Collective over
+ * `world` ranks when nccl_id != NULL. */
+PLEX_API plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, int32_t n_slots,
+                            void* pack_stream, void* copy_stream, const void* nccl_id,
+                            int32_t rank, int32_t world, uint32_t flags, plex_ctx_t* out);
+PLEX_API plex_status plex_ctx_destroy(plex_ctx_t ctx);
+PLEX_API plex_status plex_ctx_stats(plex_ctx_t ctx, int32_t which, plex_kernel_stats* out);
+PLEX_API plex_status plex_ctx_reset_stats(plex_ctx_t ctx);
+
+/* Pinned host slab for `rank`'s state under `plan` (exact size; PAPER.md:574
+ * "the host tier uses pinned memory").  Initial residency: DEVICE.
+ * Errors: E_TIER_FULL if pinning fails. */
+PLEX_API plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, plex_slab_t* out);
+PLEX_API plex_status plex_slab_destroy(plex_slab_t slab);
+/* host_ptr: the slab bytes (read/write, for verification and fault injection) */
+PLEX_API plex_status plex_slab_info(plex_slab_t slab, void** host_ptr, uint64_t* bytes, int32_t* residency);
+/* out[2*i], out[2*i+1] = (S1, S2) of segment i recorded at offload (R14). */
+PLEX_API plex_status plex_slab_checksums(plex_slab_t slab, uint64_t* out, int32_t n);
+
+/* ---- a3 + a4: suspend ----------------------------------------------------- */
+/* src[kind * n_tensors + t] = device pointer of this rank's contiguous shard
+ * of tensor t (kind in the plan's kind_mask and t in its subset; others may
+ * be NULL).  Gather-packs every segment into staging buckets (fused R14
+ * checksums), D2H-copies each bucket into the slab at its canonical offset,
+ * double-buffered on (pack, copy) streams.  Ordered after prior work on
+ * `caller_stream`; returns when the slab holds the canonical bytes (host
+ * blocking).  Residency -> HOST.  Idempotent (no-op) when already HOST. */
+PLEX_API plex_status plex_state_offload(plex_ctx_t ctx, plex_plan_t plan, const void* const* src, int32_t n_src,
+                               plex_slab_t slab, void* caller_stream);
+
+/* ---- a6 + a7: resume ------------------------------------------------------ */
+/* dst: same indexing as offload's src, caller-(re)allocated with the plan's
+ * shard shapes.  H2D-copies buckets and scatter-unpacks them, recomputing
+ * the checksums; returns PLEX_E_CHECKSUM (residency stays HOST) if any
+ * segment differs from what offload recorded.  Residency -> DEVICE.
+ * Idempotent (no-op) when already DEVICE; E_STATE if the slab was never
+ * written. */
+PLEX_API plex_status plex_state_onload(plex_ctx_t ctx, plex_plan_t plan, plex_slab_t slab, void* const* dst,
+                              int32_t n_dst, void* caller_stream);
+
+/* ---- a8 - a11: train -> rollout weight sync ------------------------------- */
+/* Collective over the ctx's world.  src_master[t] = this rank's fp32 master
+ * shard of tensor t (FSDP-world rows).  dst_arena = this rank's bf16 rollout
+ * arena (plan dst_arena_bytes; tensors at plex_plan_dst_tensor offsets).
+ * Writes exactly fuse_g(slice_g(RNE(concat_r shard_r(master)))) (DESIGN.md
+ * c1.3) into every rank's arena: each source rank casts its own rows once per
+ * destination and stores them straight into the destination arena over
+ * NVLink (peer-mapped), so no byte is sent twice. */
+PLEX_API plex_status plex_weight_sync(plex_ctx_t ctx, plex_plan_t plan, const void* const* src_master, int32_t n_src,
+                             void* dst_arena, void* caller_stream);
+/* One source rank's share of the sync into explicitly given destination arenas
+ * (dst_arenas[g], g < world; device pointers valid on ctx's device).  Not
+ * collective, no barriers: used for single-GPU emulation of a W-rank group
+ * and by plex_weight_sync itself.  Ordered on stream, blocking. */
+PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, const void* const* src_master,
+                                  int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream);
+
+/* ---- infrastructure (synthetic inputs / verification; not the method) ---- */
+/* K6: counter-based generator of DESIGN.md §3 (D2) writing `count` elements of
+ * the logical tensor `key` starting at logical flat index `index_base`. */
+PLEX_API plex_status plex_synth_fill(void* dst, int32_t kind, uint64_t seed, const char* key, uint64_t index_base,
+                            uint64_t count, int32_t special_bits, void* stream);
+/* Multiplex "training step": bits ^= mutation(job_seed, step, key, kind, i) (o10). */
+PLEX_API plex_status plex_synth_mutate(void* buf, int32_t kind, uint64_t job_seed, uint64_t step, const char* key,
+                              uint64_t index_base, uint64_t count, void* stream);
+/* K7: accumulate (S1, S2) of R14 over `count` elements of size `esize` (2|4)
+ * into dev_out[0..1] (device, caller zeroes). */
+PLEX_API plex_status plex_checksum(const void* src, int32_t esize, uint64_t index_base, uint64_t count,
+                          uint64_t* dev_out, void* stream);
+/* fp32 -> bf16 RNE of `count` contiguous elements (the a8 cast on its own). */
+PLEX_API plex_status plex_cast_rne(const void* src_f32, void* dst_bf16, uint64_t count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLEX_H */

@@ -1,0 +1,140 @@
+"""ctypes binding of libplex.so (include/plex.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels / copy engines.
+
+Importing this module loads the in-tree ``libplex.so`` and fails loudly if it
+is missing: there is no CPU or PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libplex.so")
+
+OK, E_INVAL, E_LAYOUT, E_TIER_FULL, E_STATE, E_CUDA, E_NCCL, E_CHECKSUM = 0, -1, -2, -3, -4, -5, -6, -7
+KIND_PARAM, KIND_MASTER, KIND_EXP_AVG, KIND_EXP_AVG_SQ = 0, 1, 2, 3
+NUM_KINDS = 4
+KINDMASK_ALL, KINDMASK_OPTIM = 0xF, 0xE
+ROLE_REPLICATED, ROLE_COL, ROLE_ROW, ROLE_EXPERT = 0, 1, 2, 3
+SLAB_KIND_MAJOR, SLAB_KEY_MAJOR = 0, 1
+RANKMAP_TP_FAST, RANKMAP_DP_FAST = 0, 1
+OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
+RES_DEVICE, RES_HOST = 0, 1
+CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
+SLAB_HUGEPAGE = 0x1
+STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK = range(8)
+STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack")
+NUM_STATS = 8
+
+EXPORTS = [
+    "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
+    "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
+    "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
+    "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_checksums",
+    "plex_state_offload", "plex_state_onload", "plex_weight_sync", "plex_weight_sync_rank",
+    "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
+]
+
+
+class PlexError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"plex error {code}: {msg}")
+        self.code = code
+
+
+class TensorDesc(C.Structure):
+    _fields_ = [("key", C.c_char_p), ("d0", C.c_int64), ("d1", C.c_int64), ("ndim", C.c_int32),
+                ("role", C.c_int32), ("group", C.c_int32), ("slot", C.c_int32), ("expert", C.c_int32),
+                ("unit", C.c_int32)]
+
+
+class PlanReq(C.Structure):
+    _fields_ = [("n_tensors", C.c_int32), ("tensors", C.POINTER(TensorDesc)), ("world", C.c_int32),
+                ("tp", C.c_int32), ("dp", C.c_int32), ("ep", C.c_int32), ("rank_map", C.c_int32),
+                ("slab_layout", C.c_int32), ("kind_mask", C.c_uint32), ("n_subset", C.c_int32),
+                ("subset", C.POINTER(C.c_int32)), ("bucket_bytes", C.c_uint64), ("tile_bytes", C.c_uint64),
+                ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32)]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("ops", C.c_int32 * 4), ("op_jobs", C.c_int64 * 4),
+                ("n_tensors", C.c_int32), ("world", C.c_int32), ("tp", C.c_int32), ("dp", C.c_int32),
+                ("ep", C.c_int32), ("total_params", C.c_uint64)]
+
+
+class RankInfo(C.Structure):
+    _fields_ = [("slab_bytes", C.c_uint64), ("payload_bytes", C.c_uint64), ("n_segments", C.c_int32),
+                ("n_buckets", C.c_int32), ("n_pack_items", C.c_uint64), ("dst_arena_bytes", C.c_uint64),
+                ("n_dst_tensors", C.c_int32), ("n_push_items", C.c_uint64), ("send_bytes", C.c_uint64),
+                ("recv_bytes", C.c_uint64), ("local_bytes", C.c_uint64), ("src_read_bytes", C.c_uint64)]
+
+
+class SegDesc(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("kind", C.c_int32), ("slab_offset", C.c_uint64), ("nbytes", C.c_uint64),
+                ("row0", C.c_int64), ("row1", C.c_int64), ("index_base", C.c_uint64)]
+
+
+class DstDesc(C.Structure):
+    _fields_ = [("group", C.c_int32), ("first_tensor", C.c_int32), ("arena_offset", C.c_uint64),
+                ("rows", C.c_int64), ("cols", C.c_int64)]
+
+
+class KernelStats(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    P, VP, I32, U32, U64, I64 = C.POINTER, C.c_void_p, C.c_int32, C.c_uint32, C.c_uint64, C.c_int64
+    sig = {
+        "plex_last_error": (C.c_char_p, []),
+        "plex_version": (C.c_char_p, []),
+        "plex_transition_plan": (C.c_int, [P(PlanReq), P(VP)]),
+        "plex_plan_destroy": (C.c_int, [VP]),
+        "plex_plan_query": (C.c_int, [VP, P(PlanStats)]),
+        "plex_plan_rank_info": (C.c_int, [VP, I32, P(RankInfo)]),
+        "plex_plan_segment": (C.c_int, [VP, I32, I32, P(SegDesc)]),
+        "plex_plan_dst_tensor": (C.c_int, [VP, I32, I32, P(DstDesc)]),
+        "plex_plan_shard_rows": (C.c_int, [VP, I32, I32, P(I64), P(I64)]),
+        "plex_plan_ledger": (C.c_int, [VP, P(U64), I32]),
+        "plex_nccl_unique_id": (C.c_int, [VP]),
+        "plex_ctx_create": (C.c_int, [I32, VP, U64, I32, VP, VP, VP, I32, I32, U32, P(VP)]),
+        "plex_ctx_destroy": (C.c_int, [VP]),
+        "plex_ctx_stats": (C.c_int, [VP, I32, P(KernelStats)]),
+        "plex_ctx_reset_stats": (C.c_int, [VP]),
+        "plex_slab_create": (C.c_int, [VP, I32, U32, P(VP)]),
+        "plex_slab_destroy": (C.c_int, [VP]),
+        "plex_slab_info": (C.c_int, [VP, P(VP), P(U64), P(I32)]),
+        "plex_slab_checksums": (C.c_int, [VP, P(U64), I32]),
+        "plex_state_offload": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
+        "plex_state_onload": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),
+        "plex_weight_sync": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
+        "plex_weight_sync_rank": (C.c_int, [VP, VP, I32, P(VP), I32, P(VP), I32, VP]),
+        "plex_synth_fill": (C.c_int, [VP, I32, U64, C.c_char_p, U64, U64, I32, VP]),
+        "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
+        "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),
+        "plex_cast_rne": (C.c_int, [VP, VP, U64, VP]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(code: int) -> None:
+    if code != OK:
+        raise PlexError(code, lib.plex_last_error().decode(errors="replace"))
+
+
+def ptr_array(ptrs) -> "C.Array":
+    arr = (C.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p or None
+    return arr

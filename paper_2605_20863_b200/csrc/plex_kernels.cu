@@ -1,0 +1,356 @@
+// sm_100a kernels of the state-transition hot path.
+//
+// K1 gather-pack (+R14 checksum)   a3   PAPER.md:462 (migrating model states HBM->host)
+// K2 scatter-unpack (+verify)      a7   PAPER.md:572 (resident and safe to use)
+// K3+K4 fused RNE cast + reshard push over NVLink   a8-a11
+// K6 synthetic init / mutation, K7 checksum, plain cast: infrastructure.
+//
+// Everything here is HBM- (or NVLink-) bound data movement with a few integer
+// ops per element: no tensor cores (nothing is a contraction).  Access is
+// 16-B vectorised (ld.global.nc.L1::no_allocate / st.global.v4), one 256-
+// thread CTA per 64 KiB work item with 4 independent 16-B loads in flight per
+// thread, work items precomputed by the planner so index math stays cheap
+// (DESIGN.md §5).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plex_internal.h"
+
+namespace plex {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// ---- R14 checksum of one 16-B vector whose first element has logical index i0.
+struct Cks {
+    unsigned long long s1 = 0, s2 = 0;
+    __device__ __forceinline__ void add_sum(uint64_t s, uint64_t t, uint64_t i0) {
+        s1 += s;
+        s2 += (i0 + 1) * s + t;
+    }
+    __device__ __forceinline__ void add_vec(const uint4& v, int esize, uint64_t i0) {
+        if (esize == 4) {
+            const uint64_t s = (uint64_t)v.x + v.y + v.z + v.w;
+            const uint64_t t = (uint64_t)v.y + 2ull * v.z + 3ull * v.w;
+            add_sum(s, t, i0);
+        } else {
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            uint32_t s = 0, t = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t lo = w[k] & 0xFFFFu, hi = w[k] >> 16;
+                s += lo + hi;
+                t += (2 * k) * lo + (2 * k + 1) * hi;
+            }
+            add_sum(s, t, i0);
+        }
+    }
+    __device__ __forceinline__ void add_elem(uint32_t b, uint64_t i) {
+        s1 += b;
+        s2 += (i + 1) * (uint64_t)b;
+    }
+};
+
+__device__ __forceinline__ void block_reduce_add(Cks c, unsigned long long* out) {
+    __shared__ unsigned long long sh[2][kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
+        c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sh[0][w] = c.s1; sh[1][w] = c.s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0, b = 0;
+#pragma unroll
+        for (int k = 0; k < kThreads / 32; ++k) { a += sh[0][k]; b += sh[1][k]; }
+        atomicAdd(out, a);
+        atomicAdd(out + 1, b);
+    }
+}
+
+// ---- K1 / K2: pack (tensor -> staging) or unpack (staging -> tensor) -------
+// One CTA per PackItem.  The item covers slab bytes [slab_lo, slab_lo+len) of
+// one segment's slot: data bytes (copied, checksummed) then padding (pack
+// writes zeros; unpack skips it).
+template <bool kPack>
+__global__ void __launch_bounds__(kThreads) pack_kernel(const PackItem* __restrict__ items,
+                                                        const SegDev* __restrict__ segs,
+                                                        const uint64_t* __restrict__ ptrs,
+                                                        uint8_t* __restrict__ staging, uint64_t bucket_lo,
+                                                        unsigned long long* __restrict__ cks) {
+    const PackItem it = items[blockIdx.x];
+    const SegDev s = segs[it.seg];
+    uint8_t* buf = staging + (it.slab_lo - bucket_lo);
+    uint8_t* tens = reinterpret_cast<uint8_t*>(ptrs[s.ptr_slot]);
+    const uint64_t o0 = it.slab_lo - s.slab_off;
+    const uint64_t o1 = o0 + it.len;
+    const uint64_t de = o1 < s.bytes ? o1 : s.bytes;   // end of the data part
+    const int es = (int)s.esize;
+    Cks c;
+    if (o0 < de) {
+        const uint64_t n = de - o0;
+        const uint64_t ib = s.index_base + o0 / es;
+        uint8_t* t = tens + o0;
+        const uint8_t* src = kPack ? t : buf;
+        uint8_t* dst = kPack ? buf : t;
+        const bool vec = ((reinterpret_cast<uintptr_t>(t)) & 15) == 0;
+        const uint64_t nv = vec ? n / 16 : 0;
+        const uint32_t epv = 16 / es;
+        uint64_t v = threadIdx.x;
+        for (; v + 3 * kThreads < nv; v += 4 * kThreads) {
+            uint4 a0 = ld_stream(src + 16 * v);
+            uint4 a1 = ld_stream(src + 16 * (v + kThreads));
+            uint4 a2 = ld_stream(src + 16 * (v + 2 * kThreads));
+            uint4 a3 = ld_stream(src + 16 * (v + 3 * kThreads));
+            st_v4(dst + 16 * v, a0);
+            st_v4(dst + 16 * (v + kThreads), a1);
+            st_v4(dst + 16 * (v + 2 * kThreads), a2);
+            st_v4(dst + 16 * (v + 3 * kThreads), a3);
+            c.add_vec(a0, es, ib + v * epv);
+            c.add_vec(a1, es, ib + (v + kThreads) * epv);
+            c.add_vec(a2, es, ib + (v + 2 * kThreads) * epv);
+            c.add_vec(a3, es, ib + (v + 3 * kThreads) * epv);
+        }
+        for (; v < nv; v += kThreads) {
+            uint4 a = ld_stream(src + 16 * v);
+            st_v4(dst + 16 * v, a);
+            c.add_vec(a, es, ib + v * epv);
+        }
+        // scalar head/tail: whole elements after the vector part
+        const uint64_t ne = n / es;
+        for (uint64_t e = nv * epv + threadIdx.x; e < ne; e += kThreads) {
+            uint32_t b;
+            if (es == 4) {
+                b = reinterpret_cast<const uint32_t*>(src)[e];
+                reinterpret_cast<uint32_t*>(dst)[e] = b;
+            } else {
+                b = reinterpret_cast<const uint16_t*>(src)[e];
+                reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)b;
+            }
+            c.add_elem(b, ib + e);
+        }
+    }
+    if (kPack && de < o1) {   // zero padding (< 256 B)
+        const uint64_t p0 = (o0 > de ? o0 : de) - o0;
+        for (uint64_t b = p0 + threadIdx.x; b < it.len; b += kThreads) buf[b] = 0;
+    }
+    if (o0 < de) block_reduce_add(c, cks + 2 * it.seg);
+}
+
+__global__ void verify_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
+                              uint32_t n, int* __restrict__ bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (got[2 * i] != want[2 * i] || got[2 * i + 1] != want[2 * i + 1]) atomicAdd(bad, 1);
+}
+
+// ---- a8: fp32 -> bf16 round-to-nearest-even (R8), integer bit math ---------
+// r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16; any NaN -> 0x7FC0.  Subnormals are
+// rounded like any other value (no flush); overflow rounds to +-inf.
+__device__ __forceinline__ uint32_t rne_bf16(uint32_t u) {
+    const uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+    return ((u & 0x7FFFFFFFu) > 0x7F800000u) ? 0x7FC0u : r;
+}
+__device__ __forceinline__ uint32_t rne_pack2(uint32_t lo, uint32_t hi) {
+    return rne_bf16(lo) | (rne_bf16(hi) << 16);
+}
+__device__ __forceinline__ uint4 rne_8(const uint4& a, const uint4& b) {
+    return make_uint4(rne_pack2(a.x, a.y), rne_pack2(a.z, a.w), rne_pack2(b.x, b.y), rne_pack2(b.z, b.w));
+}
+
+// ---- K3+K4: fused cast + reshard push ---------------------------------------
+// One CTA per PushItem: rows x cols fp32 rectangle of this rank's master shard
+// -> RNE -> bf16 rectangle of destination rank dst_rank's arena, which is a
+// peer-mapped pointer (NVLink store) unless dst_rank is this rank.
+__global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restrict__ items,
+                                                        const uint64_t* __restrict__ src_ptrs,
+                                                        const uint64_t* __restrict__ dst_arenas) {
+    const PushItem it = items[blockIdx.x];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(src_ptrs[it.tensor]) + it.src_elem;
+    uint16_t* dst = reinterpret_cast<uint16_t*>(dst_arenas[it.dst_rank]) + it.dst_elem;
+    const uint32_t rows = it.rows, cols = it.cols, ss = it.src_stride, ds = it.dst_stride;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
+                     (cols % 8 == 0) && (ss % 4 == 0) && (ds % 8 == 0);
+    if (vec) {
+        const uint32_t vpr = cols / 8;
+        const uint32_t total = rows * vpr;
+        if (rows == 1) {
+            uint32_t v = threadIdx.x;
+            for (; v + kThreads < total; v += 2 * kThreads) {
+                const uint4 a0 = ld_stream(src + 8 * v), b0 = ld_stream(src + 8 * v + 4);
+                const uint4 a1 = ld_stream(src + 8 * (v + kThreads)), b1 = ld_stream(src + 8 * (v + kThreads) + 4);
+                st_v4(dst + 8 * v, rne_8(a0, b0));
+                st_v4(dst + 8 * (v + kThreads), rne_8(a1, b1));
+            }
+            for (; v < total; v += kThreads) {
+                const uint4 a = ld_stream(src + 8 * v), b = ld_stream(src + 8 * v + 4);
+                st_v4(dst + 8 * v, rne_8(a, b));
+            }
+        } else {
+            for (uint32_t v = threadIdx.x; v < total; v += kThreads) {
+                const uint32_t r = v / vpr, c = v - r * vpr;
+                const uint32_t* s = src + (uint64_t)r * ss + 8 * c;
+                const uint4 a = ld_stream(s), b = ld_stream(s + 4);
+                st_v4(dst + (uint64_t)r * ds + 8 * c, rne_8(a, b));
+            }
+        }
+    } else {
+        const uint64_t total = (uint64_t)rows * cols;
+        for (uint64_t e = threadIdx.x; e < total; e += kThreads) {
+            const uint64_t r = e / cols, c = e - r * cols;
+            dst[r * ds + c] = (uint16_t)rne_bf16(src[r * ss + c]);
+        }
+    }
+}
+
+__global__ void cast_kernel(const uint32_t* __restrict__ src, uint16_t* __restrict__ dst, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t nv = n / 8;
+        for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += stride)
+            st_v4(dst + 8 * v, rne_8(ld_stream(src + 8 * v), ld_stream(src + 8 * v + 4)));
+        done = nv * 8;
+    }
+    for (uint64_t e = done + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += stride)
+        dst[e] = (uint16_t)rne_bf16(src[e]);
+}
+
+// ---- K6: counter-based synthetic generator (D2) ---------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__constant__ uint32_t c_specials[16] = {
+    0x00000000u, 0x80000000u, 0x00000001u, 0x00018000u, 0x007FFFFFu, 0x3F808000u, 0x3F818000u, 0x3F808001u,
+    0x3F807FFFu, 0x7F7FFFFFu, 0x7F7F8000u, 0x7F800000u, 0xFF800000u, 0x7FC00000u, 0x7F800001u, 0xFFC12345u};
+
+__global__ void synth_kernel(void* __restrict__ dst, int kind, uint64_t base, uint64_t index_base, uint64_t n,
+                             int special_bits) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t smask = special_bits > 0 ? ((1ull << special_bits) - 1) : 0;
+    const uint32_t lo = kind == 1 ? 0x76u : kind == 2 ? 0x68u : 0x58u;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t z = splitmix64(base ^ (index_base + i));
+        if (kind == 0) {
+            const uint32_t b = (uint32_t)(z >> 63) << 15 | (0x76u + (uint32_t)((z >> 32) & 7)) << 7 |
+                               (uint32_t)((z >> 8) & 0x7F);
+            reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)b;
+        } else {
+            const uint32_t sign = kind == 3 ? 0u : (uint32_t)(z >> 63);
+            uint32_t b = sign << 31 | (lo + (uint32_t)((z >> 32) & 7)) << 23 | (uint32_t)((z >> 8) & 0x7FFFFF);
+            if (special_bits > 0 && (z & smask) == 0) b = c_specials[(z >> 20) & 15];
+            reinterpret_cast<uint32_t*>(dst)[i] = b;
+        }
+    }
+}
+
+__global__ void mutate_kernel(void* __restrict__ buf, int esize, uint64_t base, uint64_t index_base, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t m = (uint32_t)(splitmix64(base ^ (index_base + i)) & 0xFF);
+        if (esize == 4) reinterpret_cast<uint32_t*>(buf)[i] ^= m;
+        else reinterpret_cast<uint16_t*>(buf)[i] ^= (uint16_t)m;
+    }
+}
+
+// ---- K7: checksum of an arbitrary contiguous tensor -------------------------
+__global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __restrict__ src, int es,
+                                                            uint64_t index_base, uint64_t n_elems,
+                                                            unsigned long long* __restrict__ out) {
+    Cks c;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const uint32_t epv = 16 / es;
+    const uint64_t nv = vec ? n_elems / epv : 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)kThreads + threadIdx.x; v < nv; v += stride)
+        c.add_vec(ld_stream(src + 16 * v), es, index_base + v * epv);
+    for (uint64_t e = nv * epv + blockIdx.x * (uint64_t)kThreads + threadIdx.x; e < n_elems; e += stride) {
+        const uint32_t b = es == 4 ? reinterpret_cast<const uint32_t*>(src)[e] : reinterpret_cast<const uint16_t*>(src)[e];
+        c.add_elem(b, index_base + e);
+    }
+    block_reduce_add(c, out);
+}
+
+// ---- launchers ----------------------------------------------------------------
+cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
+    if (n_items == 0) return cudaSuccess;
+    if (pack) pack_kernel<true><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, staging, bucket_lo, cks);
+    else pack_kernel<false><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, staging, bucket_lo, cks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
+                          cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint32_t blocks = (n + kThreads - 1) / kThreads;
+    verify_kernel<<<blocks < 1024 ? blocks : 1024, kThreads, 0, s>>>(got, want, n, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_push(const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs, const uint64_t* dst_arenas,
+                        cudaStream_t s) {
+    // grid.x limit is 2^31-1; chunk very long item lists
+    const uint64_t kMax = 1ull << 30;
+    for (uint64_t o = 0; o < n_items; o += kMax) {
+        const uint64_t n = n_items - o < kMax ? n_items - o : kMax;
+        push_kernel<<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
+    }
+    return cudaGetLastError();
+}
+
+static inline uint32_t grid_for(uint64_t work, uint32_t per_block) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    const uint64_t cap = 148ull * 16;
+    if (b > cap) b = cap;
+    return b ? (uint32_t)b : 1u;
+}
+
+cudaError_t launch_cast(const void* src, void* dst, uint64_t n, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    cast_kernel<<<grid_for(n / 8 + 1, kThreads), kThreads, 0, s>>>(reinterpret_cast<const uint32_t*>(src),
+                                                                     reinterpret_cast<uint16_t*>(dst), n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_synth(void* dst, int kind, uint64_t base, uint64_t index_base, uint64_t n, int special_bits,
+                         cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    synth_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(dst, kind, base, index_base, n, special_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mutate(void* buf, int esize, uint64_t base, uint64_t index_base, uint64_t n, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    mutate_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(buf, esize, base, index_base, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_checksum(const void* src, int es, uint64_t index_base, uint64_t n, unsigned long long* out,
+                            cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    checksum_kernel<<<grid_for(n / (16 / es) + 1, kThreads), kThreads, 0, s>>>(
+        reinterpret_cast<const uint8_t*>(src), es, index_base, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace plex

@@ -1,0 +1,420 @@
+// a1 + a2: transition decision and plan (pure host; no CUDA calls).
+//
+// a1 — PAPER.md:555 (§5.2.2 "Automatic Context Switching"): if the incoming
+//      operation's job differs from the resident one, prepend offload(resident)
+//      and load(incoming).
+// a2 — canonical manifest ("indexing offloaded tensors by logical
+//      keys") -> per-rank slab segments (R4), bucket/work-item tables (R5),
+//      rollout destination tensors (R3) and the zero-redundancy
+//      push ledger.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+
+#include "plex_internal.h"
+
+namespace plex {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+static std::atomic<uint64_t> g_plan_ids{1};
+
+// R2: FSDP-N dim-0 chunk of rank r: rows [min(d0, r*c), min(d0, (r+1)*c)).
+static inline void fsdp_rows(int64_t d0, int32_t world, int32_t r, int64_t* a, int64_t* b) {
+    int64_t c = (d0 + world - 1) / world;
+    *a = std::min<int64_t>(d0, (int64_t)r * c);
+    *b = std::min<int64_t>(d0, (int64_t)(r + 1) * c);
+}
+
+// R10 rank map -> (tp rank, dp rank).
+static inline void coords(const Plan& p, int32_t g, int32_t* t, int32_t* d) {
+    if (p.rank_map == PLEX_RANKMAP_TP_FAST) { *t = g % p.tp; *d = g / p.tp; }
+    else { *t = g / p.dp; *d = g % p.dp; }
+}
+
+static plex_status build_slab(Plan& p, int32_t r) {
+    RankPlan& R = p.ranks[r];
+    const int32_t nt = (int32_t)p.tensors.size();
+    std::vector<int> kinds;
+    for (int k = 0; k < PLEX_NUM_KINDS; ++k)
+        if (p.kind_mask & (1u << k)) kinds.push_back(k);
+    std::vector<std::pair<int, int32_t>> order;   // (kind, tensor)
+    if (p.layout == PLEX_SLAB_KIND_MAJOR) {
+        for (int k : kinds) for (int32_t t : p.subset) order.emplace_back(k, t);
+    } else {
+        for (int32_t t : p.subset) for (int k : kinds) order.emplace_back(k, t);
+    }
+    uint64_t cur = 0;
+    for (auto& kt : order) {
+        const Tensor& T = p.tensors[kt.second];
+        int64_t a, b;
+        fsdp_rows(T.d0, p.world, r, &a, &b);
+        const int es = kind_esize(kt.first);
+        SegDev s{};
+        s.slab_off = align_up(cur, kSegAlign);
+        s.bytes = (uint64_t)(b - a) * (uint64_t)T.d1 * es;
+        s.index_base = (uint64_t)a * (uint64_t)T.d1;
+        s.ptr_slot = (uint32_t)(kt.first * nt + kt.second);
+        s.esize = (uint32_t)es;
+        R.segs.push_back(s);
+        plex_seg_desc d{};
+        d.tensor = kt.second; d.kind = kt.first; d.slab_offset = s.slab_off; d.nbytes = s.bytes;
+        d.row0 = a; d.row1 = b; d.index_base = s.index_base;
+        R.seg_desc.push_back(d);
+        R.payload_bytes += s.bytes;
+        cur = s.slab_off + s.bytes;
+    }
+    R.slab_bytes = align_up(cur, kSegAlign);
+    // Work items: each segment's slot [off, off + align(bytes)) split at bucket
+    // and tile boundaries.  Slots tile the slab exactly (R4), so every slab
+    // byte belongs to exactly one item.
+    const uint64_t B = p.bucket, TL = p.tile;
+    for (uint32_t si = 0; si < R.segs.size(); ++si) {
+        const SegDev& s = R.segs[si];
+        uint64_t lo = s.slab_off, hi = s.slab_off + align_up(s.bytes, kSegAlign);
+        while (lo < hi) {
+            uint64_t cut = std::min(hi, std::min((lo / B + 1) * B, lo + TL));
+            R.items.push_back(PackItem{lo, (uint32_t)(cut - lo), si});
+            lo = cut;
+        }
+    }
+    const int32_t nb = n_buckets(p, R);
+    R.bucket_item_start.assign(nb + 1, R.items.size());
+    size_t it = 0;
+    for (int32_t b = 0; b < nb; ++b) {
+        while (it < R.items.size() && R.items[it].slab_lo < (uint64_t)b * B) ++it;
+        R.bucket_item_start[b] = it;
+    }
+    R.bucket_item_start[nb] = R.items.size();
+    return PLEX_OK;
+}
+
+// R3 destination tensors of rollout rank g.
+static plex_status build_dst(Plan& p, int32_t g, const std::vector<int32_t>& group_order,
+                             const std::map<int32_t, std::vector<int32_t>>& members,
+                             const std::map<int32_t, int32_t>& n_experts) {
+    RankPlan& R = p.ranks[g];
+    int32_t t, d;
+    coords(p, g, &t, &d);
+    const int32_t epr = g % p.ep;
+    uint64_t cur = 0;
+    for (int32_t grp : group_order) {
+        const auto& mem = members.at(grp);
+        const Tensor& T0 = p.tensors[mem[0]];
+        DstTensor D{};
+        D.group = grp;
+        D.first_tensor = mem[0];
+        D.rows = 0;
+        D.cols = -1;
+        for (int32_t ti : mem) {
+            const Tensor& T = p.tensors[ti];
+            if (T.role != T0.role) { set_error("group %d mixes roles", grp); return PLEX_E_INVAL; }
+            Piece pc{ti, 0, T.d0, 0, T.d1, D.rows};
+            switch (T.role) {
+                case PLEX_ROLE_REPLICATED: break;
+                case PLEX_ROLE_COL: {
+                    const int64_t unit = std::max<int32_t>(1, T.unit);
+                    if (T.d0 % (p.tp * unit)) {
+                        set_error("%s: %lld rows not divisible by TP %d x unit %lld", T.key.c_str(),
+                                  (long long)T.d0, p.tp, (long long)unit);
+                        return PLEX_E_LAYOUT;
+                    }
+                    const int64_t n = T.d0 / p.tp;
+                    pc.r0 = t * n; pc.r1 = (t + 1) * n;
+                    break;
+                }
+                case PLEX_ROLE_ROW: {
+                    if (T.d1 % p.tp) {
+                        set_error("%s: %lld cols not divisible by TP %d", T.key.c_str(), (long long)T.d1, p.tp);
+                        return PLEX_E_LAYOUT;
+                    }
+                    if (mem.size() != 1) { set_error("row-parallel group %d has %zu members", grp, mem.size()); return PLEX_E_INVAL; }
+                    const int64_t n = T.d1 / p.tp;
+                    pc.c0 = t * n; pc.c1 = (t + 1) * n;
+                    break;
+                }
+                case PLEX_ROLE_EXPERT: {
+                    const int32_t E = n_experts.at(grp);
+                    if (E % p.ep) {
+                        set_error("%s: %d experts not divisible by EP %d", T.key.c_str(), E, p.ep);
+                        return PLEX_E_LAYOUT;
+                    }
+                    const int32_t per = E / p.ep;
+                    if (T.expert / per != epr) continue;      // not on this EP rank
+                    break;
+                }
+                default: set_error("bad role %d", T.role); return PLEX_E_INVAL;
+            }
+            const int64_t w = pc.c1 - pc.c0;
+            if (D.cols >= 0 && D.cols != w) {
+                set_error("group %d: fused pieces have different widths (%lld vs %lld)", grp,
+                          (long long)D.cols, (long long)w);
+                return PLEX_E_INVAL;
+            }
+            D.cols = w;
+            D.rows += pc.r1 - pc.r0;
+            D.pieces.push_back(pc);
+        }
+        if (D.pieces.empty()) continue;
+        D.arena_off = align_up(cur, kSegAlign);
+        cur = D.arena_off + (uint64_t)D.rows * (uint64_t)D.cols * 2;
+        R.dst.push_back(std::move(D));
+    }
+    R.arena_bytes = align_up(cur, kSegAlign);
+    return PLEX_OK;
+}
+
+static void emit_push(Plan& p, std::vector<std::vector<std::vector<PushItem>>>& per_src_dst, int32_t g) {
+    const RankPlan& G = p.ranks[g];
+    const uint64_t tile_elems = std::max<uint64_t>(8, p.tile / 4);
+    for (const DstTensor& D : G.dst) {
+        for (const Piece& pc : D.pieces) {
+            const Tensor& T = p.tensors[pc.tensor];
+            for (int32_t r = 0; r < p.world; ++r) {
+                int64_t a, b;
+                fsdp_rows(T.d0, p.world, r, &a, &b);
+                const int64_t lo = std::max(a, pc.r0), hi = std::min(b, pc.r1);
+                if (hi <= lo) continue;
+                const uint64_t w = (uint64_t)(pc.c1 - pc.c0);
+                const uint64_t rows = (uint64_t)(hi - lo);
+                const uint64_t src0 = (uint64_t)(lo - a) * T.d1 + pc.c0;             // in r's shard
+                const uint64_t dst0 = D.arena_off / 2 + (uint64_t)(pc.dst_row0 + lo - pc.r0) * D.cols;
+                const uint64_t bytes = rows * w * 2;
+                p.ledger[(size_t)r * p.world + g] += bytes;
+                auto& out = per_src_dst[r][g];
+                if (w == (uint64_t)T.d1 && w == (uint64_t)D.cols) {
+                    // contiguous run of rows*w elements on both sides
+                    const uint64_t n = rows * w;
+                    for (uint64_t o = 0; o < n; o += tile_elems) {
+                        const uint64_t c = std::min(tile_elems, n - o);
+                        out.push_back(PushItem{src0 + o, dst0 + o, (uint32_t)pc.tensor, (uint32_t)g, 1,
+                                               (uint32_t)c, (uint32_t)c, (uint32_t)c});
+                    }
+                } else {
+                    const uint64_t rpi = std::max<uint64_t>(1, tile_elems / std::max<uint64_t>(1, w));
+                    for (uint64_t o = 0; o < rows; o += rpi) {
+                        const uint64_t c = std::min(rpi, rows - o);
+                        out.push_back(PushItem{src0 + o * T.d1, dst0 + o * D.cols, (uint32_t)pc.tensor, (uint32_t)g,
+                                               (uint32_t)c, (uint32_t)w, (uint32_t)T.d1, (uint32_t)D.cols});
+                    }
+                }
+            }
+        }
+    }
+}
+
+static plex_status build(const plex_plan_req* q, Plan& p) {
+    if (!q || q->n_tensors <= 0 || !q->tensors) { set_error("empty manifest"); return PLEX_E_INVAL; }
+    if (q->world < 1) { set_error("world must be >= 1"); return PLEX_E_INVAL; }
+    p.world = q->world;
+    p.tp = q->tp; p.dp = q->dp; p.ep = q->ep > 0 ? q->ep : 1;
+    p.rank_map = q->rank_map;
+    p.layout = q->slab_layout;
+    p.kind_mask = q->kind_mask ? q->kind_mask : PLEX_KINDMASK_ALL;
+    p.bucket = q->bucket_bytes ? q->bucket_bytes : kDefaultBucket;
+    p.tile = q->tile_bytes ? q->tile_bytes : kDefaultTile;
+    if (p.bucket % kSegAlign || p.tile % kSegAlign || p.tile > (1ull << 31)) {
+        set_error("bucket/tile must be multiples of 256 B (tile < 2 GiB)"); return PLEX_E_INVAL;
+    }
+    if (p.kind_mask & ~PLEX_KINDMASK_ALL) { set_error("bad kind mask"); return PLEX_E_INVAL; }
+    if (p.layout != PLEX_SLAB_KIND_MAJOR && p.layout != PLEX_SLAB_KEY_MAJOR) { set_error("bad slab layout"); return PLEX_E_INVAL; }
+    if (p.rank_map != PLEX_RANKMAP_TP_FAST && p.rank_map != PLEX_RANKMAP_DP_FAST) { set_error("bad rank map"); return PLEX_E_INVAL; }
+    const bool sync = !(p.tp == 0 && p.dp == 0);
+    if (sync && (p.tp < 1 || p.dp < 1 || p.tp * p.dp != p.world)) {
+        set_error("tp*dp (%d*%d) must equal world %d", p.tp, p.dp, p.world); return PLEX_E_INVAL;
+    }
+    if (sync && p.world % p.ep) { set_error("EP %d must divide world %d", p.ep, p.world); return PLEX_E_LAYOUT; }
+    p.tensors.reserve(q->n_tensors);
+    uint64_t total = 0;
+    for (int32_t i = 0; i < q->n_tensors; ++i) {
+        const plex_tensor_desc& d = q->tensors[i];
+        if (d.d0 < 0 || d.d1 < 1 || (d.ndim != 1 && d.ndim != 2) || (d.ndim == 1 && d.d1 != 1)) {
+            set_error("tensor %d: bad shape", i); return PLEX_E_INVAL;
+        }
+        if (d.d1 > 0x7FFFFFFF || d.d0 > 0x7FFFFFFF) { set_error("tensor %d: dim too large", i); return PLEX_E_INVAL; }
+        if (d.role < 0 || d.role > PLEX_ROLE_EXPERT) { set_error("tensor %d: bad role", i); return PLEX_E_INVAL; }
+        if (d.role == PLEX_ROLE_EXPERT && d.expert < 0) { set_error("tensor %d: expert index", i); return PLEX_E_INVAL; }
+        p.tensors.push_back(Tensor{d.key ? d.key : "", d.d0, d.d1, d.ndim, d.role, d.group, d.slot, d.expert, d.unit});
+        total += (uint64_t)d.d0 * (uint64_t)d.d1;
+    }
+    if (q->n_subset > 0 && q->subset) {
+        p.subset.assign(q->subset, q->subset + q->n_subset);
+        std::sort(p.subset.begin(), p.subset.end());
+        p.subset.erase(std::unique(p.subset.begin(), p.subset.end()), p.subset.end());
+        for (int32_t t : p.subset)
+            if (t < 0 || t >= q->n_tensors) { set_error("subset index %d out of range", t); return PLEX_E_INVAL; }
+    } else {
+        p.subset.resize(q->n_tensors);
+        for (int32_t i = 0; i < q->n_tensors; ++i) p.subset[i] = i;
+    }
+    // a1: transition ops.
+    plex_plan_stats& st = p.stats;
+    st.n_ops = 0;
+    auto add_op = [&](int32_t op, int64_t job) { st.ops[st.n_ops] = op; st.op_jobs[st.n_ops] = job; ++st.n_ops; };
+    if (q->resident_job != q->incoming_job) {
+        if (q->resident_job >= 0) add_op(PLEX_OP_OFFLOAD, q->resident_job);
+        if (q->incoming_job >= 0) add_op(PLEX_OP_ONLOAD, q->incoming_job);
+    }
+    if (q->op == PLEX_OP_SYNC) add_op(PLEX_OP_SYNC, q->incoming_job);
+    st.n_tensors = q->n_tensors;
+    st.world = p.world; st.tp = p.tp; st.dp = p.dp; st.ep = p.ep;
+    st.total_params = total;
+
+    p.ranks.resize(p.world);
+    for (int32_t r = 0; r < p.world; ++r) {
+        plex_status s = build_slab(p, r);
+        if (s) return s;
+    }
+    p.ledger.assign((size_t)p.world * p.world, 0);
+    if (sync) {
+        std::vector<int32_t> order;
+        std::map<int32_t, std::vector<int32_t>> members;
+        std::map<int32_t, int32_t> n_experts;
+        for (int32_t i = 0; i < q->n_tensors; ++i) {
+            const Tensor& T = p.tensors[i];
+            if (!members.count(T.group)) order.push_back(T.group);
+            members[T.group].push_back(i);
+            if (T.role == PLEX_ROLE_EXPERT) n_experts[T.group] = std::max(n_experts[T.group], T.expert + 1);
+        }
+        for (auto& kv : members)
+            std::stable_sort(kv.second.begin(), kv.second.end(),
+                             [&](int32_t a, int32_t b) { return p.tensors[a].slot < p.tensors[b].slot; });
+        for (int32_t g = 0; g < p.world; ++g) {
+            plex_status s = build_dst(p, g, order, members, n_experts);
+            if (s) return s;
+        }
+        std::vector<std::vector<std::vector<PushItem>>> per(p.world, std::vector<std::vector<PushItem>>(p.world));
+        for (int32_t g = 0; g < p.world; ++g) emit_push(p, per, g);
+        // Interleave each source's items round-robin over destinations starting
+        // at r+1 so that, at any moment, every sender spreads its NVLink stores
+        // over all peers instead of all senders converging on one receiver.
+        for (int32_t r = 0; r < p.world; ++r) {
+            RankPlan& R = p.ranks[r];
+            std::vector<size_t> pos(p.world, 0);
+            size_t left = 0;
+            for (int32_t g = 0; g < p.world; ++g) left += per[r][g].size();
+            R.push.reserve(left);
+            while (left) {
+                for (int32_t k = 1; k <= p.world; ++k) {
+                    const int32_t g = (r + k) % p.world;
+                    if (pos[g] < per[r][g].size()) { R.push.push_back(per[r][g][pos[g]++]); --left; }
+                }
+            }
+            for (const PushItem& it : R.push) R.src_read_bytes += (uint64_t)it.rows * it.cols * 4;
+        }
+        for (int32_t r = 0; r < p.world; ++r)
+            for (int32_t g = 0; g < p.world; ++g) {
+                const uint64_t b = p.ledger[(size_t)r * p.world + g];
+                if (r == g) p.ranks[r].local_bytes += b;
+                else { p.ranks[r].send_bytes += b; p.ranks[g].recv_bytes += b; }
+            }
+    }
+    p.id = g_plan_ids.fetch_add(1);
+    return PLEX_OK;
+}
+
+}  // namespace plex
+
+using namespace plex;
+
+extern "C" {
+
+const char* plex_last_error(void) { return plex::g_err; }
+const char* plex_version(void) { return "plex-b200 0.1 (sm_100a)"; }
+
+plex_status plex_transition_plan(const plex_plan_req* req, plex_plan_t* out) {
+    if (!out) { set_error("out is NULL"); return PLEX_E_INVAL; }
+    *out = nullptr;
+    try {
+        auto* h = new plex_plan_s();
+        plex_status s = build(req, h->p);
+        if (s) { delete h; return s; }
+        *out = h;
+        return PLEX_OK;
+    } catch (const std::bad_alloc&) {
+        set_error("out of host memory building plan");
+        return PLEX_E_INVAL;
+    } catch (...) {
+        set_error("unexpected exception building plan");
+        return PLEX_E_INVAL;
+    }
+}
+
+plex_status plex_plan_query(plex_plan_t plan, plex_plan_stats* out) {
+    if (!plan || !out) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    *out = plan->p.stats;
+    return PLEX_OK;
+}
+
+plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* out) {
+    if (!plan || !out || rank < 0 || rank >= plan->p.world) { set_error("bad plan/rank"); return PLEX_E_INVAL; }
+    const Plan& p = plan->p;
+    const RankPlan& R = p.ranks[rank];
+    plex_rank_info o{};
+    o.slab_bytes = R.slab_bytes;
+    o.payload_bytes = R.payload_bytes;
+    o.n_segments = (int32_t)R.segs.size();
+    o.n_buckets = n_buckets(p, R);
+    o.n_pack_items = R.items.size();
+    o.dst_arena_bytes = R.arena_bytes;
+    o.n_dst_tensors = (int32_t)R.dst.size();
+    o.n_push_items = R.push.size();
+    o.send_bytes = R.send_bytes;
+    o.recv_bytes = R.recv_bytes;
+    o.local_bytes = R.local_bytes;
+    o.src_read_bytes = R.src_read_bytes;
+    *out = o;
+    return PLEX_OK;
+}
+
+plex_status plex_plan_segment(plex_plan_t plan, int32_t rank, int32_t i, plex_seg_desc* out) {
+    if (!plan || !out || rank < 0 || rank >= plan->p.world) { set_error("bad plan/rank"); return PLEX_E_INVAL; }
+    const RankPlan& R = plan->p.ranks[rank];
+    if (i < 0 || i >= (int32_t)R.seg_desc.size()) { set_error("segment %d out of range", i); return PLEX_E_INVAL; }
+    *out = R.seg_desc[i];
+    return PLEX_OK;
+}
+
+plex_status plex_plan_dst_tensor(plex_plan_t plan, int32_t rank, int32_t i, plex_dst_desc* out) {
+    if (!plan || !out || rank < 0 || rank >= plan->p.world) { set_error("bad plan/rank"); return PLEX_E_INVAL; }
+    const RankPlan& R = plan->p.ranks[rank];
+    if (i < 0 || i >= (int32_t)R.dst.size()) { set_error("dst tensor %d out of range", i); return PLEX_E_INVAL; }
+    const DstTensor& D = R.dst[i];
+    out->group = D.group;
+    out->first_tensor = D.first_tensor;
+    out->arena_offset = D.arena_off;
+    out->rows = D.rows;
+    out->cols = D.cols;
+    return PLEX_OK;
+}
+
+plex_status plex_plan_shard_rows(plex_plan_t plan, int32_t rank, int32_t t, int64_t* row0, int64_t* row1) {
+    if (!plan || !row0 || !row1 || rank < 0 || rank >= plan->p.world || t < 0 ||
+        t >= (int32_t)plan->p.tensors.size()) {
+        set_error("bad shard query");
+        return PLEX_E_INVAL;
+    }
+    fsdp_rows(plan->p.tensors[t].d0, plan->p.world, rank, row0, row1);
+    return PLEX_OK;
+}
+
+plex_status plex_plan_ledger(plex_plan_t plan, uint64_t* bytes, int32_t n) {
+    if (!plan || !bytes) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    const Plan& p = plan->p;
+    if (n != p.world * p.world) { set_error("ledger needs world*world = %d entries", p.world * p.world); return PLEX_E_INVAL; }
+    std::memcpy(bytes, p.ledger.data(), sizeof(uint64_t) * p.ledger.size());
+    return PLEX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,751 @@
+// libplex runtime: context, pinned slabs, the suspend/resume bucket pipeline
+// and the train->rollout weight sync (fused NVLink push, or the NCCL baseline).
+//
+// Blocking contract (§5.3): every state-transfer call orders
+// itself after prior work on the caller's stream, runs on the ctx's side
+// streams, and returns only when the transfer has completed, with the caller
+// stream made to wait on it ("resident and safe to use on the default CUDA
+// stream").
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <vector>
+
+#include "plex_internal.h"
+
+namespace plex {
+
+cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s);
+cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
+                          cudaStream_t s);
+cudaError_t launch_push(const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs, const uint64_t* dst_arenas,
+                        cudaStream_t s);
+cudaError_t launch_cast(const void* src, void* dst, uint64_t n, cudaStream_t s);
+cudaError_t launch_synth(void* dst, int kind, uint64_t base, uint64_t index_base, uint64_t n, int special_bits,
+                         cudaStream_t s);
+cudaError_t launch_mutate(void* buf, int esize, uint64_t base, uint64_t index_base, uint64_t n, cudaStream_t s);
+cudaError_t launch_checksum(const void* src, int es, uint64_t index_base, uint64_t n, unsigned long long* out,
+                            cudaStream_t s);
+// NCCL-baseline sync kernels (plex_nccl_sync.cu)
+plex_status nccl_sync(plex_ctx_s* ctx, const Plan& p, const void* const* src, void* arena, cudaStream_t caller);
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) {                                                               \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));         \
+            return PLEX_E_CUDA;                                                                \
+        }                                                                                      \
+    } while (0)
+#define NK(x)                                                                                  \
+    do {                                                                                       \
+        ncclResult_t r_ = (x);                                                                 \
+        if (r_ != ncclSuccess) {                                                               \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #x, ncclGetErrorString(r_));         \
+            return PLEX_E_NCCL;                                                                \
+        }                                                                                      \
+    } while (0)
+
+// Device-side copy of one rank's share of a plan (built lazily per ctx).
+struct DevPlan {
+    SegDev* segs = nullptr;
+    PackItem* items = nullptr;
+    PushItem* push = nullptr;
+    unsigned long long* cks = nullptr;        // computed (S1,S2) per segment
+    unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
+    std::vector<uint64_t> bucket_payload;     // data bytes per bucket (stats)
+};
+
+struct Timed {
+    int which;
+    uint64_t bytes;
+    cudaEvent_t a, b;
+};
+
+}  // namespace plex
+
+using namespace plex;
+
+struct plex_ctx_s {
+    int device = 0;
+    uint8_t* staging = nullptr;
+    uint64_t staging_bytes = 0;
+    int n_slots = 2;
+    cudaStream_t pack = nullptr, copy = nullptr;
+    int rank = 0, world = 1;
+    uint32_t flags = 0;
+    ncclComm_t comm = nullptr;
+    // events
+    cudaEvent_t ev_caller = nullptr, ev_pack_done = nullptr, ev_copy_done = nullptr;
+    std::vector<cudaEvent_t> ev_pack, ev_copy;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    std::vector<Timed> pending;
+    plex_kernel_stats stats[PLEX_NUM_STATS] = {};
+    // pointer tables (pinned host mirror -> device)
+    uint64_t* h_ptrs = nullptr;
+    uint64_t* d_ptrs = nullptr;
+    size_t ptr_cap = 0;
+    int* h_flag = nullptr;
+    int* d_flag = nullptr;
+    // small device scratch for NCCL barriers and handle exchange
+    uint8_t* d_scratch = nullptr;
+    uint8_t* h_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // peer arenas opened over CUDA IPC: rank -> (handle bytes, mapped base)
+    std::map<int, std::pair<std::vector<uint8_t>, void*>> peers;
+    std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
+    // NCCL-baseline staging views (send | recv halves of `staging`)
+};
+
+struct plex_slab_s {
+    uint64_t plan_id = 0;
+    int rank = 0;
+    uint64_t bytes = 0;
+    uint8_t* host = nullptr;
+    bool registered = false;   // mmap + cudaHostRegister path
+    size_t map_bytes = 0;
+    int residency = PLEX_RES_DEVICE;
+    bool written = false;
+    std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
+};
+
+namespace plex {
+
+static std::mutex g_ctx_mu;
+static std::set<plex_ctx_s*> g_ctxs;
+
+static void free_devplan(DevPlan& d) {
+    cudaFree(d.segs);
+    cudaFree(d.items);
+    cudaFree(d.push);
+    cudaFree(d.cks);
+    cudaFree(d.cks_want);
+    d = DevPlan{};
+}
+
+template <class T>
+static plex_status upload(T** dptr, const std::vector<T>& v) {
+    *dptr = nullptr;
+    if (v.empty()) return PLEX_OK;
+    CK(cudaMalloc(dptr, sizeof(T) * v.size()));
+    CK(cudaMemcpy(*dptr, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return PLEX_OK;
+}
+
+static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
+    auto it = c->dev.find(p.id);
+    if (it != c->dev.end()) { *out = &it->second; return PLEX_OK; }
+    const RankPlan& R = p.ranks[c->rank];
+    DevPlan d;
+    plex_status s;
+    if ((s = upload(&d.segs, R.segs)) || (s = upload(&d.items, R.items)) || (s = upload(&d.push, R.push))) {
+        free_devplan(d);
+        return s;
+    }
+    const size_t nck = std::max<size_t>(1, 2 * R.segs.size());
+    if (cudaMalloc(&d.cks, nck * 8) != cudaSuccess || cudaMalloc(&d.cks_want, nck * 8) != cudaSuccess) {
+        free_devplan(d);
+        set_error("cudaMalloc of checksum tables failed");
+        return PLEX_E_CUDA;
+    }
+    const int32_t nb = n_buckets(p, R);
+    d.bucket_payload.assign(nb, 0);
+    for (const PackItem& it : R.items) {
+        const SegDev& sg = R.segs[it.seg];
+        const uint64_t o0 = it.slab_lo - sg.slab_off, o1 = o0 + it.len;
+        const uint64_t de = std::min(o1, sg.bytes);
+        if (de > o0) d.bucket_payload[it.slab_lo / p.bucket] += de - o0;
+    }
+    *out = &(c->dev[p.id] = d);
+    return PLEX_OK;
+}
+
+static plex_status ensure_ptrs(plex_ctx_s* c, size_t n) {
+    if (n <= c->ptr_cap) return PLEX_OK;
+    size_t cap = std::max<size_t>(n, 2 * c->ptr_cap);
+    cudaFreeHost(c->h_ptrs);
+    cudaFree(c->d_ptrs);
+    c->h_ptrs = nullptr;
+    c->d_ptrs = nullptr;
+    c->ptr_cap = 0;
+    CK(cudaHostAlloc(&c->h_ptrs, cap * 8, cudaHostAllocDefault));
+    CK(cudaMalloc(&c->d_ptrs, cap * 8));
+    c->ptr_cap = cap;
+    return PLEX_OK;
+}
+
+// ---- timing ------------------------------------------------------------------
+static plex_status timed_begin(plex_ctx_s* c, cudaStream_t s, cudaEvent_t* a) {
+    if (!(c->flags & PLEX_CTX_TIMING)) return PLEX_OK;
+    while (c->pool_used + 2 > c->pool.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->pool.push_back(e);
+    }
+    *a = c->pool[c->pool_used++];
+    CK(cudaEventRecord(*a, s));
+    return PLEX_OK;
+}
+static plex_status timed_end(plex_ctx_s* c, cudaStream_t s, cudaEvent_t a, int which, uint64_t bytes) {
+    if (!(c->flags & PLEX_CTX_TIMING)) return PLEX_OK;
+    cudaEvent_t b = c->pool[c->pool_used++];
+    CK(cudaEventRecord(b, s));
+    c->pending.push_back(Timed{which, bytes, a, b});
+    return PLEX_OK;
+}
+static plex_status timed_collect(plex_ctx_s* c) {
+    for (const Timed& t : c->pending) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, t.a, t.b));
+        c->stats[t.which].launches += 1;
+        c->stats[t.which].total_ms += ms;
+        c->stats[t.which].bytes += t.bytes;
+    }
+    c->pending.clear();
+    c->pool_used = 0;
+    return PLEX_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
+    CK(cudaEventRecord(c->ev_pack_done, c->pack));
+    CK(cudaEventRecord(c->ev_copy_done, c->copy));
+    CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
+    CK(cudaStreamWaitEvent(caller, c->ev_copy_done, 0));
+    CK(cudaStreamSynchronize(c->pack));
+    CK(cudaStreamSynchronize(c->copy));
+    return timed_collect(c);
+}
+
+static plex_status check_common(plex_ctx_s* c, plex_plan_t plan) {
+    if (!c || !plan) { set_error("NULL ctx/plan"); return PLEX_E_INVAL; }
+    if (plan->p.world != c->world) {
+        set_error("plan world %d != ctx world %d", plan->p.world, c->world);
+        return PLEX_E_INVAL;
+    }
+    if (c->staging_bytes < (uint64_t)c->n_slots * plan->p.bucket) {
+        set_error("staging %llu B < %d slots x bucket %llu B", (unsigned long long)c->staging_bytes, c->n_slots,
+                  (unsigned long long)plan->p.bucket);
+        return PLEX_E_INVAL;
+    }
+    return PLEX_OK;
+}
+
+static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* const* ptrs, int32_t n) {
+    const size_t nt = p.tensors.size();
+    if (!ptrs || (size_t)n != PLEX_NUM_KINDS * nt) {
+        set_error("expected %zu pointers (4 kinds x %zu tensors), got %d", PLEX_NUM_KINDS * nt, nt, n);
+        return PLEX_E_INVAL;
+    }
+    plex_status s = ensure_ptrs(c, PLEX_NUM_KINDS * nt);
+    if (s) return s;
+    const RankPlan& R = p.ranks[c->rank];
+    for (size_t i = 0; i < PLEX_NUM_KINDS * nt; ++i) c->h_ptrs[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+    for (const SegDev& sg : R.segs) {
+        if (sg.bytes && !ptrs[sg.ptr_slot]) {
+            set_error("NULL pointer for tensor %u kind %u", sg.ptr_slot % (uint32_t)nt, sg.ptr_slot / (uint32_t)nt);
+            return PLEX_E_INVAL;
+        }
+    }
+    return PLEX_OK;
+}
+
+}  // namespace plex
+
+extern "C" {
+
+plex_status plex_nccl_unique_id(void* out128) {
+    if (!out128) { set_error("NULL out"); return PLEX_E_INVAL; }
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, int32_t n_slots, void* pack_stream,
+                            void* copy_stream, const void* nccl_id, int32_t rank, int32_t world, uint32_t flags,
+                            plex_ctx_t* out) {
+    if (!out) { set_error("NULL out"); return PLEX_E_INVAL; }
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world || n_slots < 1 || n_slots > 64 || !staging || !staging_bytes) {
+        set_error("bad ctx arguments (rank %d world %d slots %d)", rank, world, n_slots);
+        return PLEX_E_INVAL;
+    }
+    if (reinterpret_cast<uintptr_t>(staging) % 256) { set_error("staging must be 256-B aligned"); return PLEX_E_INVAL; }
+    DeviceGuard g(device);
+    auto* c = new plex_ctx_s();
+    c->device = device;
+    c->staging = reinterpret_cast<uint8_t*>(staging);
+    c->staging_bytes = staging_bytes;
+    c->n_slots = n_slots;
+    c->pack = reinterpret_cast<cudaStream_t>(pack_stream);
+    c->copy = reinterpret_cast<cudaStream_t>(copy_stream);
+    c->rank = rank;
+    c->world = world;
+    c->flags = flags;
+    auto fail = [&](plex_status s) {
+        plex_ctx_destroy(c);
+        return s;
+    };
+    if (cudaEventCreateWithFlags(&c->ev_caller, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_pack_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copy_done, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("cudaEventCreate failed");
+        return fail(PLEX_E_CUDA);
+    }
+    c->ev_pack.resize(n_slots);
+    c->ev_copy.resize(n_slots);
+    for (int i = 0; i < n_slots; ++i)
+        if (cudaEventCreateWithFlags(&c->ev_pack[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess) {
+            set_error("cudaEventCreate failed");
+            return fail(PLEX_E_CUDA);
+        }
+    c->scratch_bytes = 256 * (size_t)world + 256;
+    if (cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&c->d_flag, 64) != cudaSuccess ||
+        cudaMalloc(&c->d_scratch, 2 * c->scratch_bytes) != cudaSuccess ||
+        cudaHostAlloc(&c->h_scratch, 2 * c->scratch_bytes, cudaHostAllocDefault) != cudaSuccess) {
+        set_error("ctx scratch allocation failed");
+        return fail(PLEX_E_CUDA);
+    }
+    if (nccl_id && world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            c->comm = nullptr;
+            set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+            return fail(PLEX_E_NCCL);
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        g_ctxs.insert(c);
+    }
+    *out = c;
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_destroy(plex_ctx_t c) {
+    if (!c) return PLEX_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        g_ctxs.erase(c);
+    }
+    DeviceGuard g(c->device);
+    if (c->pack) cudaStreamSynchronize(c->pack);
+    if (c->copy) cudaStreamSynchronize(c->copy);
+    for (auto& kv : c->dev) free_devplan(kv.second);
+    for (auto& kv : c->peers)
+        if (kv.second.second) cudaIpcCloseMemHandle(kv.second.second);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (cudaEvent_t e : c->ev_pack) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_copy) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+    if (c->ev_caller) cudaEventDestroy(c->ev_caller);
+    if (c->ev_pack_done) cudaEventDestroy(c->ev_pack_done);
+    if (c->ev_copy_done) cudaEventDestroy(c->ev_copy_done);
+    cudaFreeHost(c->h_ptrs);
+    cudaFree(c->d_ptrs);
+    cudaFreeHost(c->h_flag);
+    cudaFree(c->d_flag);
+    cudaFree(c->d_scratch);
+    cudaFreeHost(c->h_scratch);
+    delete c;
+    return PLEX_OK;
+}
+
+plex_status plex_plan_destroy(plex_plan_t plan) {
+    if (!plan) return PLEX_OK;
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (plex_ctx_s* c : g_ctxs) {
+        auto it = c->dev.find(plan->p.id);
+        if (it != c->dev.end()) {
+            DeviceGuard g(c->device);
+            cudaStreamSynchronize(c->pack);
+            free_devplan(it->second);
+            c->dev.erase(it);
+        }
+    }
+    delete plan;
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_stats(plex_ctx_t c, int32_t which, plex_kernel_stats* out) {
+    if (!c || !out || which < 0 || which >= PLEX_NUM_STATS) { set_error("bad stats query"); return PLEX_E_INVAL; }
+    *out = c->stats[which];
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_reset_stats(plex_ctx_t c) {
+    if (!c) { set_error("NULL ctx"); return PLEX_E_INVAL; }
+    for (auto& s : c->stats) s = plex_kernel_stats{};
+    return PLEX_OK;
+}
+
+// ---- slabs ("the host tier uses pinned memory") ---------------
+plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, plex_slab_t* out) {
+    if (!plan || !out || rank < 0 || rank >= plan->p.world) { set_error("bad slab arguments"); return PLEX_E_INVAL; }
+    *out = nullptr;
+    const RankPlan& R = plan->p.ranks[rank];
+    auto* s = new plex_slab_s();
+    s->plan_id = plan->p.id;
+    s->rank = rank;
+    s->bytes = R.slab_bytes;
+    s->cks.assign(2 * R.segs.size(), 0);
+    const size_t alloc = std::max<uint64_t>(R.slab_bytes, 256);
+    if (flags & PLEX_SLAB_HUGEPAGE) {
+        const size_t huge = 2ull << 20;
+        s->map_bytes = align_up(alloc, huge);
+        void* p = mmap(nullptr, s->map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) {
+            delete s;
+            set_error("mmap of %zu B failed", s->map_bytes);
+            return PLEX_E_TIER_FULL;
+        }
+        madvise(p, s->map_bytes, MADV_HUGEPAGE);
+        cudaError_t e = cudaHostRegister(p, s->map_bytes, cudaHostRegisterDefault);
+        if (e != cudaSuccess) {
+            munmap(p, s->map_bytes);
+            delete s;
+            set_error("cudaHostRegister(%zu B): %s", alloc, cudaGetErrorString(e));
+            return PLEX_E_TIER_FULL;
+        }
+        s->host = reinterpret_cast<uint8_t*>(p);
+        s->registered = true;
+    } else {
+        cudaError_t e = cudaHostAlloc(&s->host, alloc, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            delete s;
+            set_error("cudaHostAlloc(%zu B): %s", alloc, cudaGetErrorString(e));
+            return PLEX_E_TIER_FULL;
+        }
+    }
+    *out = s;
+    return PLEX_OK;
+}
+
+plex_status plex_slab_destroy(plex_slab_t s) {
+    if (!s) return PLEX_OK;
+    if (s->registered) {
+        cudaHostUnregister(s->host);
+        munmap(s->host, s->map_bytes);
+    } else {
+        cudaFreeHost(s->host);
+    }
+    delete s;
+    return PLEX_OK;
+}
+
+plex_status plex_slab_info(plex_slab_t s, void** host_ptr, uint64_t* bytes, int32_t* residency) {
+    if (!s) { set_error("NULL slab"); return PLEX_E_INVAL; }
+    if (host_ptr) *host_ptr = s->host;
+    if (bytes) *bytes = s->bytes;
+    if (residency) *residency = s->residency;
+    return PLEX_OK;
+}
+
+plex_status plex_slab_checksums(plex_slab_t s, uint64_t* out, int32_t n) {
+    if (!s || !out || (size_t)n != s->cks.size()) { set_error("need %zu entries", s ? s->cks.size() : 0); return PLEX_E_INVAL; }
+    std::memcpy(out, s->cks.data(), 8 * s->cks.size());
+    return PLEX_OK;
+}
+
+// ---- a3 + a4: suspend -----------------------------------------------------------
+plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
+                               void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st) return st;
+    if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) { set_error("slab does not belong to this plan/rank"); return PLEX_E_INVAL; }
+    if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
+    DeviceGuard g(c->device);
+    const Plan& p = plan->p;
+    const RankPlan& R = p.ranks[c->rank];
+    if ((st = fill_state_ptrs(c, p, src, n_src))) return st;
+    DevPlan* d;
+    if ((st = get_devplan(c, p, &d))) return st;
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    const size_t np = PLEX_NUM_KINDS * p.tensors.size();
+    CK(cudaEventRecord(c->ev_caller, caller));
+    CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, np * 8, cudaMemcpyHostToDevice, c->pack));
+    CK(cudaMemsetAsync(d->cks, 0, 16 * std::max<size_t>(1, R.segs.size()), c->pack));
+    const int32_t nb = n_buckets(p, R);
+    for (int32_t b = 0; b < nb; ++b) {
+        const int slot = b % c->n_slots;
+        uint8_t* stg = c->staging + (uint64_t)slot * p.bucket;
+        const uint64_t lo = (uint64_t)b * p.bucket;
+        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+        if (b >= c->n_slots) CK(cudaStreamWaitEvent(c->pack, c->ev_copy[slot], 0));
+        const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+        cudaEvent_t ta = nullptr;
+        if ((st = timed_begin(c, c->pack, &ta))) return st;
+        CK(launch_pack(true, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, stg, lo, d->cks, c->pack));
+        if ((st = timed_end(c, c->pack, ta, PLEX_STAT_PACK, 2 * d->bucket_payload[b]))) return st;
+        CK(cudaEventRecord(c->ev_pack[slot], c->pack));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_pack[slot], 0));
+        if ((st = timed_begin(c, c->copy, &ta))) return st;
+        CK(cudaMemcpyAsync(slab->host + lo, stg, len, cudaMemcpyDeviceToHost, c->copy));
+        if ((st = timed_end(c, c->copy, ta, PLEX_STAT_D2H, len))) return st;
+        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+    }
+    std::vector<uint64_t> cks(2 * R.segs.size());
+    if (!cks.empty()) CK(cudaMemcpyAsync(cks.data(), d->cks, 8 * cks.size(), cudaMemcpyDeviceToHost, c->pack));
+    if ((st = finish(c, caller))) return st;
+    slab->cks.swap(cks);
+    slab->residency = PLEX_RES_HOST;
+    slab->written = true;
+    return PLEX_OK;
+}
+
+// ---- a6 + a7: resume ---------------------------------------------------------------
+plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, void* const* dst, int32_t n_dst,
+                              void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st) return st;
+    if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) { set_error("slab does not belong to this plan/rank"); return PLEX_E_INVAL; }
+    if (slab->residency == PLEX_RES_DEVICE) {
+        if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
+        return PLEX_OK;                                     // idempotent
+    }
+    DeviceGuard g(c->device);
+    const Plan& p = plan->p;
+    const RankPlan& R = p.ranks[c->rank];
+    if ((st = fill_state_ptrs(c, p, reinterpret_cast<const void* const*>(dst), n_dst))) return st;
+    DevPlan* d;
+    if ((st = get_devplan(c, p, &d))) return st;
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    const size_t np = PLEX_NUM_KINDS * p.tensors.size();
+    CK(cudaEventRecord(c->ev_caller, caller));
+    CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, np * 8, cudaMemcpyHostToDevice, c->pack));
+    const size_t nck = 2 * R.segs.size();
+    CK(cudaMemsetAsync(d->cks, 0, 8 * std::max<size_t>(2, nck), c->pack));
+    if (nck) CK(cudaMemcpyAsync(d->cks_want, slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, c->pack));
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->pack));
+    const int32_t nb = n_buckets(p, R);
+    for (int32_t b = 0; b < nb; ++b) {
+        const int slot = b % c->n_slots;
+        uint8_t* stg = c->staging + (uint64_t)slot * p.bucket;
+        const uint64_t lo = (uint64_t)b * p.bucket;
+        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+        if (b >= c->n_slots) CK(cudaStreamWaitEvent(c->copy, c->ev_pack[slot], 0));
+        cudaEvent_t ta = nullptr;
+        if ((st = timed_begin(c, c->copy, &ta))) return st;
+        CK(cudaMemcpyAsync(stg, slab->host + lo, len, cudaMemcpyHostToDevice, c->copy));
+        if ((st = timed_end(c, c->copy, ta, PLEX_STAT_H2D, len))) return st;
+        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+        CK(cudaStreamWaitEvent(c->pack, c->ev_copy[slot], 0));
+        const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+        if ((st = timed_begin(c, c->pack, &ta))) return st;
+        CK(launch_pack(false, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, stg, lo, d->cks, c->pack));
+        if ((st = timed_end(c, c->pack, ta, PLEX_STAT_UNPACK, 2 * d->bucket_payload[b]))) return st;
+        CK(cudaEventRecord(c->ev_pack[slot], c->pack));
+    }
+    CK(launch_verify(d->cks, d->cks_want, (uint32_t)R.segs.size(), c->d_flag, c->pack));
+    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->pack));
+    if ((st = finish(c, caller))) return st;
+    if (*c->h_flag) {
+        set_error("onload: %d segment checksum(s) differ from offload", *c->h_flag);
+        return PLEX_E_CHECKSUM;
+    }
+    slab->residency = PLEX_RES_DEVICE;
+    return PLEX_OK;
+}
+
+// ---- a8 - a11: weight sync -------------------------------------------------------------
+static plex_status push_rank(plex_ctx_s* c, const Plan& p, int32_t rank, const void* const* src, int32_t n_src,
+                             void* const* arenas, cudaStream_t s, const PushItem* d_items) {
+    const size_t nt = p.tensors.size();
+    if (!src || (size_t)n_src != nt) { set_error("expected %zu master pointers, got %d", nt, n_src); return PLEX_E_INVAL; }
+    const RankPlan& R = p.ranks[rank];
+    plex_status st = ensure_ptrs(c, nt + p.world);
+    if (st) return st;
+    for (size_t t = 0; t < nt; ++t) c->h_ptrs[t] = reinterpret_cast<uint64_t>(src[t]);
+    for (int32_t g = 0; g < p.world; ++g) {
+        if (!arenas[g] && p.ranks[g].arena_bytes) { set_error("NULL arena for rank %d", g); return PLEX_E_INVAL; }
+        c->h_ptrs[nt + g] = reinterpret_cast<uint64_t>(arenas[g]);
+    }
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, (nt + p.world) * 8, cudaMemcpyHostToDevice, s));
+    cudaEvent_t ta = nullptr;
+    if ((st = timed_begin(c, s, &ta))) return st;
+    CK(launch_push(d_items, R.push.size(), c->d_ptrs, c->d_ptrs + nt, s));
+    if ((st = timed_end(c, s, ta, PLEX_STAT_PUSH, R.src_read_bytes + R.src_read_bytes / 2))) return st;
+    return PLEX_OK;
+}
+
+plex_status plex_weight_sync_rank(plex_ctx_t c, plex_plan_t plan, int32_t rank, const void* const* src_master,
+                                  int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream) {
+    if (!c || !plan) { set_error("NULL ctx/plan"); return PLEX_E_INVAL; }
+    const Plan& p = plan->p;
+    if (p.tp == 0) { set_error("plan has no rollout layout"); return PLEX_E_INVAL; }
+    if (rank < 0 || rank >= p.world || n_arenas != p.world || !dst_arenas) { set_error("bad rank/arenas"); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    // device tables of `rank` (emulation may drive several ranks from one ctx)
+    const uint64_t key = p.id ^ (0x9E3779B97F4A7C15ull * (uint64_t)(rank + 1));
+    auto it = c->dev.find(key);
+    if (it == c->dev.end()) {
+        DevPlan d;
+        plex_status s = upload(&d.push, p.ranks[rank].push);
+        if (s) return s;
+        it = c->dev.emplace(key, d).first;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    plex_status st = push_rank(c, p, rank, src_master, n_src, dst_arenas, s, it->second.push);
+    if (st) return st;
+    CK(cudaStreamSynchronize(s));
+    return timed_collect(c);
+}
+
+typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+
+static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, std::vector<void*>& arenas) {
+    static cuMemGetAddressRange_t getrange = nullptr;
+    if (!getrange) {
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&getrange), cudaEnableDefault, &q));
+        if (!getrange) { set_error("cuMemGetAddressRange unavailable"); return PLEX_E_CUDA; }
+    }
+    unsigned long long base = 0;
+    size_t sz = 0;
+    if (getrange(&base, &sz, reinterpret_cast<unsigned long long>(arena)) != 0) {
+        set_error("cuMemGetAddressRange failed for the rollout arena");
+        return PLEX_E_CUDA;
+    }
+    struct Pub {
+        cudaIpcMemHandle_t h;
+        uint64_t offset;
+        uint64_t pad[7];
+    };
+    static_assert(sizeof(Pub) <= 256, "Pub");
+    Pub me{};
+    CK(cudaIpcGetMemHandle(&me.h, reinterpret_cast<void*>(base)));
+    me.offset = reinterpret_cast<uint64_t>(arena) - base;
+    std::memcpy(c->h_scratch, &me, sizeof(me));
+    uint8_t* d_send = c->d_scratch;
+    uint8_t* d_all = c->d_scratch + 256;
+    CK(cudaMemcpyAsync(d_send, c->h_scratch, 256, cudaMemcpyHostToDevice, c->pack));
+    NK(ncclAllGather(d_send, d_all, 256, ncclUint8, c->comm, c->pack));
+    CK(cudaMemcpyAsync(c->h_scratch + 256, d_all, 256 * (size_t)c->world, cudaMemcpyDeviceToHost, c->pack));
+    CK(cudaStreamSynchronize(c->pack));
+    arenas.assign(c->world, nullptr);
+    for (int g = 0; g < c->world; ++g) {
+        if (g == c->rank) { arenas[g] = arena; continue; }
+        Pub pub;
+        std::memcpy(&pub, c->h_scratch + 256 + 256 * (size_t)g, sizeof(pub));
+        std::vector<uint8_t> hb(reinterpret_cast<uint8_t*>(&pub.h), reinterpret_cast<uint8_t*>(&pub.h) + sizeof(pub.h));
+        auto it = c->peers.find(g);
+        if (it == c->peers.end() || it->second.first != hb) {
+            if (it != c->peers.end() && it->second.second) cudaIpcCloseMemHandle(it->second.second);
+            void* mapped = nullptr;
+            CK(cudaIpcOpenMemHandle(&mapped, pub.h, cudaIpcMemLazyEnablePeerAccess));
+            c->peers[g] = {hb, mapped};
+        }
+        arenas[g] = reinterpret_cast<uint8_t*>(c->peers[g].second) + pub.offset;
+    }
+    return PLEX_OK;
+}
+
+plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* src_master, int32_t n_src,
+                             void* dst_arena, void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st) return st;
+    const Plan& p = plan->p;
+    if (p.tp == 0) { set_error("plan has no rollout layout"); return PLEX_E_INVAL; }
+    if (!dst_arena && p.ranks[c->rank].arena_bytes) { set_error("NULL arena"); return PLEX_E_INVAL; }
+    if (c->world > 1 && !c->comm) { set_error("world > 1 needs a ctx created with an NCCL id"); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    if (c->flags & PLEX_CTX_SYNC_NCCL) return nccl_sync(c, p, src_master, dst_arena, caller);
+    DevPlan* d;
+    if ((st = get_devplan(c, p, &d))) return st;
+    std::vector<void*> arenas(1, dst_arena);
+    if (c->world > 1 && (st = exchange_arenas(c, p, dst_arena, arenas))) return st;
+    CK(cudaEventRecord(c->ev_caller, caller));
+    CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
+    int* d_bar = reinterpret_cast<int*>(c->d_scratch + 256 + 256 * (size_t)c->world);
+    if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all arenas free
+    if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push))) return st;
+    if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all pushes landed
+    return finish(c, caller);
+}
+
+// ---- infrastructure --------------------------------------------------------------------
+static uint64_t fnv1a64(const char* s) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    for (; *s; ++s) {
+        h ^= (uint8_t)*s;
+        h *= 0x100000001B3ull;
+    }
+    return h;
+}
+static uint64_t stream_base(uint64_t seed, const char* key, int kind) {
+    return (seed * 0xD1B54A32D192ED03ull) ^ fnv1a64(key) ^ ((uint64_t)kind << 56);
+}
+
+plex_status plex_synth_fill(void* dst, int32_t kind, uint64_t seed, const char* key, uint64_t index_base, uint64_t count,
+                            int32_t special_bits, void* stream) {
+    if ((!dst && count) || !key || kind < 0 || kind >= PLEX_NUM_KINDS || special_bits < 0 || special_bits > 63) {
+        set_error("bad synth arguments");
+        return PLEX_E_INVAL;
+    }
+    CK(launch_synth(dst, kind, stream_base(seed, key, kind), index_base, count, kind ? special_bits : 0,
+                    reinterpret_cast<cudaStream_t>(stream)));
+    return PLEX_OK;
+}
+
+plex_status plex_synth_mutate(void* buf, int32_t kind, uint64_t job_seed, uint64_t step, const char* key,
+                              uint64_t index_base, uint64_t count, void* stream) {
+    if ((!buf && count) || !key || kind < 0 || kind >= PLEX_NUM_KINDS) { set_error("bad mutate arguments"); return PLEX_E_INVAL; }
+    const uint64_t base = stream_base(job_seed, key, kind) ^ ((step + 1) * 0xA24BAED4963EE407ull);
+    CK(launch_mutate(buf, kind_esize(kind), base, index_base, count, reinterpret_cast<cudaStream_t>(stream)));
+    return PLEX_OK;
+}
+
+plex_status plex_checksum(const void* src, int32_t esize, uint64_t index_base, uint64_t count, uint64_t* dev_out,
+                          void* stream) {
+    if ((!src && count) || !dev_out || (esize != 2 && esize != 4)) { set_error("bad checksum arguments"); return PLEX_E_INVAL; }
+    CK(launch_checksum(src, esize, index_base, count, reinterpret_cast<unsigned long long*>(dev_out),
+                       reinterpret_cast<cudaStream_t>(stream)));
+    return PLEX_OK;
+}
+
+plex_status plex_cast_rne(const void* src_f32, void* dst_bf16, uint64_t count, void* stream) {
+    if ((!src_f32 || !dst_bf16) && count) { set_error("bad cast arguments"); return PLEX_E_INVAL; }
+    CK(launch_cast(src_f32, dst_bf16, count, reinterpret_cast<cudaStream_t>(stream)));
+    return PLEX_OK;
+}
+
+}  // extern "C"
+
+namespace plex {
+plex_status nccl_sync(plex_ctx_s* c, const Plan& p, const void* const* src, void* arena, cudaStream_t caller) {
+    (void)c; (void)p; (void)src; (void)arena; (void)caller;
+    set_error("PLEX_CTX_SYNC_NCCL transport not built yet");
+    return PLEX_E_INVAL;
+}
+}  // namespace plex

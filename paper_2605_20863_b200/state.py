@@ -1,0 +1,421 @@
+"""Python API of the B200 state-transition path (thin: marshalling only).
+
+    mgr  = StateManager(device=0)                    # one per rank process
+    plan = mgr.plan(manifest, head_dim=128, tp=2, dp=4)
+    job  = Job(mgr, plan, seed=1).alloc().init_synthetic()
+    job.suspend(); job.resume(); job.sync(arena)
+
+Everything that touches a byte of state runs in libplex.so (CUDA kernels,
+copy engines, NCCL); this module only builds argument arrays, owns PyTorch
+device memory and streams, and bootstraps the NCCL id over torch.distributed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import re
+from collections import OrderedDict
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib, ptr_array
+
+KIND_TORCH = {0: torch.bfloat16, 1: torch.float32, 2: torch.float32, 3: torch.float32}
+
+_LAYER = re.compile(r"^(model\.layers\.\d+\.)")
+
+
+# ---------------------------------------------------------------------------
+# R3 roles from parameter names (product side; the oracle has its own reading)
+# ---------------------------------------------------------------------------
+def describe(manifest: Sequence[Tuple[str, Tuple[int, ...]]], head_dim: int = 1):
+    """Return (descs, group_names): plex_tensor_desc fields per tensor and the
+    rollout tensor name of every destination group.
+
+    Column-parallel q/k/v (+bias) fuse into ``qkv_proj`` (split unit =
+    head_dim), gate/up into ``gate_up_proj``; o_proj/down_proj are
+    row-parallel; embed_tokens/lm_head vocab-parallel (column split); experts
+    stack into ``experts.w13_weight`` (gate_e|up_e) and ``experts.w2_weight``;
+    everything else (norms, router) is replicated.
+    """
+    groups: Dict[str, int] = OrderedDict()
+
+    def gid(name: str) -> int:
+        if name not in groups:
+            groups[name] = len(groups)
+        return groups[name]
+
+    descs = []
+    for key, shape in manifest:
+        d0 = int(shape[0])
+        d1 = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        ndim = len(shape)
+        m = _LAYER.match(key)
+        pre = m.group(1) if m else ""
+        role, slot, expert, unit = L.ROLE_REPLICATED, 0, -1, 1
+        gname = key
+        mm = re.match(r"^(model\.layers\.\d+\.)self_attn\.([qkv])_proj\.(weight|bias)$", key)
+        me = re.match(r"^(model\.layers\.\d+\.)mlp\.experts\.(\d+)\.(gate|up|down)_proj\.weight$", key)
+        if key.endswith("embed_tokens.weight") or key == "lm_head.weight":
+            role = L.ROLE_COL
+        elif mm:
+            role, slot, unit = L.ROLE_COL, "qkv".index(mm.group(2)), head_dim
+            gname = f"{pre}self_attn.qkv_proj.{mm.group(3)}"
+        elif key.endswith("self_attn.o_proj.weight"):
+            role = L.ROLE_ROW
+        elif me:
+            e, which = int(me.group(2)), me.group(3)
+            role, expert = L.ROLE_EXPERT, e
+            if which == "down":
+                gname, slot = f"{pre}mlp.experts.w2_weight", e
+            else:
+                gname, slot = f"{pre}mlp.experts.w13_weight", 2 * e + (0 if which == "gate" else 1)
+        elif re.match(r"^model\.layers\.\d+\.mlp\.(gate|up)_proj\.weight$", key):
+            role, slot = L.ROLE_COL, 0 if ".gate_proj." in key else 1
+            gname = f"{pre}mlp.gate_up_proj.weight"
+        elif re.match(r"^model\.layers\.\d+\.mlp\.down_proj\.weight$", key):
+            role = L.ROLE_ROW
+        descs.append(dict(key=key, d0=d0, d1=d1, ndim=ndim, role=role, group=gid(gname), slot=slot,
+                          expert=expert, unit=unit))
+    names = {v: k for k, v in groups.items()}
+    return descs, names
+
+
+class Plan:
+    """Immutable transition plan (plex_transition_plan)."""
+
+    def __init__(self, manifest, head_dim: int = 1, world: int = 1, tp: int = 0, dp: int = 0, ep: int = 1,
+                 rank_map: int = L.RANKMAP_TP_FAST, slab_layout: int = L.SLAB_KIND_MAJOR,
+                 kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
+                 bucket_bytes: int = 64 << 20, tile_bytes: int = 64 << 10,
+                 resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE):
+        self.manifest = list(manifest)
+        self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
+        descs, self.group_names = describe(self.manifest, head_dim)
+        self.descs = descs
+        self._keys = [d["key"].encode() for d in descs]
+        arr = (L.TensorDesc * len(descs))()
+        for i, d in enumerate(descs):
+            arr[i] = L.TensorDesc(self._keys[i], d["d0"], d["d1"], d["ndim"], d["role"], d["group"], d["slot"],
+                                  d["expert"], d["unit"])
+        self._arr = arr
+        sub = None
+        n_sub = 0
+        if subset is not None:
+            idx = [self.index[k] for k in subset]
+            sub = (C.c_int32 * max(1, len(idx)))(*idx)
+            n_sub = len(idx)
+        self._sub = sub
+        req = L.PlanReq(len(descs), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
+                        bucket_bytes, tile_bytes, resident_job, incoming_job, op)
+        h = C.c_void_p()
+        check(lib.plex_transition_plan(C.byref(req), C.byref(h)))
+        self.h = h
+        self.world, self.tp, self.dp, self.ep = world, tp, dp, ep
+        self.kind_mask = kind_mask
+        self.bucket_bytes = bucket_bytes
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and lib is not None:
+            lib.plex_plan_destroy(h)
+            self.h = None
+
+    # ---- queries ----------------------------------------------------------
+    def stats(self) -> L.PlanStats:
+        s = L.PlanStats()
+        check(lib.plex_plan_query(self.h, C.byref(s)))
+        return s
+
+    def ops(self) -> List[Tuple[int, int]]:
+        s = self.stats()
+        return [(s.ops[i], s.op_jobs[i]) for i in range(s.n_ops)]
+
+    def rank_info(self, rank: int) -> L.RankInfo:
+        r = L.RankInfo()
+        check(lib.plex_plan_rank_info(self.h, rank, C.byref(r)))
+        return r
+
+    def segments(self, rank: int) -> List[L.SegDesc]:
+        n = self.rank_info(rank).n_segments
+        out = []
+        for i in range(n):
+            s = L.SegDesc()
+            check(lib.plex_plan_segment(self.h, rank, i, C.byref(s)))
+            out.append(s)
+        return out
+
+    def shard_rows(self, rank: int, t: int) -> Tuple[int, int]:
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.plex_plan_shard_rows(self.h, rank, t, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def shard_shape(self, rank: int, t: int) -> Tuple[int, ...]:
+        a, b = self.shard_rows(rank, t)
+        shape = self.manifest[t][1]
+        return (b - a,) + tuple(shape[1:])
+
+    def dst_tensors(self, rank: int) -> List[Tuple[str, int, Tuple[int, ...]]]:
+        """(rollout name, arena byte offset, shape) of rank's destination tensors."""
+        n = self.rank_info(rank).n_dst_tensors
+        out = []
+        for i in range(n):
+            d = L.DstDesc()
+            check(lib.plex_plan_dst_tensor(self.h, rank, i, C.byref(d)))
+            name = self.group_names[d.group]
+            shape: Tuple[int, ...] = (d.rows, d.cols)
+            if name.endswith(("w13_weight", "w2_weight")):
+                per = self.n_experts(name) // self.ep
+                shape = (per, d.rows // per, d.cols)
+            elif self.descs[d.first_tensor]["ndim"] == 1:
+                shape = (d.rows,)
+            out.append((name, d.arena_offset, shape))
+        return out
+
+    def n_experts(self, group_name: str) -> int:
+        pre = group_name.rsplit("mlp.experts.", 1)[0]
+        return sum(1 for d in self.descs if d["key"].startswith(pre + "mlp.experts.")
+                   and d["key"].endswith("down_proj.weight"))
+
+    def ledger(self) -> np.ndarray:
+        n = self.world * self.world
+        buf = (C.c_uint64 * n)()
+        check(lib.plex_plan_ledger(self.h, buf, n))
+        return np.frombuffer(buf, dtype=np.uint64).reshape(self.world, self.world).astype(np.int64).copy()
+
+
+class Slab:
+    """Pinned host slab of one rank's state under a plan (plex_slab_create)."""
+
+    def __init__(self, plan: Plan, rank: int, hugepage: bool = False):
+        h = C.c_void_p()
+        check(lib.plex_slab_create(plan.h, rank, L.SLAB_HUGEPAGE if hugepage else 0, C.byref(h)))
+        self.h = h
+        self.plan = plan
+        self.rank = rank
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and lib is not None:
+            lib.plex_slab_destroy(h)
+            self.h = None
+
+    def info(self) -> Tuple[int, int, int]:
+        p, n, r = C.c_void_p(), C.c_uint64(), C.c_int32()
+        check(lib.plex_slab_info(self.h, C.byref(p), C.byref(n), C.byref(r)))
+        return p.value or 0, n.value, r.value
+
+    @property
+    def residency(self) -> int:
+        return self.info()[2]
+
+    def host_bytes(self) -> np.ndarray:
+        """Writable NumPy view of the pinned slab bytes."""
+        p, n, _ = self.info()
+        if n == 0:
+            return np.zeros(0, dtype=np.uint8)
+        return np.ctypeslib.as_array((C.c_uint8 * n).from_address(p))
+
+    def checksums(self) -> np.ndarray:
+        n = 2 * self.plan.rank_info(self.rank).n_segments
+        buf = (C.c_uint64 * max(1, n))()
+        check(lib.plex_slab_checksums(self.h, buf, n))
+        return np.frombuffer(buf, dtype=np.uint64)[:n].reshape(-1, 2).copy()
+
+
+def _stream_ptr(s) -> int:
+    if s is None:
+        return torch.cuda.current_stream().cuda_stream
+    return s.cuda_stream
+
+
+class StateManager:
+    """One per rank process: the ctx (streams, staging, NCCL communicator)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 64 << 20,
+                 n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
+                 nccl_id: Optional[bytes] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("StateManager needs a CUDA device (no CPU fallback)")
+        self.device = device
+        torch.cuda.set_device(device)
+        self.rank, self.world = rank, world
+        self.bucket_bytes = bucket_bytes
+        self.n_slots = n_slots
+        self.pack_stream = torch.cuda.Stream(device)
+        self.copy_stream = torch.cuda.Stream(device)
+        self.staging = torch.empty(n_slots * bucket_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+        idbuf = None
+        if world > 1 and bootstrap:
+            if nccl_id is None:
+                nccl_id = self._bootstrap_id()
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        flags = (L.CTX_TIMING if timing else 0) | (L.CTX_SYNC_NCCL if sync_nccl else 0)
+        h = C.c_void_p()
+        check(lib.plex_ctx_create(device, self.staging.data_ptr(), self.staging.numel(), n_slots,
+                                  self.pack_stream.cuda_stream, self.copy_stream.cuda_stream,
+                                  idbuf, rank, world, flags, C.byref(h)))
+        self.h = h
+
+    def _bootstrap_id(self) -> bytes:
+        import torch.distributed as dist
+        buf = C.create_string_buffer(128)
+        if self.rank == 0:
+            check(lib.plex_nccl_unique_id(buf))
+        obj = [bytes(buf.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and lib is not None:
+            lib.plex_ctx_destroy(h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---- plans / slabs --------------------------------------------------------
+    def plan(self, manifest, **kw) -> Plan:
+        kw.setdefault("world", self.world)
+        kw.setdefault("bucket_bytes", self.bucket_bytes)
+        return Plan(manifest, **kw)
+
+    def slab(self, plan: Plan, rank: Optional[int] = None, hugepage: bool = False) -> Slab:
+        return Slab(plan, self.rank if rank is None else rank, hugepage)
+
+    # ---- the four hot-path calls --------------------------------------------------
+    @staticmethod
+    def _state_ptrs(plan: Plan, shards: Dict[Tuple[str, int], torch.Tensor]):
+        nt = len(plan.manifest)
+        ptrs = [0] * (L.NUM_KINDS * nt)
+        for (key, kind), t in shards.items():
+            if not t.is_contiguous():
+                raise ValueError(f"shard {key}/{kind} must be contiguous")
+            ptrs[kind * nt + plan.index[key]] = t.data_ptr() if t.numel() else 0
+        return ptr_array(ptrs), len(ptrs)
+
+    def offload(self, plan: Plan, shards, slab: Slab, stream=None) -> None:
+        arr, n = self._state_ptrs(plan, shards)
+        check(lib.plex_state_offload(self.h, plan.h, arr, n, slab.h, _stream_ptr(stream)))
+
+    def onload(self, plan: Plan, slab: Slab, shards, stream=None) -> None:
+        arr, n = self._state_ptrs(plan, shards)
+        check(lib.plex_state_onload(self.h, plan.h, slab.h, arr, n, _stream_ptr(stream)))
+
+    def sync(self, plan: Plan, masters: Sequence[torch.Tensor], arena: torch.Tensor, stream=None) -> None:
+        arr = ptr_array([m.data_ptr() if m.numel() else 0 for m in masters])
+        check(lib.plex_weight_sync(self.h, plan.h, arr, len(masters), arena.data_ptr(), _stream_ptr(stream)))
+
+    def sync_rank(self, plan: Plan, rank: int, masters: Sequence[torch.Tensor], arenas: Sequence[torch.Tensor],
+                  stream=None) -> None:
+        arr = ptr_array([m.data_ptr() if m.numel() else 0 for m in masters])
+        ar = ptr_array([a.data_ptr() for a in arenas])
+        check(lib.plex_weight_sync_rank(self.h, plan.h, rank, arr, len(masters), ar, len(arenas),
+                                        _stream_ptr(stream)))
+
+    # ---- helpers ---------------------------------------------------------------------
+    def arena(self, plan: Plan, rank: Optional[int] = None) -> torch.Tensor:
+        n = plan.rank_info(self.rank if rank is None else rank).dst_arena_bytes
+        return torch.empty(max(n, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    @staticmethod
+    def rollout_views(plan: Plan, rank: int, arena: torch.Tensor) -> "OrderedDict[str, torch.Tensor]":
+        out = OrderedDict()
+        for name, off, shape in plan.dst_tensors(rank):
+            n = int(np.prod(shape))
+            out[name] = arena[off:off + 2 * n].view(torch.bfloat16).view(shape)
+        return out
+
+    def stats(self) -> Dict[str, dict]:
+        out = {}
+        for i, nm in enumerate(L.STAT_NAMES):
+            s = L.KernelStats()
+            check(lib.plex_ctx_stats(self.h, i, C.byref(s)))
+            out[nm] = {"launches": s.launches, "ms": s.total_ms, "bytes": s.bytes}
+        return out
+
+    def reset_stats(self) -> None:
+        check(lib.plex_ctx_reset_stats(self.h))
+
+
+# ---- infrastructure (synthetic inputs, verification) ------------------------------
+def synth_fill(t: torch.Tensor, kind: int, seed: int, key: str, index_base: int = 0, special_bits: int = 0,
+               stream=None) -> None:
+    check(lib.plex_synth_fill(t.data_ptr() if t.numel() else None, kind, seed, key.encode(), index_base,
+                              t.numel(), special_bits, _stream_ptr(stream)))
+
+
+def synth_mutate(t: torch.Tensor, kind: int, job_seed: int, step: int, key: str, index_base: int = 0,
+                 stream=None) -> None:
+    check(lib.plex_synth_mutate(t.data_ptr() if t.numel() else None, kind, job_seed, step, key.encode(),
+                                index_base, t.numel(), _stream_ptr(stream)))
+
+
+def checksum(t: torch.Tensor, index_base: int = 0, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """(S1, S2) of R14 as a 2-element int64 device tensor (bit pattern of uint64)."""
+    if out is None:
+        out = torch.zeros(2, dtype=torch.int64, device=t.device)
+    check(lib.plex_checksum(t.data_ptr() if t.numel() else None, t.element_size(), index_base, t.numel(),
+                            out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def cast_rne(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
+    assert src.dtype == torch.float32 and dst.dtype == torch.bfloat16 and src.numel() == dst.numel()
+    check(lib.plex_cast_rne(src.data_ptr(), dst.data_ptr(), src.numel(), _stream_ptr(stream)))
+
+
+class Job:
+    """One job's state on this rank: its FSDP shards (4 kinds), pinned slab
+    and plan.  suspend/resume implement a3-a7 plus the release/re-acquire of
+    a5 (device storage freed while HOST-resident)."""
+
+    def __init__(self, mgr: StateManager, plan: Plan, seed: int = 0, rank: Optional[int] = None,
+                 hugepage: bool = False, slab: bool = True):
+        self.mgr, self.plan, self.seed = mgr, plan, seed
+        self.rank = mgr.rank if rank is None else rank
+        self.slab = Slab(plan, self.rank, hugepage) if slab else None
+        self.shards: "OrderedDict[Tuple[str, int], torch.Tensor]" = OrderedDict()
+        self.dev = f"cuda:{mgr.device}"
+
+    def alloc(self, kinds=(0, 1, 2, 3)) -> "Job":
+        for t, (key, _) in enumerate(self.plan.manifest):
+            shp = self.plan.shard_shape(self.rank, t)
+            for kd in kinds:
+                self.shards[(key, kd)] = torch.empty(shp, dtype=KIND_TORCH[kd], device=self.dev)
+        return self
+
+    def init_synthetic(self, special_bits: int = 0) -> "Job":
+        for t, (key, shape) in enumerate(self.plan.manifest):
+            r0, _ = self.plan.shard_rows(self.rank, t)
+            re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+            for (k2, kd), x in self.shards.items():
+                if k2 == key:
+                    synth_fill(x, kd, self.seed, key, r0 * re_, special_bits)
+        return self
+
+    def slab_shards(self):
+        mask = self.plan.kind_mask
+        return OrderedDict((kk, v) for kk, v in self.shards.items() if mask & (1 << kk[1]))
+
+    def masters(self) -> List[torch.Tensor]:
+        return [self.shards[(k, 1)] for k, _ in self.plan.manifest]
+
+    def suspend(self, stream=None, release: bool = True) -> None:
+        self.mgr.offload(self.plan, self.slab_shards(), self.slab, stream)
+        if release:
+            for v in self.slab_shards().values():
+                v.untyped_storage().resize_(0)
+
+    def resume(self, stream=None) -> None:
+        for v in self.slab_shards().values():
+            need = v.numel() * v.element_size()
+            if v.untyped_storage().nbytes() != need:
+                v.untyped_storage().resize_(need)
+        self.mgr.onload(self.plan, self.slab, self.slab_shards(), stream)
+
+    def sync(self, arena: torch.Tensor, stream=None) -> None:
+        self.mgr.sync(self.plan, self.masters(), arena, stream)

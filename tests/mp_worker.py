@@ -1,0 +1,78 @@
+"""torchrun worker for the multi-GPU parity test (tests/test_gpu_multi.py).
+
+Each rank: bootstraps the library's NCCL communicator over torch.distributed,
+runs the real collective plex_weight_sync (CUDA-IPC peer-mapped arenas, fused
+cast + NVLink push) and a suspend/resume round trip of its own shards, and
+checks both bit-exactly against the CPU oracle.  Exit code 0 = all ranks ok.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import paper_2605_20863_b200 as P  # noqa: E402
+from oracle import plex_oracle as O  # noqa: E402
+from plexgen import MODELS, manifest  # noqa: E402
+from _state import full_state, fsdp_shards, master_shards  # noqa: E402
+
+
+def bits_np(t):
+    t = t.detach().contiguous().cpu()
+    return t.view(torch.int16).numpy().view(np.uint16) if t.element_size() == 2 else t.view(torch.int32).numpy().view(np.uint32)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=1 << 16, n_slots=2)
+    bad = 0
+    cases = [("mid", 2 if world % 2 == 0 else 1, 1), ("mid-moe", 2 if world % 2 == 0 else 1, world),
+             ("toy-odd", 1, 1)]
+    for model, tp, ep in cases:
+        dp = world // tp
+        hd = MODELS[model].head_dim
+        for rank_map in (0, 1):
+            plan = mgr.plan(manifest(model), head_dim=hd, tp=tp, dp=dp, ep=ep, rank_map=rank_map, tile_bytes=2048)
+            job = P.Job(mgr, plan, seed=21).alloc().init_synthetic(special_bits=3)
+            arena = mgr.arena(plan)
+            arena.fill_(0xCD)
+            for _ in range(2):                              # second call reuses mapped peers
+                job.sync(arena)
+            full = full_state(model, seed=21, special_bits=3)
+            want = O.weight_sync(master_shards(full, world, O.fsdp_rows), tp, dp, ep, rank_map, hd)[rank]
+            for name, v in P.StateManager.rollout_views(plan, rank, arena).items():
+                if not np.array_equal(bits_np(v), want[name]):
+                    print(f"[rank {rank}] sync mismatch {model} map={rank_map} {name}", flush=True)
+                    bad += 1
+            # suspend / resume of this rank's shards
+            before = {k: bits_np(v) for k, v in job.shards.items()}
+            job.suspend()
+            segs, size = O.slab_layout(manifest(model), world, rank)
+            osh = fsdp_shards(full, world, rank, O.fsdp_rows)
+            if not np.array_equal(job.slab.host_bytes(), O.pack_slab(segs, size, osh)):
+                print(f"[rank {rank}] slab mismatch {model}", flush=True)
+                bad += 1
+            job.resume()
+            for k, v in job.shards.items():
+                if not np.array_equal(bits_np(v), before[k]):
+                    print(f"[rank {rank}] restore mismatch {model} {k}", flush=True)
+                    bad += 1
+            del arena
+    t = torch.tensor([bad], device=f"cuda:{local}")
+    dist.all_reduce(t)
+    mgr.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mp_worker world={world} mismatches={int(t.item())}", flush=True)
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

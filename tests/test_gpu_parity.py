@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Multi-rank layouts are emulated on one GPU (every rank's buffers on cuda:0,
+one ctx per rank; the sync's per-rank push kernels write into all ranks'
+arenas), so the full W-rank data path is covered without W GPUs.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import plex_oracle as O
+from plexgen import MODELS, gen_bits, gen_range, manifest, mutation_bits
+
+from _state import full_state, fsdp_shards, master_shards
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2605_20863_b200")
+from paper_2605_20863_b200 import _lib as L  # noqa: E402
+from paper_2605_20863_b200.state import KIND_TORCH  # noqa: E402
+
+U16, U32 = np.uint16, np.uint32
+
+
+def bits_np(t: torch.Tensor) -> np.ndarray:
+    t = t.detach().contiguous().cpu()
+    if t.element_size() == 2:
+        return t.view(torch.int16).numpy().view(U16)
+    return t.view(torch.int32).numpy().view(U32)
+
+
+def to_dev(a: np.ndarray, kind: int) -> torch.Tensor:
+    dt = torch.int16 if kind == 0 else torch.int32
+    return torch.from_numpy(a.view(np.int16 if kind == 0 else np.int32).copy()).view(KIND_TORCH[kind]).cuda() \
+        if a.size else torch.empty(a.shape, dtype=KIND_TORCH[kind], device="cuda")
+
+
+def mgr(W=1, r=0, bucket=4096, slots=2, **kw):
+    return P.StateManager(device=0, rank=r, world=W, bucket_bytes=bucket, n_slots=slots, bootstrap=False, **kw)
+
+
+def rank_shards(plan, r, seed, special_bits=0, kinds=(0, 1, 2, 3)):
+    out = {}
+    for t, (key, shape) in enumerate(plan.manifest):
+        a, b = plan.shard_rows(r, t)
+        re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        for kd in kinds:
+            x = torch.empty((b - a,) + tuple(shape[1:]), dtype=KIND_TORCH[kd], device="cuda")
+            P.synth_fill(x, kd, seed, key, a * re_, special_bits if kd else 0)
+            out[(key, kd)] = x
+    torch.cuda.synchronize()
+    return out
+
+
+# ---- K6 generator parity ----------------------------------------------------------
+@pytest.mark.parametrize("model,W", [("toy-odd", 3), ("mid", 4), ("toy-moe", 2)])
+def test_synth_matches_generator(model, W):
+    plan = P.Plan(manifest(model), world=W)
+    for r in range(W):
+        sh = rank_shards(plan, r, seed=5, special_bits=3)
+        for (key, kd), x in sh.items():
+            shape = dict(plan.manifest)[key]
+            re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+            a, _ = plan.shard_rows(r, plan.index[key])
+            want = gen_range(5, key, kd, a * re_, x.numel(), 3 if kd else 0)
+            assert np.array_equal(bits_np(x).reshape(-1), want), (key, kd)
+
+
+# ---- a8 cast parity -------------------------------------------------------------------
+def test_cast_matches_oracle_specials_and_random():
+    rng = np.random.default_rng(0)
+    u = np.concatenate([
+        np.array([int(l.split()[0], 16) for l in open(__file__.replace("test_gpu_parity.py", "golden/rne_specials.txt"))
+                  if l.strip() and not l.startswith("#")], dtype=U32),
+        rng.integers(0, 1 << 32, size=(1 << 24) + 13, dtype=np.uint64).astype(U32)])
+    src = to_dev(u, 1)
+    for off in (0, 1, 3):                      # aligned and misaligned vector paths
+        s = src[off:]
+        dst = torch.empty(s.numel(), dtype=torch.bfloat16, device="cuda")
+        P.cast_rne(s, dst)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits_np(dst), O.rne_bf16(u[off:]))
+
+
+@pytest.mark.slow
+def test_cast_exhaustive():
+    """All 2^32 fp32 bit patterns (R8), GPU vs oracle, in 2^26 chunks."""
+    n = 1 << 26
+    dst = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    for c in range(1 << 6):
+        u = np.arange(c * n, (c + 1) * n, dtype=np.uint64).astype(U32)
+        P.cast_rne(to_dev(u, 1), dst)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits_np(dst), O.rne_bf16(u)), c
+
+
+# ---- K7 checksum parity ---------------------------------------------------------------------
+@pytest.mark.parametrize("kind,n,base,off", [(0, 100_003, 0, 0), (1, 77_777, 12345, 0), (0, 5000, 7, 3), (3, 1 << 20, 1 << 31, 1)])
+def test_checksum_matches_oracle(kind, n, base, off):
+    a = gen_range(9, "ck", kind, 0, n + off)
+    x = to_dev(a, kind)[off:]
+    got = P.checksum(x, base).cpu().numpy().view(np.uint64)
+    assert tuple(int(v) for v in got) == O.checksum(a[off:], base)
+
+
+# ---- a3-a7 suspend/resume round trip ----------------------------------------------------------
+RT_CASES = [("toy", 1, L.SLAB_KIND_MAJOR, 4096), ("toy-odd", 3, L.SLAB_KIND_MAJOR, 1024),
+            ("toy-moe", 4, L.SLAB_KEY_MAJOR, 2048), ("mid", 2, L.SLAB_KIND_MAJOR, 1 << 16),
+            ("mid-moe", 8, L.SLAB_KEY_MAJOR, 1 << 14), ("toy", 13, L.SLAB_KIND_MAJOR, 512),
+            ("mid", 1, L.SLAB_KEY_MAJOR, 1 << 20)]
+
+
+@pytest.mark.parametrize("model,W,layout,bucket", RT_CASES)
+def test_offload_onload_roundtrip(model, W, layout, bucket):
+    man = manifest(model)
+    plan = P.Plan(man, world=W, slab_layout=layout, bucket_bytes=bucket, tile_bytes=512)
+    full = full_state(model, seed=11, special_bits=3)
+    for r in range(W):
+        m = mgr(W, r, bucket=bucket, slots=3)
+        sh = rank_shards(plan, r, seed=11, special_bits=3)
+        slab = P.Slab(plan, r)
+        assert slab.residency == L.RES_DEVICE
+        with pytest.raises(P.PlexError) as e:           # never written: E_STATE
+            m.onload(plan, slab, sh)
+        assert e.value.code == L.E_STATE
+        m.offload(plan, sh, slab)
+        assert slab.residency == L.RES_HOST
+        segs, size = O.slab_layout(man, W, r, layout)
+        osh = fsdp_shards(full, W, r, O.fsdp_rows)
+        assert np.array_equal(slab.host_bytes(), O.pack_slab(segs, size, osh))
+        want_ck = np.array(O.segment_checksums(segs, osh), dtype=np.uint64).reshape(-1, 2)
+        assert np.array_equal(slab.checksums(), want_ck)
+        # release + re-acquire (a5), then restore into fresh garbage-filled buffers
+        new = {k: torch.full_like(v, 7) if v.numel() else torch.empty_like(v) for k, v in sh.items()}
+        del sh
+        m.offload(plan, new, slab)                      # HOST already: no-op, slab unchanged
+        assert np.array_equal(slab.host_bytes(), O.pack_slab(segs, size, osh))
+        m.onload(plan, slab, new)
+        assert slab.residency == L.RES_DEVICE
+        for (key, kd), x in new.items():
+            assert np.array_equal(bits_np(x), osh[(key, kd)]), (key, kd)
+
+
+def test_onload_detects_slab_corruption():
+    man = manifest("mid")
+    plan = P.Plan(man, world=2, bucket_bytes=1 << 16)
+    m = mgr(2, 1, bucket=1 << 16)
+    sh = rank_shards(plan, 1, seed=3)
+    slab = P.Slab(plan, 1)
+    m.offload(plan, sh, slab)
+    hb = slab.host_bytes()
+    seg = plan.segments(1)[17]
+    pos = seg.slab_offset + seg.nbytes // 2
+    hb[pos] ^= 0x10
+    with pytest.raises(P.PlexError) as e:
+        m.onload(plan, slab, sh)
+    assert e.value.code == L.E_CHECKSUM
+    assert slab.residency == L.RES_HOST                 # no partial state change
+    hb[pos] ^= 0x10
+    m.onload(plan, slab, sh)
+    assert slab.residency == L.RES_DEVICE
+
+
+def test_job_suspend_resume_releases_memory():
+    man = manifest("mid")
+    m = mgr(1, 0, bucket=1 << 18)
+    plan = m.plan(man)
+    job = P.Job(m, plan, seed=4).alloc().init_synthetic()
+    before = {k: bits_np(v) for k, v in job.shards.items()}
+    job.suspend()
+    assert all(v.untyped_storage().nbytes() == 0 for v in job.shards.values())
+    job.resume()
+    for k, v in job.shards.items():
+        assert np.array_equal(bits_np(v), before[k])
+
+
+# ---- a8-a11 weight sync (emulated W ranks on one GPU) -------------------------------------------
+SYNC_CASES = [("toy", 1, 1, 1, 1), ("toy", 2, 2, 1, 1), ("toy-odd", 3, 1, 3, 1), ("toy-tied", 4, 2, 2, 1),
+              ("toy-kv4", 4, 4, 1, 1), ("toy-moe", 4, 2, 2, 2), ("toy-moe", 8, 2, 4, 4), ("mid", 4, 2, 2, 1),
+              ("mid", 8, 2, 4, 1), ("mid-moe", 8, 2, 4, 8), ("toy", 5, 1, 5, 1)]
+
+
+@pytest.mark.parametrize("model,W,tp,dp,ep", SYNC_CASES)
+@pytest.mark.parametrize("rank_map", [L.RANKMAP_TP_FAST, L.RANKMAP_DP_FAST])
+def test_weight_sync_emulated(model, W, tp, dp, ep, rank_map):
+    man = manifest(model)
+    hd = MODELS[model].head_dim
+    plan = P.Plan(man, head_dim=hd, world=W, tp=tp, dp=dp, ep=ep, rank_map=rank_map, tile_bytes=512)
+    m = mgr(W, 0)
+    masters = [[rank_shards(plan, r, seed=2, special_bits=3, kinds=(1,))[(k, 1)] for k, _ in man]
+               for r in range(W)]
+    arenas = [torch.full((max(256, plan.rank_info(g).dst_arena_bytes),), 0xAB, dtype=torch.uint8, device="cuda")
+              for g in range(W)]
+    for r in range(W):
+        m.sync_rank(plan, r, masters[r], arenas)
+    full = full_state(model, seed=2, kinds=(1,), special_bits=3)
+    want = O.weight_sync(master_shards(full, W, O.fsdp_rows), tp, dp, ep, rank_map, hd)
+    for g in range(W):
+        views = P.StateManager.rollout_views(plan, g, arenas[g])
+        assert list(views) == list(want[g])
+        for name, v in views.items():
+            assert np.array_equal(bits_np(v), want[g][name]), (g, name)
+
+
+def test_weight_sync_world1_collective_entry():
+    man = manifest("mid")
+    m = mgr(1, 0)
+    plan = m.plan(man, head_dim=32, tp=1, dp=1)
+    job = P.Job(m, plan, seed=8, slab=False).alloc(kinds=(1,)).init_synthetic(special_bits=3)
+    arena = m.arena(plan)
+    job.sync(arena)
+    full = full_state("mid", seed=8, kinds=(1,), special_bits=3)
+    want = O.weight_sync(master_shards(full, 1, O.fsdp_rows), 1, 1, 1, O.TP_FAST, 32)[0]
+    for name, v in P.StateManager.rollout_views(plan, 0, arena).items():
+        assert np.array_equal(bits_np(v), want[name]), name
+
+
+# ---- o10 multiplex trace (emulated 4 ranks, 4 jobs) ----------------------------------------------------
+def test_multiplex_emulated():
+    W = 4
+    models = ["toy", "toy-tied", "toy-moe", "mid"]
+    layouts = [(2, 2, 1), (1, 4, 1), (2, 2, 2), (2, 2, 1)]
+    seeds = [0, 1, 2, 3]
+    schedule = [0, 1, 2, 3] * 2 + [3, 1]
+    plans = [P.Plan(manifest(mo), head_dim=MODELS[mo].head_dim, world=W, tp=tp, dp=dp, ep=ep, bucket_bytes=1 << 14,
+                    tile_bytes=1024) for mo, (tp, dp, ep) in zip(models, layouts)]
+    mgrs = [mgr(W, r, bucket=1 << 14) for r in range(W)]
+    jobs = [[P.Job(mgrs[r], plans[j], seed=seeds[j], rank=r).alloc().init_synthetic() for r in range(W)]
+            for j in range(4)]
+    for j in range(4):                      # every job starts HOST-resident
+        for r in range(W):
+            jobs[j][r].suspend()
+    resident = None
+    steps = [0] * 4
+    outs = []
+    for j in schedule:
+        ops = O.transition_ops(resident, j)
+        for op, job in ops:
+            for r in range(W):
+                (jobs[job][r].suspend() if op == O.OP_OFFLOAD else jobs[job][r].resume())
+        resident = j
+        for r in range(W):
+            for t, (key, shape) in enumerate(plans[j].manifest):
+                a, _ = plans[j].shard_rows(r, t)
+                re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+                for kd in range(4):
+                    P.synth_mutate(jobs[j][r].shards[(key, kd)], kd, seeds[j], steps[j], key, a * re_)
+        steps[j] += 1
+        arenas = [mgrs[0].arena(plans[j], g) for g in range(W)]
+        for r in range(W):
+            mgrs[0].sync_rank(plans[j], r, jobs[j][r].masters(), arenas)
+        outs.append([{k: bits_np(v) for k, v in P.StateManager.rollout_views(plans[j], g, arenas[g]).items()}
+                     for g in range(W)])
+    # oracle replay
+    ojobs = []
+    for mo, sd, (tp, dp, ep) in zip(models, seeds, layouts):
+        full = full_state(mo, seed=sd)
+        ojobs.append({"manifest": manifest(mo), "tp": tp, "dp": dp, "ep": ep,
+                      "shards": [fsdp_shards(full, W, r, O.fsdp_rows) for r in range(W)]})
+
+    def mut(job, step, key, kind, bits, base):
+        idx = np.arange(base, base + bits.size, dtype=np.uint64)
+        return bits ^ mutation_bits(seeds[job], step, key, kind, idx).reshape(bits.shape)
+
+    # the oracle's sync uses head_dim=None: shapes here are all head-divisible
+    visits, final = O.multiplex_replay(ojobs, schedule, W, mut)
+    for v, (ops, want) in enumerate(visits):
+        for g in range(W):
+            for name, x in want[g].items():
+                assert np.array_equal(outs[v][g][name], x), (v, g, name)
+    for j in range(4):
+        if j != resident:
+            for r in range(W):
+                jobs[j][r].resume()
+        for r in range(W):
+            for k, x in jobs[j][r].shards.items():
+                assert np.array_equal(bits_np(x), final[j][r][k]), (j, r, k)
