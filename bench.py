@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--hugepage", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    ap.add_argument("--cpu-sample-layers", type=int, default=2)
     ap.add_argument("--sync-nccl", action="store_true", help="NCCL send/recv sync transport (baseline)")
     ap.add_argument("--out", default="")
     return ap.parse_args()
@@ -117,10 +117,11 @@ def load_peaks():
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (bounded sample of the same workload)
 # ---------------------------------------------------------------------------
-def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int, reps: int = 1):
-    """Time the oracle's o4 pack, o5 parse, o6 cast and o7 reshard over the
-    first ``layers`` decoder layers of rank 0's FSDP-``world`` shard (+ the
-    final norm).  Returns (GB of state per second, seconds, sample string)."""
+def cpu_oracle_prepare(model: str, world: int, tp: int, ep: int, layers: int):
+    """Inputs of the CPU baseline: the first ``layers`` decoder layers (+ final
+    norm) of rank 0's FSDP-``world`` shard (4 kinds) and every rank's master
+    rows of those tensors.  Returns a callable that runs one timed sample:
+    the oracle's o4 pack, o5 parse, and o6/o7 gather->RNE->reshard."""
     import numpy as np
 
     from oracle import plex_oracle as O
@@ -129,15 +130,7 @@ def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int, rep
     man = [(k, s) for k, s in manifest(model)
            if any(k.startswith(f"model.layers.{l}.") for l in range(layers)) or k == "model.norm.weight"]
     dp = world // tp
-    shards = {}
-    for k, s in man:
-        a, b = O.fsdp_rows(s[0], world, 0)
-        re_ = int(np.prod(s[1:])) if len(s) > 1 else 1
-        for kd in range(4):
-            shards[(k, kd)] = gen_range(0, k, kd, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:]))
-    S = sum(x.nbytes for x in shards.values())
-    # master shards of every rank for the reshard of this sample
-    ms = {}
+    shards, ms = {}, {}
     for k, s in man:
         re_ = int(np.prod(s[1:])) if len(s) > 1 else 1
         parts = []
@@ -145,16 +138,30 @@ def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int, rep
             a, b = O.fsdp_rows(s[0], world, r)
             parts.append(gen_range(0, k, 1, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:])))
         ms[k] = parts
-    t0 = time.perf_counter()
-    for _ in range(reps):
+        a, b = O.fsdp_rows(s[0], world, 0)
+        for kd in range(4):
+            shards[(k, kd)] = parts[0] if kd == 1 else \
+                gen_range(0, k, kd, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:]))
+    S = sum(x.nbytes for x in shards.values())
+
+    def one():
+        t0 = time.perf_counter()
         segs, size = O.slab_layout(man, world, 0)
         slab = O.pack_slab(segs, size, shards)
         O.parse_slab(slab, segs, dict(man))
         O.weight_sync(ms, tp, dp, ep)
-    dt = (time.perf_counter() - t0) / reps
+        dt = time.perf_counter() - t0
+        return S / dt / 1e9, dt
+
     sample = (f"{model} layers[0:{layers}]+norm, rank-0 FSDP-{world} shard ({S / 1e9:.3f} GB state): "
               f"o4 pack + o5 parse + o6/o7 gather-RNE-reshard to TP-{tp}xDP-{dp} (all ranks' outputs)")
-    return S / dt / 1e9, dt, sample
+    return one, sample
+
+
+def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int):
+    one, sample = cpu_oracle_prepare(model, world, tp, ep, layers)
+    v, dt = one()
+    return v, dt, sample
 
 
 def run_reference(a):
@@ -163,12 +170,12 @@ def run_reference(a):
         return
     world = a.gpus
     tp = a.tp or min(2, world)
-    for _ in range(max(0, a.warmup)):
-        pass  # the oracle has no warm state; warm-up steps would only repeat the sample
+    one, sample = cpu_oracle_prepare(a.model, world, tp, a.ep, a.cpu_sample_layers)
+    for _ in range(a.warmup):
+        one()
     vals, secs = [], []
-    sample = ""
     for _ in range(a.steps):
-        v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
+        v, dt = one()
         vals.append(v)
         secs.append(dt)
     v = statistics.median(vals)

@@ -84,72 +84,202 @@ __device__ __forceinline__ void block_reduce_add(Cks c, unsigned long long* out)
 }
 
 // ---- K1 / K2: pack (tensor -> staging) or unpack (staging -> tensor) -------
-// One CTA per PackItem.  The item covers slab bytes [slab_lo, slab_lo+len) of
-// one segment's slot: data bytes (copied, checksummed) then padding (pack
-// writes zeros; unpack skips it).
-template <bool kPack>
-__global__ void __launch_bounds__(kThreads) pack_kernel(const PackItem* __restrict__ items,
-                                                        const SegDev* __restrict__ segs,
-                                                        const uint64_t* __restrict__ ptrs,
-                                                        uint8_t* __restrict__ staging, uint64_t bucket_lo,
-                                                        unsigned long long* __restrict__ cks) {
-    const PackItem it = items[blockIdx.x];
+// Persistent, one CTA per SM, TMA bulk-copy pipeline (cp.async.bulk, SASS
+// UBLKCP): warp 4 lane 0 streams 32 KiB chunks global->shared into a 6-stage
+// ring (mbarrier complete_tx); consumer warps 0-3 fold the R14 checksum from
+// shared memory while consumer thread 0 streams the same stage back out
+// shared->global (bulk_group).  Each stage is released once the bulk store has
+// read it.  Byte ranges that TMA cannot move (a tensor not 16-B aligned, or
+// the <16-B tail of a segment) go through the consumer threads directly;
+// padding bytes of a slot are written as zeros on pack and skipped on unpack.
+// Work: the bucket's PackItems (slot byte ranges <= 64 KiB), strided over CTAs.
+constexpr int kStages = 6;
+constexpr uint32_t kChunk = 32u * 1024u;
+constexpr int kConsumers = 128;
+constexpr int kTmaThreads = kConsumers + 32;
+constexpr size_t kTmaSmem = (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(smem_u32(p)));
+    return r;
+}
+
+// Geometry of one item, identical for producer and consumers.
+struct ItemGeo {
+    uint8_t* tens;      // tensor bytes at the item's first slot byte
+    uint8_t* buf;       // staging bytes at the item's first slot byte
+    uint64_t ib;        // logical index of the item's first element
+    uint32_t len;       // slot bytes of the item
+    uint32_t data;      // data bytes of the item (rest is padding)
+    uint32_t seg;
+    int es;
+    bool vec;           // tensor side 16-B aligned -> bulk copies allowed
+};
+
+__device__ __forceinline__ ItemGeo item_geo(const PackItem& it, const SegDev* segs, const uint64_t* ptrs,
+                                            uint8_t* staging, uint64_t bucket_lo) {
     const SegDev s = segs[it.seg];
-    uint8_t* buf = staging + (it.slab_lo - bucket_lo);
-    uint8_t* tens = reinterpret_cast<uint8_t*>(ptrs[s.ptr_slot]);
+    ItemGeo g;
     const uint64_t o0 = it.slab_lo - s.slab_off;
-    const uint64_t o1 = o0 + it.len;
-    const uint64_t de = o1 < s.bytes ? o1 : s.bytes;   // end of the data part
-    const int es = (int)s.esize;
-    Cks c;
-    if (o0 < de) {
-        const uint64_t n = de - o0;
-        const uint64_t ib = s.index_base + o0 / es;
-        uint8_t* t = tens + o0;
-        const uint8_t* src = kPack ? t : buf;
-        uint8_t* dst = kPack ? buf : t;
-        const bool vec = ((reinterpret_cast<uintptr_t>(t)) & 15) == 0;
-        const uint64_t nv = vec ? n / 16 : 0;
-        const uint32_t epv = 16 / es;
-        uint64_t v = threadIdx.x;
-        for (; v + 3 * kThreads < nv; v += 4 * kThreads) {
-            uint4 a0 = ld_stream(src + 16 * v);
-            uint4 a1 = ld_stream(src + 16 * (v + kThreads));
-            uint4 a2 = ld_stream(src + 16 * (v + 2 * kThreads));
-            uint4 a3 = ld_stream(src + 16 * (v + 3 * kThreads));
-            st_v4(dst + 16 * v, a0);
-            st_v4(dst + 16 * (v + kThreads), a1);
-            st_v4(dst + 16 * (v + 2 * kThreads), a2);
-            st_v4(dst + 16 * (v + 3 * kThreads), a3);
-            c.add_vec(a0, es, ib + v * epv);
-            c.add_vec(a1, es, ib + (v + kThreads) * epv);
-            c.add_vec(a2, es, ib + (v + 2 * kThreads) * epv);
-            c.add_vec(a3, es, ib + (v + 3 * kThreads) * epv);
+    g.tens = reinterpret_cast<uint8_t*>(ptrs[s.ptr_slot]) + o0;
+    g.buf = staging + (it.slab_lo - bucket_lo);
+    g.es = (int)s.esize;
+    g.ib = s.index_base + o0 / s.esize;
+    g.len = it.len;
+    g.data = o0 >= s.bytes ? 0u : (uint32_t)(s.bytes - o0 < it.len ? s.bytes - o0 : it.len);
+    g.seg = it.seg;
+    g.vec = (reinterpret_cast<uintptr_t>(g.tens) & 15) == 0;
+    return g;
+}
+
+// bulk bytes of chunk [co, co + kChunk) of an item
+__device__ __forceinline__ uint32_t chunk_bulk(const ItemGeo& g, uint32_t co) {
+    if (!g.vec || co >= g.data) return 0;
+    const uint32_t e = g.data - co < kChunk ? g.data - co : kChunk;
+    return e & ~15u;
+}
+
+template <bool kPack>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
+                const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
+                unsigned long long* __restrict__ cks) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kChunk);
+    uint64_t* empty = full + kStages;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
         }
-        for (; v < nv; v += kThreads) {
-            uint4 a = ld_stream(src + 16 * v);
-            st_v4(dst + 16 * v, a);
-            c.add_vec(a, es, ib + v * epv);
-        }
-        // scalar head/tail: whole elements after the vector part
-        const uint64_t ne = n / es;
-        for (uint64_t e = nv * epv + threadIdx.x; e < ne; e += kThreads) {
-            uint32_t b;
-            if (es == 4) {
-                b = reinterpret_cast<const uint32_t*>(src)[e];
-                reinterpret_cast<uint32_t*>(dst)[e] = b;
-            } else {
-                b = reinterpret_cast<const uint16_t*>(src)[e];
-                reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)b;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid >= kConsumers) {
+        // ---------------- producer warp ----------------
+        if (tid != kConsumers) return;
+        uint32_t q = 0;
+        for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
+            const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+            const uint8_t* src = kPack ? g.tens : g.buf;
+            for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
+                const int st = (int)(q % kStages);
+                if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+                const uint32_t nb = chunk_bulk(g, co);
+                if (nb) {
+                    mbar_arrive_tx(&full[st], nb);
+                    bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
+                } else {
+                    mbar_arrive(&full[st]);
+                }
             }
-            c.add_elem(b, ib + e);
+        }
+        return;
+    }
+    // ---------------- consumer warps ----------------
+    uint32_t q = 0;
+    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
+        const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+        const uint8_t* src = kPack ? g.tens : g.buf;
+        uint8_t* dst = kPack ? g.buf : g.tens;
+        Cks c;
+        for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
+            const int st = (int)(q % kStages);
+            const uint8_t* sm = smem + (size_t)st * kChunk;
+            const uint32_t nb = chunk_bulk(g, co);
+            const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
+            const uint32_t dend = g.data < cend ? g.data : cend;        // data end within chunk
+            mbar_wait(&full[st], (q / kStages) & 1);
+            if (tid == 0 && nb) {
+                bulk_store(dst + co, sm, nb);
+                bulk_commit();
+            }
+            // checksum of the bulk part from shared memory
+            const uint32_t epv = 16 / g.es;
+            for (uint32_t v = tid; v < nb / 16; v += kConsumers)
+                c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
+            // non-bulk data (misaligned tensor or <16-B tail): element by element
+            const uint32_t t0 = co + nb;
+            if (t0 < dend) {
+                const uint32_t ne = (dend - t0) / g.es;
+                for (uint32_t e = tid; e < ne; e += kConsumers) {
+                    const uint32_t off = t0 + e * g.es;
+                    uint32_t b;
+                    if (g.es == 4) {
+                        b = *reinterpret_cast<const uint32_t*>(src + off);
+                        *reinterpret_cast<uint32_t*>(dst + off) = b;
+                    } else {
+                        b = *reinterpret_cast<const uint16_t*>(src + off);
+                        *reinterpret_cast<uint16_t*>(dst + off) = (uint16_t)b;
+                    }
+                    c.add_elem(b, g.ib + off / g.es);
+                }
+            }
+            (void)epv;
+            if (kPack && dend < cend) {
+                const uint32_t p0 = co > g.data ? co : g.data;
+                for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
+            }
+            consumers_sync();                       // every consumer done reading stage st
+            if (tid == 0) {
+                if (nb) bulk_wait_read_all();       // bulk store done reading stage st
+                mbar_arrive(&empty[st]);
+            }
+        }
+        if (g.data) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
+                c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
+            }
+            if ((tid & 31) == 0) {
+                atomicAdd(cks + 2 * g.seg, c.s1);
+                atomicAdd(cks + 2 * g.seg + 1, c.s2);
+            }
         }
     }
-    if (kPack && de < o1) {   // zero padding (< 256 B)
-        const uint64_t p0 = (o0 > de ? o0 : de) - o0;
-        for (uint64_t b = p0 + threadIdx.x; b < it.len; b += kThreads) buf[b] = 0;
-    }
-    if (o0 < de) block_reduce_add(c, cks + 2 * it.seg);
+    if (tid == 0) bulk_wait_all();                 // writes complete before exit
 }
 
 __global__ void verify_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
@@ -291,11 +421,26 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 }
 
 // ---- launchers ----------------------------------------------------------------
+static int g_num_sms = 0;
+static bool g_smem_set[2] = {false, false};
+
 cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                         uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
     if (n_items == 0) return cudaSuccess;
-    if (pack) pack_kernel<true><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, staging, bucket_lo, cks);
-    else pack_kernel<false><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, staging, bucket_lo, cks);
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    auto kern = pack ? pack_kernel<true> : pack_kernel<false>;
+    if (!g_smem_set[pack]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+        if (e != cudaSuccess) return e;
+        g_smem_set[pack] = true;
+    }
+    const uint32_t grid = n_items < (uint32_t)g_num_sms ? n_items : (uint32_t)g_num_sms;
+    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo, cks);
     return cudaGetLastError();
 }
 
