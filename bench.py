@@ -2,15 +2,18 @@
 """Benchmark of the B200 state-transition hot path (BASELINE.json metric:
 "state-switch latency (ms) and GB/s vs HBM/host-link/NVLink peak").
 
-One STEP = one pass of the whole hot path over one job's
-synthetic Qwen2.5-7B-shaped state on the GPU group:
-    suspend (a3 gather-pack + a4 D2H into the pinned slab)
-    resume  (a6 H2D + a7 scatter-unpack + checksum verify)
-    sync    (a8 fp32->bf16 RNE + a9-a11 reshard into the rollout layout)
+One STEP = one pass of the whole hot path on the GPU group
+shared by two synthetic Qwen2.5-7B-shaped jobs A and B: the context switch of
+PAPER.md:555 (resident A -> incoming B = [OFFLOAD A, ONLOAD B]) followed by the
+train->rollout weight sync of B; the next step switches back.
+    suspend A (a3 gather-pack + a4 D2H into A's pinned slab)
+    resume  B (a6 H2D + a7 scatter-unpack + checksum verify)   -- concurrent with
+              the suspend when both jobs fit in HBM (duplex, NEXT-1)
+    sync    B (a8 fp32->bf16 RNE + a9-a11 reshard into the rollout layout)
 Workload at N GPUs: FSDP-N shards -> rollout TP-min(2,N) x DP-N/TP (configs[1]
-is N=8: FSDP-8 -> TP-2 x DP-4).  ``value`` = state bytes switched by all ranks
-per second (sum over ranks of the per-rank state S, ÷ the max-over-ranks step
-time); ``ms_per_step`` is the switch latency.
+is N=8: FSDP-8 -> TP-2 x DP-4).  ``value`` = state bytes moved through the
+switch by all ranks per second (sum over ranks of S_out + S_in, ÷ the
+max-over-ranks step time); ``ms_per_step`` is the switch + sync latency.
 
     python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
     python bench.py --impl reference ...                        # the CPU oracle
@@ -42,9 +45,10 @@ def parse():
     ap.add_argument("--model", default="qwen2.5-7b")
     ap.add_argument("--tp", type=int, default=0, help="rollout TP (default min(2, N))")
     ap.add_argument("--ep", type=int, default=1)
-    ap.add_argument("--bucket-mb", type=int, default=64)
+    ap.add_argument("--bucket-mb", type=int, default=256)
     ap.add_argument("--slots", type=int, default=3)
     ap.add_argument("--hugepage", action="store_true")
+    ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=2)
@@ -221,6 +225,13 @@ def run_plex(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def allmin(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
+
     def allsum(x: float) -> float:
         if world == 1:
             return x
@@ -236,13 +247,23 @@ def run_plex(a):
     mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=a.slots, timing=True,
                          sync_nccl=a.sync_nccl)
     t0 = time.perf_counter()
-    plan = mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep)
-    plan_s = time.perf_counter() - t0
+    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep) for _ in range(2)]
+    plan_s = (time.perf_counter() - t0) / 2
+    plan = plans[0]
     info = plan.rank_info(rank)
-    job = P.Job(mgr, plan, seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+    # two jobs of the same shape (seeds 1, 2): B starts suspended in its slab,
+    # A resident -- one resident job per GPU group (R17)
+    job_b = P.Job(mgr, plans[1], seed=2, hugepage=a.hugepage).alloc().init_synthetic()
+    job_b.suspend()
+    job_a = P.Job(mgr, plans[0], seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+    jobs = [job_a, job_b]
     arena = mgr.arena(plan)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
+    # duplex switch (offload A || onload B) needs both jobs on the device at once
+    free, total = torch.cuda.mem_get_info(local)
+    duplex = (not a.no_duplex) and (info.payload_bytes + (4 << 30) < free)
+    duplex = allmin(1.0 if duplex else 0.0) > 0.5
 
     # host-link roofline BW_host(k = world): pinned copy of 4 GiB, all ranks at once
     probe = 4 << 30
@@ -263,10 +284,28 @@ def run_plex(a):
     del h, dbuf
     torch.cuda.empty_cache()
 
-    def step():
-        job.suspend(release=False)
-        job.resume()
-        job.sync(arena)
+    phase_ev = []
+    cur = {"i": 0}
+
+    def step(record=False):
+        """PAPER.md:555 transition: resident A -> incoming B = [OFFLOAD A, ONLOAD B], then SYNC B."""
+        i = cur["i"]
+        out, inc = jobs[i], jobs[1 - i]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
+        if ev:
+            ev[0].record()
+        if duplex:
+            out.switch_to(inc)
+        else:
+            out.suspend()
+            inc.resume()
+        if ev:
+            ev[1].record()
+        inc.sync(arena)
+        if ev:
+            ev[2].record()
+            phase_ev.append(ev)
+        cur["i"] = 1 - i
 
     for _ in range(a.warmup):
         step()
@@ -278,33 +317,33 @@ def run_plex(a):
     barrier()
     e0.record()
     for _ in range(a.steps):
-        step()
+        step(record=True)
     e1.record()
     barrier()
     clk = clocks.stop()
+    phases = {n: allmax(sum(ev[i].elapsed_time(ev[i + 1]) for ev in phase_ev) / a.steps)
+              for i, n in enumerate(("switch", "sync"))}
     ms_local = e0.elapsed_time(e1) / a.steps
     ms = allmax(ms_local)
     st = mgr.stats()
 
-    # end-to-end through the public API: state starts and ends in pinned host
-    # memory (release/re-acquire of device storage included), host clock.
+    # end-to-end through the public API (Job.switch_to / suspend+resume, Job.sync),
+    # host clock: every step H2D-copies the incoming job's state (the step's input)
+    # from pinned host memory and D2H-copies the outgoing job's state (its result),
+    # with release / re-acquire of device storage.
     e2e_steps = a.steps if a.e2e_steps < 0 else a.e2e_steps
     e2e = None
     if e2e_steps > 0:
-        job.suspend()                       # state now HOST-resident, device storage released
         barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            job.resume()                    # H2D of the step's input (the job state)
-            job.sync(arena)
-            job.suspend()                   # D2H of the step's result (the updated state)
+            step()
+        torch.cuda.synchronize()
         barrier()
         e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
-        job.resume()
-        e2e = {"S": info.payload_bytes, "s": e2e_s, "h2d": info.slab_bytes,
-               "d2h": info.slab_bytes + 16 * info.n_segments}
+        e2e = {"s": e2e_s, "h2d": info.slab_bytes, "d2h": info.slab_bytes + 16 * info.n_segments}
 
-    S_total = allsum(float(info.payload_bytes))
+    S_total = allsum(float(2 * info.payload_bytes))      # offloaded + onloaded state per switch
     value = S_total / (ms * 1e-3) / 1e9
     peak_hbm, peak_kind = load_peaks()
 
@@ -338,15 +377,17 @@ def run_plex(a):
             rl["host_" + k] = {"bound": "host_link", "achieved": round(gbs, 2), "peak": round(ref, 2),
                                "unit": "GB/s", "frac": frac(gbs, ref),
                                "peak_kind": f"measured pinned copy, {world} GPU(s) concurrently"}
-    if "push" in kern and world > 1:
-        nv = max(info.send_bytes, info.recv_bytes)
-        nv = allmax(float(nv))
-        t_push = allmax(kern["push"]["ms"] / a.steps)
-        gbs = nv / (t_push * 1e-3) / 1e9
+    if world > 1:
+        # NVLink: max over ranks of max(send, recv) bytes over the whole sync call
+        nv = allmax(float(max(info.send_bytes, info.recv_bytes)))
+        gbs = nv / (phases["sync"] * 1e-3) / 1e9
         rl["nvlink"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s",
-                        "frac": frac(gbs, 900.0), "bytes_max_rank": nv,
+                        "frac": frac(gbs, 900.0), "bytes_max_rank": nv, "over": "whole sync call (max over ranks)",
                         "peak_kind": "nominal 900 GB/s/dir (measured peer copy ref 770)"}
-    # our kernel launches per timed step: pack + unpack + push + 1 verify per onload
+        if st["nccl"]["launches"]:
+            rl["nccl_exchange"] = {"ms_per_step": round(st["nccl"]["ms"] / a.steps, 3),
+                                   "rounds_per_step": st["nccl"]["launches"] / a.steps}
+    # our kernel launches in the timed region: pack + unpack + push (+NCCL-path K4/K5) + 1 verify per onload
     launches = sum(v["launches"] for v in kern.values()) + a.steps
     if rank == 0:
         line = {
@@ -354,10 +395,13 @@ def run_plex(a):
             "warmup": a.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16/fp32 bits (byte copy; fp32->bf16 RNE integer cast)",
             "data": "synthetic (counter-based generator, DESIGN.md §3); random-init Qwen2.5-7B-shaped state",
-            "config": {"workload": f"{a.model} state (bf16 param + fp32 master/m/v) FSDP-{world} -> rollout "
-                                   f"TP-{tp}xDP-{dp}: suspend+resume+sync per step",
-                       "model_shape": a.model, "state_bytes_per_rank": info.payload_bytes,
-                       "state_bytes_total": int(S_total), "bucket_bytes": bucket, "staging_slots": a.slots,
+            "config": {"workload": f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
+                                   f"rollout TP-{tp}xDP-{dp}; step = context switch A->B (full suspend of A + full "
+                                   f"resume of B, {'duplex: offload || onload' if duplex else 'sequential'}) + "
+                                   f"weight sync of B",
+                       "model_shape": a.model, "state_bytes_per_rank_per_job": info.payload_bytes,
+                       "bytes_switched_per_step": int(S_total), "duplex": duplex,
+                       "bucket_bytes": bucket, "staging_slots": a.slots,
                        "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
                        "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
                        "sync_transport": "nccl" if a.sync_nccl else "nvlink-push"},
@@ -366,6 +410,7 @@ def run_plex(a):
                          "algorithmic_bytes_per_launch": int(per_launch_bytes), "avg_launch_ms": round(avg_ms, 4),
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "rooflines": rl,
+            "phases_ms": {k: round(v, 3) for k, v in phases.items()},
             "clocks": clk,
             "gpu_launches": int(launches),
         }
@@ -373,7 +418,8 @@ def run_plex(a):
             line["e2e"] = {"value": round(S_total / e2e["s"] / 1e9, 3), "unit": "GB/s",
                            "ms_per_step": round(e2e["s"] * 1e3, 2), "h2d_bytes_per_step": e2e["h2d"],
                            "d2h_bytes_per_step": e2e["d2h"],
-                           "api": "Job.resume -> Job.sync -> Job.suspend(release) (host clock)"}
+                           "api": "Job.switch_to (or suspend+resume) with storage release/acquire -> Job.sync "
+                                  "(host clock)"}
         if not a.no_cpu_baseline and world == 1:
             v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
             line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
@@ -383,7 +429,7 @@ def run_plex(a):
             with open(a.out, "w") as f:
                 json.dump(line, f, indent=1)
     barrier()
-    del job, arena
+    del jobs, job_a, job_b, arena
     mgr.close()
     if world > 1:
         dist.destroy_process_group()

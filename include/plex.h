@@ -264,6 +264,20 @@ PLEX_API plex_status plex_state_offload(plex_ctx_t ctx, plex_plan_t plan, const 
 PLEX_API plex_status plex_state_onload(plex_ctx_t ctx, plex_plan_t plan, plex_slab_t slab, void* const* dst,
                               int32_t n_dst, void* caller_stream);
 
+/* ---- NEXT-1: duplex switch (offload A || onload B) ------------------------ */
+/* The context switch of PAPER.md:555 (OFFLOAD resident A, ONLOAD incoming B)
+ * as one call whose two halves run concurrently: A's buckets go D2H on
+ * ctx's copy stream while B's come H2D on a second, library-owned copy
+ * stream, so the switch costs ~max(T_offload, T_load) instead of the sum
+ * C_setup = T_offload + T_load of Eq. 3.  src_out/dst_in
+ * as in plex_state_offload/onload (each half skipped if already done).  Needs
+ * staging >= n_slots x (bucket_out + bucket_in).  Blocking; residencies flip
+ * per half on success; E_CHECKSUM if B fails verification (B stays HOST, A
+ * is HOST and its slab valid). */
+PLEX_API plex_status plex_state_switch(plex_ctx_t ctx, plex_plan_t plan_out, const void* const* src_out, int32_t n_src,
+                                       plex_slab_t slab_out, plex_plan_t plan_in, plex_slab_t slab_in,
+                                       void* const* dst_in, int32_t n_dst, void* caller_stream);
+
 /* ---- a8 - a11: train -> rollout weight sync ------------------------------- */
 /* Collective over the ctx's world.  src_master[t] = this rank's fp32 master
  * shard of tensor t (FSDP-world rows).  dst_arena = this rank's bf16 rollout

@@ -32,7 +32,7 @@ EXPORTS = [
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_checksums",
-    "plex_state_offload", "plex_state_onload", "plex_weight_sync", "plex_weight_sync_rank",
+    "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
 
@@ -111,6 +111,7 @@ def _load() -> C.CDLL:
         "plex_slab_checksums": (C.c_int, [VP, P(U64), I32]),
         "plex_state_offload": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_state_onload": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),
+        "plex_state_switch": (C.c_int, [VP, VP, P(VP), I32, VP, VP, VP, P(VP), I32, VP]),
         "plex_weight_sync": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_weight_sync_rank": (C.c_int, [VP, VP, I32, P(VP), I32, P(VP), I32, VP]),
         "plex_synth_fill": (C.c_int, [VP, I32, U64, C.c_char_p, U64, U64, I32, VP]),

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "plex_internal.h"
 
@@ -93,11 +94,6 @@ __device__ __forceinline__ void block_reduce_add(Cks c, unsigned long long* out)
 // the <16-B tail of a segment) go through the consumer threads directly;
 // padding bytes of a slot are written as zeros on pack and skipped on unpack.
 // Work: the bucket's PackItems (slot byte ranges <= 64 KiB), strided over CTAs.
-constexpr int kStages = 6;
-constexpr uint32_t kChunk = 32u * 1024u;
-constexpr int kConsumers = 128;
-constexpr int kTmaThreads = kConsumers + 32;
-constexpr size_t kTmaSmem = (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -133,8 +129,8 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ uint4 lds128(const void* p) {
     uint4 r;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -171,33 +167,48 @@ __device__ __forceinline__ ItemGeo item_geo(const PackItem& it, const SegDev* se
     return g;
 }
 
-// bulk bytes of chunk [co, co + kChunk) of an item
-__device__ __forceinline__ uint32_t chunk_bulk(const ItemGeo& g, uint32_t co) {
+// bulk bytes of chunk [co, co + chunk) of an item
+__device__ __forceinline__ uint32_t chunk_bulk(const ItemGeo& g, uint32_t co, uint32_t chunk) {
     if (!g.vec || co >= g.data) return 0;
-    const uint32_t e = g.data - co < kChunk ? g.data - co : kChunk;
+    const uint32_t e = g.data - co < chunk ? g.data - co : chunk;
     return e & ~15u;
 }
 
-template <bool kPack>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int STAGES, int CHUNK_KB, int CWARPS, int CTAS>
+struct TmaCfg {
+    static constexpr int kStages = STAGES;
+    static constexpr uint32_t kChunk = (uint32_t)CHUNK_KB * 1024u;
+    static constexpr int kConsumers = CWARPS * 32;
+    static constexpr int kThreads = kConsumers + 32;
+    static constexpr int kCtasPerSm = CTAS;
+    static constexpr size_t kSmem = (size_t)STAGES * kChunk + 2 * STAGES * sizeof(uint64_t);
+};
+
+template <bool kPack, class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
                 const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
                 unsigned long long* __restrict__ cks) {
+    constexpr int kStages = Cfg::kStages;
+    constexpr uint32_t kChunk = Cfg::kChunk;
+    constexpr int kConsumers = Cfg::kConsumers;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kChunk);
     uint64_t* empty = full + kStages;
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            // released by every consumer warp (done reading) + the bulk store (done reading)
+            mbar_init(&empty[i], kConsumers / 32 + 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (tid >= kConsumers) {
-        // ---------------- producer warp ----------------
+        // ---------------- producer warp: TMA loads ----------------
         if (tid != kConsumers) return;
         uint32_t q = 0;
         for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
                 const int st = (int)(q % kStages);
                 if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
-                const uint32_t nb = chunk_bulk(g, co);
+                const uint32_t nb = chunk_bulk(g, co, kChunk);
                 if (nb) {
                     mbar_arrive_tx(&full[st], nb);
                     bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         return;
     }
-    // ---------------- consumer warps ----------------
+    // ---------------- consumer warps: checksum + TMA stores ----------------
     uint32_t q = 0;
     for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
         const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
@@ -227,16 +238,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
             const int st = (int)(q % kStages);
             const uint8_t* sm = smem + (size_t)st * kChunk;
-            const uint32_t nb = chunk_bulk(g, co);
+            const uint32_t nb = chunk_bulk(g, co, kChunk);
             const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
             const uint32_t dend = g.data < cend ? g.data : cend;        // data end within chunk
             mbar_wait(&full[st], (q / kStages) & 1);
             if (tid == 0 && nb) {
-                bulk_store(dst + co, sm, nb);
+                bulk_store(dst + co, sm, nb);                           // write back while we checksum
                 bulk_commit();
             }
-            // checksum of the bulk part from shared memory
-            const uint32_t epv = 16 / g.es;
+            // checksum of the bulk part, read back from shared memory
             for (uint32_t v = tid; v < nb / 16; v += kConsumers)
                 c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
             // non-bulk data (misaligned tensor or <16-B tail): element by element
@@ -256,14 +266,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     c.add_elem(b, g.ib + off / g.es);
                 }
             }
-            (void)epv;
             if (kPack && dend < cend) {
                 const uint32_t p0 = co > g.data ? co : g.data;
                 for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
             }
-            consumers_sync();                       // every consumer done reading stage st
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);                     // this warp is done with stage st
             if (tid == 0) {
-                if (nb) bulk_wait_read_all();       // bulk store done reading stage st
+                if (nb) bulk_wait_read_all();                           // the bulk store has read stage st
                 mbar_arrive(&empty[st]);
             }
         }
@@ -273,13 +283,72 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
                 c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
             }
-            if ((tid & 31) == 0) {
+            if (lane == 0) {
                 atomicAdd(cks + 2 * g.seg, c.s1);
                 atomicAdd(cks + 2 * g.seg + 1, c.s2);
             }
         }
     }
-    if (tid == 0) bulk_wait_all();                 // writes complete before exit
+    if (tid == 0) bulk_wait_all();                 // every bulk store complete before exit
+}
+
+// LDG/STG variant (experiment): persistent CTAs, 8 independent 16-B loads in
+// flight per thread, checksum in registers, warp-level atomics per item.
+template <bool kPack>
+__global__ void __launch_bounds__(256, 4)
+    pack_ldg_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
+                    const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
+                    unsigned long long* __restrict__ cks) {
+    constexpr int U = 8;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
+        const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+        const uint8_t* src = kPack ? g.tens : g.buf;
+        uint8_t* dst = kPack ? g.buf : g.tens;
+        Cks c;
+        const uint32_t nv = g.vec ? g.data / 16 : 0;
+        const uint32_t epv = 16 / g.es;
+        uint32_t v = tid;
+        for (; v + (U - 1) * 256 < nv; v += U * 256) {
+            uint4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = ld_stream(src + 16ull * (v + u * 256));
+#pragma unroll
+            for (int u = 0; u < U; ++u) st_v4(dst + 16ull * (v + u * 256), x[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) c.add_vec(x[u], g.es, g.ib + (uint64_t)(v + u * 256) * epv);
+        }
+        for (; v < nv; v += 256) {
+            const uint4 x = ld_stream(src + 16ull * v);
+            st_v4(dst + 16ull * v, x);
+            c.add_vec(x, g.es, g.ib + (uint64_t)v * epv);
+        }
+        const uint32_t ne = g.data / g.es;
+        for (uint32_t e = nv * epv + tid; e < ne; e += 256) {
+            uint32_t b;
+            if (g.es == 4) {
+                b = reinterpret_cast<const uint32_t*>(src)[e];
+                reinterpret_cast<uint32_t*>(dst)[e] = b;
+            } else {
+                b = reinterpret_cast<const uint16_t*>(src)[e];
+                reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)b;
+            }
+            c.add_elem(b, g.ib + e);
+        }
+        if (kPack)
+            for (uint32_t b = g.data + tid; b < g.len; b += 256) dst[b] = 0;
+        if (g.data) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
+                c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
+            }
+            if (lane == 0) {
+                atomicAdd(cks + 2 * g.seg, c.s1);
+                atomicAdd(cks + 2 * g.seg + 1, c.s2);
+            }
+        }
+    }
 }
 
 __global__ void verify_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
@@ -304,45 +373,54 @@ __device__ __forceinline__ uint4 rne_8(const uint4& a, const uint4& b) {
 
 // ---- K3+K4: fused cast + reshard push ---------------------------------------
 // One CTA per PushItem: rows x cols fp32 rectangle of this rank's master shard
-// -> RNE -> bf16 rectangle of destination rank dst_rank's arena, which is a
-// peer-mapped pointer (NVLink store) unless dst_rank is this rank.
+// -> RNE -> bf16 rectangle of destination dst_rank's buffer, which is a
+// peer-mapped arena (NVLink store), the local arena, or (NCCL baseline, K4) a
+// send segment.  kCast = false is K5 of the NCCL baseline: a bf16 -> bf16
+// rectangle copy from a receive segment into the arena.
+template <bool kCast>
 __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restrict__ items,
                                                         const uint64_t* __restrict__ src_ptrs,
                                                         const uint64_t* __restrict__ dst_arenas) {
     const PushItem it = items[blockIdx.x];
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(src_ptrs[it.tensor]) + it.src_elem;
+    constexpr int kSrcEs = kCast ? 4 : 2;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(src_ptrs[it.tensor]) + (uint64_t)it.src_elem * kSrcEs;
     uint16_t* dst = reinterpret_cast<uint16_t*>(dst_arenas[it.dst_rank]) + it.dst_elem;
     const uint32_t rows = it.rows, cols = it.cols, ss = it.src_stride, ds = it.dst_stride;
     const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
-                     (cols % 8 == 0) && (ss % 4 == 0) && (ds % 8 == 0);
+                     (cols % 8 == 0) && ((ss * kSrcEs) % 16 == 0) && (ds % 8 == 0);
+    auto load8 = [&](uint64_t e) -> uint4 {      // 8 elements starting at source element e
+        if (kCast) {
+            const uint4 a = ld_stream(src + 4 * e), b = ld_stream(src + 4 * e + 16);
+            return rne_8(a, b);
+        } else {
+            return ld_stream(src + 2 * e);
+        }
+    };
     if (vec) {
         const uint32_t vpr = cols / 8;
         const uint32_t total = rows * vpr;
         if (rows == 1) {
             uint32_t v = threadIdx.x;
             for (; v + kThreads < total; v += 2 * kThreads) {
-                const uint4 a0 = ld_stream(src + 8 * v), b0 = ld_stream(src + 8 * v + 4);
-                const uint4 a1 = ld_stream(src + 8 * (v + kThreads)), b1 = ld_stream(src + 8 * (v + kThreads) + 4);
-                st_v4(dst + 8 * v, rne_8(a0, b0));
-                st_v4(dst + 8 * (v + kThreads), rne_8(a1, b1));
+                const uint4 x0 = load8(8ull * v);
+                const uint4 x1 = load8(8ull * (v + kThreads));
+                st_v4(dst + 8ull * v, x0);
+                st_v4(dst + 8ull * (v + kThreads), x1);
             }
-            for (; v < total; v += kThreads) {
-                const uint4 a = ld_stream(src + 8 * v), b = ld_stream(src + 8 * v + 4);
-                st_v4(dst + 8 * v, rne_8(a, b));
-            }
+            for (; v < total; v += kThreads) st_v4(dst + 8ull * v, load8(8ull * v));
         } else {
             for (uint32_t v = threadIdx.x; v < total; v += kThreads) {
                 const uint32_t r = v / vpr, c = v - r * vpr;
-                const uint32_t* s = src + (uint64_t)r * ss + 8 * c;
-                const uint4 a = ld_stream(s), b = ld_stream(s + 4);
-                st_v4(dst + (uint64_t)r * ds + 8 * c, rne_8(a, b));
+                st_v4(dst + (uint64_t)r * ds + 8 * c, load8((uint64_t)r * ss + 8 * c));
             }
         }
     } else {
         const uint64_t total = (uint64_t)rows * cols;
         for (uint64_t e = threadIdx.x; e < total; e += kThreads) {
             const uint64_t r = e / cols, c = e - r * cols;
-            dst[r * ds + c] = (uint16_t)rne_bf16(src[r * ss + c]);
+            const uint64_t si = r * ss + c;
+            dst[r * ds + c] = kCast ? (uint16_t)rne_bf16(reinterpret_cast<const uint32_t*>(src)[si])
+                                    : reinterpret_cast<const uint16_t*>(src)[si];
         }
     }
 }
@@ -422,7 +500,41 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 
 // ---- launchers ----------------------------------------------------------------
 static int g_num_sms = 0;
-static bool g_smem_set[2] = {false, false};
+static int g_variant = -1;
+
+template <bool kPack, class Cfg>
+static cudaError_t launch_tma(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                              uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Cfg::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const uint32_t cap = (uint32_t)g_num_sms * Cfg::kCtasPerSm;
+    const uint32_t grid = n_items < cap ? n_items : cap;
+    pack_kernel<kPack, Cfg><<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo, cks);
+    return cudaGetLastError();
+}
+
+template <bool kPack>
+static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                                 uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
+    switch (g_variant) {
+        case 1: return launch_tma<kPack, TmaCfg<12, 16, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 2: return launch_tma<kPack, TmaCfg<6, 16, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 3: return launch_tma<kPack, TmaCfg<4, 48, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 4: {
+            const uint32_t cap = (uint32_t)g_num_sms * 4;
+            pack_ldg_kernel<kPack><<<n_items < cap ? n_items : cap, 256, 0, s>>>(items, n_items, segs, ptrs, staging,
+                                                                              bucket_lo, cks);
+            return cudaGetLastError();
+        }
+        case 5: return launch_tma<kPack, TmaCfg<3, 32, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        default: return launch_tma<kPack, TmaCfg<6, 32, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+    }
+}
 
 cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                         uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
@@ -433,15 +545,12 @@ cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, cons
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
     }
-    auto kern = pack ? pack_kernel<true> : pack_kernel<false>;
-    if (!g_smem_set[pack]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-        if (e != cudaSuccess) return e;
-        g_smem_set[pack] = true;
+    if (g_variant < 0) {
+        const char* v = getenv("PLEX_PACK_VARIANT");
+        g_variant = v ? atoi(v) : 0;
     }
-    const uint32_t grid = n_items < (uint32_t)g_num_sms ? n_items : (uint32_t)g_num_sms;
-    kern<<<grid, kTmaThreads, kTmaSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo, cks);
-    return cudaGetLastError();
+    return pack ? launch_pack_t<true>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s)
+                : launch_pack_t<false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
 }
 
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
@@ -452,13 +561,14 @@ cudaError_t launch_verify(const unsigned long long* got, const unsigned long lon
     return cudaGetLastError();
 }
 
-cudaError_t launch_push(const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs, const uint64_t* dst_arenas,
-                        cudaStream_t s) {
+cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
+                        const uint64_t* dst_arenas, cudaStream_t s) {
     // grid.x limit is 2^31-1; chunk very long item lists
     const uint64_t kMax = 1ull << 30;
     for (uint64_t o = 0; o < n_items; o += kMax) {
         const uint64_t n = n_items - o < kMax ? n_items - o : kMax;
-        push_kernel<<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
+        if (cast) push_kernel<true><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
+        else push_kernel<false><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
     }
     return cudaGetLastError();
 }

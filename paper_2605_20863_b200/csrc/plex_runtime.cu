@@ -26,8 +26,8 @@ cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, cons
                         uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s);
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
                           cudaStream_t s);
-cudaError_t launch_push(const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs, const uint64_t* dst_arenas,
-                        cudaStream_t s);
+cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
+                        const uint64_t* dst_arenas, cudaStream_t s);
 cudaError_t launch_cast(const void* src, void* dst, uint64_t n, cudaStream_t s);
 cudaError_t launch_synth(void* dst, int kind, uint64_t base, uint64_t index_base, uint64_t n, int special_bits,
                          cudaStream_t s);
@@ -61,7 +61,18 @@ struct DevPlan {
     PushItem* push = nullptr;
     unsigned long long* cks = nullptr;        // computed (S1,S2) per segment
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
+    unsigned long long* cks_in = nullptr;     // recomputed at onload
     std::vector<uint64_t> bucket_payload;     // data bytes per bucket (stats)
+    // NCCL-baseline schedule (built lazily for one per-pair round quota Q)
+    uint64_t nq = 0;                          // Q it was built for (0 = none)
+    int rounds = 0;
+    PushItem* local = nullptr;                // local rectangles: cast straight into the arena
+    uint64_t n_local = 0, local_bytes = 0;
+    PushItem* rpack = nullptr;                // K4: cast into send segments, per round
+    PushItem* runpack = nullptr;              // K5: receive segments -> arena, per round
+    std::vector<uint64_t> rpack_start, runpack_start;   // rounds + 1
+    std::vector<uint64_t> rpack_bytes, runpack_bytes;   // algorithmic bytes per round
+    std::vector<uint64_t> send_bytes, recv_bytes;       // rounds * world
 };
 
 struct Timed {
@@ -94,6 +105,12 @@ struct plex_ctx_s {
     uint64_t* h_ptrs = nullptr;
     uint64_t* d_ptrs = nullptr;
     size_t ptr_cap = 0;
+    // second half of a duplex switch (NEXT-1): own pointer table, streams, events
+    uint64_t* h_ptrs2 = nullptr;
+    uint64_t* d_ptrs2 = nullptr;
+    size_t ptr_cap2 = 0;
+    cudaStream_t pack2 = nullptr, copy2 = nullptr;     // library-owned, created lazily
+    std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
     // small device scratch for NCCL barriers and handle exchange
@@ -103,7 +120,7 @@ struct plex_ctx_s {
     // peer arenas opened over CUDA IPC: rank -> (handle bytes, mapped base)
     std::map<int, std::pair<std::vector<uint8_t>, void*>> peers;
     std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
-    // NCCL-baseline staging views (send | recv halves of `staging`)
+    cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
 };
 
 struct plex_slab_s {
@@ -129,6 +146,10 @@ static void free_devplan(DevPlan& d) {
     cudaFree(d.push);
     cudaFree(d.cks);
     cudaFree(d.cks_want);
+    cudaFree(d.cks_in);
+    cudaFree(d.local);
+    cudaFree(d.rpack);
+    cudaFree(d.runpack);
     d = DevPlan{};
 }
 
@@ -152,7 +173,8 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
         return s;
     }
     const size_t nck = std::max<size_t>(1, 2 * R.segs.size());
-    if (cudaMalloc(&d.cks, nck * 8) != cudaSuccess || cudaMalloc(&d.cks_want, nck * 8) != cudaSuccess) {
+    if (cudaMalloc(&d.cks, nck * 8) != cudaSuccess || cudaMalloc(&d.cks_want, nck * 8) != cudaSuccess ||
+        cudaMalloc(&d.cks_in, nck * 8) != cudaSuccess) {
         free_devplan(d);
         set_error("cudaMalloc of checksum tables failed");
         return PLEX_E_CUDA;
@@ -169,19 +191,20 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     return PLEX_OK;
 }
 
-static plex_status ensure_ptrs(plex_ctx_s* c, size_t n) {
-    if (n <= c->ptr_cap) return PLEX_OK;
-    size_t cap = std::max<size_t>(n, 2 * c->ptr_cap);
-    cudaFreeHost(c->h_ptrs);
-    cudaFree(c->d_ptrs);
-    c->h_ptrs = nullptr;
-    c->d_ptrs = nullptr;
-    c->ptr_cap = 0;
-    CK(cudaHostAlloc(&c->h_ptrs, cap * 8, cudaHostAllocDefault));
-    CK(cudaMalloc(&c->d_ptrs, cap * 8));
-    c->ptr_cap = cap;
+static plex_status ensure_table(uint64_t** h, uint64_t** d, size_t* capp, size_t n) {
+    if (n <= *capp) return PLEX_OK;
+    size_t cap = std::max<size_t>(n, 2 * *capp);
+    cudaFreeHost(*h);
+    cudaFree(*d);
+    *h = nullptr;
+    *d = nullptr;
+    *capp = 0;
+    CK(cudaHostAlloc(h, cap * 8, cudaHostAllocDefault));
+    CK(cudaMalloc(d, cap * 8));
+    *capp = cap;
     return PLEX_OK;
 }
+static plex_status ensure_ptrs(plex_ctx_s* c, size_t n) { return ensure_table(&c->h_ptrs, &c->d_ptrs, &c->ptr_cap, n); }
 
 // ---- timing ------------------------------------------------------------------
 static plex_status timed_begin(plex_ctx_s* c, cudaStream_t s, cudaEvent_t* a) {
@@ -252,21 +275,132 @@ static plex_status check_common(plex_ctx_s* c, plex_plan_t plan) {
     return PLEX_OK;
 }
 
-static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* const* ptrs, int32_t n) {
+static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* const* ptrs, int32_t n, int table = 0) {
     const size_t nt = p.tensors.size();
     if (!ptrs || (size_t)n != PLEX_NUM_KINDS * nt) {
         set_error("expected %zu pointers (4 kinds x %zu tensors), got %d", PLEX_NUM_KINDS * nt, nt, n);
         return PLEX_E_INVAL;
     }
-    plex_status s = ensure_ptrs(c, PLEX_NUM_KINDS * nt);
+    plex_status s = table == 0 ? ensure_ptrs(c, PLEX_NUM_KINDS * nt)
+                               : ensure_table(&c->h_ptrs2, &c->d_ptrs2, &c->ptr_cap2, PLEX_NUM_KINDS * nt);
     if (s) return s;
+    uint64_t* h = table == 0 ? c->h_ptrs : c->h_ptrs2;
     const RankPlan& R = p.ranks[c->rank];
-    for (size_t i = 0; i < PLEX_NUM_KINDS * nt; ++i) c->h_ptrs[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+    for (size_t i = 0; i < PLEX_NUM_KINDS * nt; ++i) h[i] = reinterpret_cast<uint64_t>(ptrs[i]);
     for (const SegDev& sg : R.segs) {
         if (sg.bytes && !ptrs[sg.ptr_slot]) {
             set_error("NULL pointer for tensor %u kind %u", sg.ptr_slot % (uint32_t)nt, sg.ptr_slot / (uint32_t)nt);
             return PLEX_E_INVAL;
         }
+    }
+    return PLEX_OK;
+}
+
+// ---- bucket pipeline halves (a3+a4 offload, a6+a7 onload) -------------------------
+// A Pipe is one direction's staging ring: slot s of a bucket b = b mod n_slots;
+// ev_k[s] = the kernel finished with the slot, ev_c[s] = the copy finished.
+struct Pipe {
+    uint8_t* staging;
+    int n_slots;
+    cudaEvent_t* ev_k;
+    cudaEvent_t* ev_c;
+    cudaStream_t kern;
+    cudaStream_t copy;
+    uint64_t* h_ptrs;
+    uint64_t* d_ptrs;
+};
+
+struct Half {           // one offload or onload in flight
+    const Plan* p;
+    const RankPlan* R;
+    DevPlan* d;
+    plex_slab_s* slab;
+    int32_t nb;
+    std::vector<uint64_t> cks;     // offload: recorded checksums (host)
+};
+
+static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const size_t np = PLEX_NUM_KINDS * h.p->tensors.size();
+    CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
+    CK(cudaMemsetAsync(h.d->cks, 0, 16 * std::max<size_t>(1, h.R->segs.size()), pp.kern));
+    h.nb = n_buckets(*h.p, *h.R);
+    h.cks.assign(2 * h.R->segs.size(), 0);
+    return PLEX_OK;
+}
+
+static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
+    const Plan& p = *h.p;
+    const RankPlan& R = *h.R;
+    const int slot = b % pp.n_slots;
+    uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
+    const uint64_t lo = (uint64_t)b * p.bucket;
+    const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+    if (b >= pp.n_slots) CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
+    const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+    cudaEvent_t ta = nullptr;
+    plex_status st;
+    if ((st = timed_begin(c, pp.kern, &ta))) return st;
+    CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.kern));
+    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_PACK, 2 * h.d->bucket_payload[b]))) return st;
+    CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
+    CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
+    if ((st = timed_begin(c, pp.copy, &ta))) return st;
+    CK(cudaMemcpyAsync(h.slab->host + lo, stg, len, cudaMemcpyDeviceToHost, pp.copy));
+    if ((st = timed_end(c, pp.copy, ta, PLEX_STAT_D2H, len))) return st;
+    CK(cudaEventRecord(pp.ev_c[slot], pp.copy));
+    return PLEX_OK;
+}
+
+static plex_status off_end(plex_ctx_s* c, Pipe& pp, Half& h) {
+    (void)c;
+    if (!h.cks.empty()) CK(cudaMemcpyAsync(h.cks.data(), h.d->cks, 8 * h.cks.size(), cudaMemcpyDeviceToHost, pp.kern));
+    return PLEX_OK;
+}
+
+static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const size_t np = PLEX_NUM_KINDS * h.p->tensors.size();
+    const size_t nck = 2 * h.R->segs.size();
+    CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
+    CK(cudaMemsetAsync(h.d->cks_in, 0, 8 * std::max<size_t>(2, nck), pp.kern));
+    if (nck) CK(cudaMemcpyAsync(h.d->cks_want, h.slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, pp.kern));
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
+    h.nb = n_buckets(*h.p, *h.R);
+    return PLEX_OK;
+}
+
+static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
+    const Plan& p = *h.p;
+    const RankPlan& R = *h.R;
+    const int slot = b % pp.n_slots;
+    uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
+    const uint64_t lo = (uint64_t)b * p.bucket;
+    const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+    if (b >= pp.n_slots) CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
+    cudaEvent_t ta = nullptr;
+    plex_status st;
+    if ((st = timed_begin(c, pp.copy, &ta))) return st;
+    CK(cudaMemcpyAsync(stg, h.slab->host + lo, len, cudaMemcpyHostToDevice, pp.copy));
+    if ((st = timed_end(c, pp.copy, ta, PLEX_STAT_H2D, len))) return st;
+    CK(cudaEventRecord(pp.ev_c[slot], pp.copy));
+    CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
+    const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+    if ((st = timed_begin(c, pp.kern, &ta))) return st;
+    CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.kern));
+    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.d->bucket_payload[b]))) return st;
+    CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
+    return PLEX_OK;
+}
+
+static plex_status on_end(plex_ctx_s* c, Pipe& pp, Half& h) {
+    CK(launch_verify(h.d->cks_in, h.d->cks_want, (uint32_t)h.R->segs.size(), c->d_flag, pp.kern));
+    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
+    return PLEX_OK;
+}
+
+static plex_status check_slab(plex_ctx_s* c, plex_plan_t plan, plex_slab_t slab) {
+    if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) {
+        set_error("slab does not belong to this plan/rank");
+        return PLEX_E_INVAL;
     }
     return PLEX_OK;
 }
@@ -323,6 +457,11 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
             set_error("cudaEventCreate failed");
             return fail(PLEX_E_CUDA);
         }
+    for (auto& e : c->ev_sync)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            set_error("cudaEventCreate failed");
+            return fail(PLEX_E_CUDA);
+        }
     c->scratch_bytes = 256 * (size_t)world + 256;
     if (cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&c->d_flag, 64) != cudaSuccess ||
         cudaMalloc(&c->d_scratch, 2 * c->scratch_bytes) != cudaSuccess ||
@@ -357,6 +496,8 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     DeviceGuard g(c->device);
     if (c->pack) cudaStreamSynchronize(c->pack);
     if (c->copy) cudaStreamSynchronize(c->copy);
+    if (c->pack2) cudaStreamSynchronize(c->pack2);
+    if (c->copy2) cudaStreamSynchronize(c->copy2);
     for (auto& kv : c->dev) free_devplan(kv.second);
     for (auto& kv : c->peers)
         if (kv.second.second) cudaIpcCloseMemHandle(kv.second.second);
@@ -364,11 +505,18 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     for (cudaEvent_t e : c->ev_pack) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_sync) if (e) cudaEventDestroy(e);
     if (c->ev_caller) cudaEventDestroy(c->ev_caller);
     if (c->ev_pack_done) cudaEventDestroy(c->ev_pack_done);
     if (c->ev_copy_done) cudaEventDestroy(c->ev_copy_done);
     cudaFreeHost(c->h_ptrs);
     cudaFree(c->d_ptrs);
+    cudaFreeHost(c->h_ptrs2);
+    cudaFree(c->d_ptrs2);
+    for (cudaEvent_t e : c->ev_pack2) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_copy2) cudaEventDestroy(e);
+    if (c->pack2) cudaStreamDestroy(c->pack2);
+    if (c->copy2) cudaStreamDestroy(c->copy2);
     cudaFreeHost(c->h_flag);
     cudaFree(c->d_flag);
     cudaFree(c->d_scratch);
@@ -477,45 +625,21 @@ plex_status plex_slab_checksums(plex_slab_t s, uint64_t* out, int32_t n) {
 plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
                                void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st) return st;
-    if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) { set_error("slab does not belong to this plan/rank"); return PLEX_E_INVAL; }
+    if (st || (st = check_slab(c, plan, slab))) return st;
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
     DeviceGuard g(c->device);
-    const Plan& p = plan->p;
-    const RankPlan& R = p.ranks[c->rank];
-    if ((st = fill_state_ptrs(c, p, src, n_src))) return st;
-    DevPlan* d;
-    if ((st = get_devplan(c, p, &d))) return st;
+    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}};
+    if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
+    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
-    const size_t np = PLEX_NUM_KINDS * p.tensors.size();
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
-    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, np * 8, cudaMemcpyHostToDevice, c->pack));
-    CK(cudaMemsetAsync(d->cks, 0, 16 * std::max<size_t>(1, R.segs.size()), c->pack));
-    const int32_t nb = n_buckets(p, R);
-    for (int32_t b = 0; b < nb; ++b) {
-        const int slot = b % c->n_slots;
-        uint8_t* stg = c->staging + (uint64_t)slot * p.bucket;
-        const uint64_t lo = (uint64_t)b * p.bucket;
-        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
-        if (b >= c->n_slots) CK(cudaStreamWaitEvent(c->pack, c->ev_copy[slot], 0));
-        const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
-        cudaEvent_t ta = nullptr;
-        if ((st = timed_begin(c, c->pack, &ta))) return st;
-        CK(launch_pack(true, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, stg, lo, d->cks, c->pack));
-        if ((st = timed_end(c, c->pack, ta, PLEX_STAT_PACK, 2 * d->bucket_payload[b]))) return st;
-        CK(cudaEventRecord(c->ev_pack[slot], c->pack));
-        CK(cudaStreamWaitEvent(c->copy, c->ev_pack[slot], 0));
-        if ((st = timed_begin(c, c->copy, &ta))) return st;
-        CK(cudaMemcpyAsync(slab->host + lo, stg, len, cudaMemcpyDeviceToHost, c->copy));
-        if ((st = timed_end(c, c->copy, ta, PLEX_STAT_D2H, len))) return st;
-        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
-    }
-    std::vector<uint64_t> cks(2 * R.segs.size());
-    if (!cks.empty()) CK(cudaMemcpyAsync(cks.data(), d->cks, 8 * cks.size(), cudaMemcpyDeviceToHost, c->pack));
-    if ((st = finish(c, caller))) return st;
-    slab->cks.swap(cks);
+    if ((st = off_begin(c, pp, h))) return st;
+    for (int32_t b = 0; b < h.nb; ++b)
+        if ((st = off_bucket(c, pp, h, b))) return st;
+    if ((st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
+    slab->cks.swap(h.cks);
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
     return PLEX_OK;
@@ -525,55 +649,110 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
 plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, void* const* dst, int32_t n_dst,
                               void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st) return st;
-    if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) { set_error("slab does not belong to this plan/rank"); return PLEX_E_INVAL; }
+    if (st || (st = check_slab(c, plan, slab))) return st;
     if (slab->residency == PLEX_RES_DEVICE) {
         if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
         return PLEX_OK;                                     // idempotent
     }
     DeviceGuard g(c->device);
-    const Plan& p = plan->p;
-    const RankPlan& R = p.ranks[c->rank];
-    if ((st = fill_state_ptrs(c, p, reinterpret_cast<const void* const*>(dst), n_dst))) return st;
-    DevPlan* d;
-    if ((st = get_devplan(c, p, &d))) return st;
+    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}};
+    if ((st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst)) ||
+        (st = get_devplan(c, plan->p, &h.d)))
+        return st;
+    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
-    const size_t np = PLEX_NUM_KINDS * p.tensors.size();
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
-    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, np * 8, cudaMemcpyHostToDevice, c->pack));
-    const size_t nck = 2 * R.segs.size();
-    CK(cudaMemsetAsync(d->cks, 0, 8 * std::max<size_t>(2, nck), c->pack));
-    if (nck) CK(cudaMemcpyAsync(d->cks_want, slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, c->pack));
-    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->pack));
-    const int32_t nb = n_buckets(p, R);
-    for (int32_t b = 0; b < nb; ++b) {
-        const int slot = b % c->n_slots;
-        uint8_t* stg = c->staging + (uint64_t)slot * p.bucket;
-        const uint64_t lo = (uint64_t)b * p.bucket;
-        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
-        if (b >= c->n_slots) CK(cudaStreamWaitEvent(c->copy, c->ev_pack[slot], 0));
-        cudaEvent_t ta = nullptr;
-        if ((st = timed_begin(c, c->copy, &ta))) return st;
-        CK(cudaMemcpyAsync(stg, slab->host + lo, len, cudaMemcpyHostToDevice, c->copy));
-        if ((st = timed_end(c, c->copy, ta, PLEX_STAT_H2D, len))) return st;
-        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
-        CK(cudaStreamWaitEvent(c->pack, c->ev_copy[slot], 0));
-        const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
-        if ((st = timed_begin(c, c->pack, &ta))) return st;
-        CK(launch_pack(false, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, stg, lo, d->cks, c->pack));
-        if ((st = timed_end(c, c->pack, ta, PLEX_STAT_UNPACK, 2 * d->bucket_payload[b]))) return st;
-        CK(cudaEventRecord(c->ev_pack[slot], c->pack));
-    }
-    CK(launch_verify(d->cks, d->cks_want, (uint32_t)R.segs.size(), c->d_flag, c->pack));
-    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->pack));
-    if ((st = finish(c, caller))) return st;
+    if ((st = on_begin(c, pp, h))) return st;
+    for (int32_t b = 0; b < h.nb; ++b)
+        if ((st = on_bucket(c, pp, h, b))) return st;
+    if ((st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
     if (*c->h_flag) {
         set_error("onload: %d segment checksum(s) differ from offload", *c->h_flag);
         return PLEX_E_CHECKSUM;
     }
     slab->residency = PLEX_RES_DEVICE;
+    return PLEX_OK;
+}
+
+// ---- NEXT-1: duplex switch -----------------------------------------------------------
+// Offload the resident job A and onload the incoming job B at the same time:
+// A's buckets stream D2H on the ctx copy stream while B's stream H2D on a
+// second, library-owned copy stream, so the two directions of the host link
+// run concurrently and C_setup = T_offload + T_load (Eq. 3)
+// becomes ~max(T_offload, T_load).  Staging holds both rings back to back.
+plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* const* src_out, int32_t n_src,
+                              plex_slab_t slab_out, plex_plan_t plan_in, plex_slab_t slab_in, void* const* dst_in,
+                              int32_t n_dst, void* caller_stream) {
+    plex_status st = check_common(c, plan_out);
+    if (st || (st = check_common(c, plan_in)) || (st = check_slab(c, plan_out, slab_out)) ||
+        (st = check_slab(c, plan_in, slab_in)))
+        return st;
+    if (slab_out == slab_in) { set_error("switch needs two different slabs"); return PLEX_E_INVAL; }
+    if (slab_in->residency == PLEX_RES_DEVICE && !slab_in->written) {
+        set_error("incoming slab holds no offloaded state");
+        return PLEX_E_STATE;
+    }
+    const uint64_t need = (uint64_t)c->n_slots * (plan_out->p.bucket + plan_in->p.bucket);
+    if (c->staging_bytes < need) {
+        set_error("switch needs staging >= n_slots x (bucket_out + bucket_in) = %llu B", (unsigned long long)need);
+        return PLEX_E_INVAL;
+    }
+    DeviceGuard g(c->device);
+    const bool do_off = slab_out->residency == PLEX_RES_DEVICE;
+    const bool do_on = slab_in->residency == PLEX_RES_HOST;
+    Half ho{&plan_out->p, &plan_out->p.ranks[c->rank], nullptr, slab_out, 0, {}};
+    Half hi{&plan_in->p, &plan_in->p.ranks[c->rank], nullptr, slab_in, 0, {}};
+    if (do_off && ((st = fill_state_ptrs(c, plan_out->p, src_out, n_src, 0)) || (st = get_devplan(c, plan_out->p, &ho.d))))
+        return st;
+    if (do_on && ((st = fill_state_ptrs(c, plan_in->p, reinterpret_cast<const void* const*>(dst_in), n_dst, 1)) ||
+                  (st = get_devplan(c, plan_in->p, &hi.d))))
+        return st;
+    if (!c->pack2) {
+        CK(cudaStreamCreateWithFlags(&c->pack2, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy2, cudaStreamNonBlocking));
+        c->ev_pack2.resize(c->n_slots);
+        c->ev_copy2.resize(c->n_slots);
+        for (int i = 0; i < c->n_slots; ++i) {
+            CK(cudaEventCreateWithFlags(&c->ev_pack2[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
+        }
+    }
+    Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
+    Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
+            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2};
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    CK(cudaEventRecord(c->ev_caller, caller));
+    for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
+    if (do_off && (st = off_begin(c, po, ho))) return st;
+    if (do_on && (st = on_begin(c, pi, hi))) return st;
+    const int32_t nb = std::max(do_off ? ho.nb : 0, do_on ? hi.nb : 0);
+    for (int32_t b = 0; b < nb; ++b) {        // interleave so both directions start at once
+        if (do_off && b < ho.nb && (st = off_bucket(c, po, ho, b))) return st;
+        if (do_on && b < hi.nb && (st = on_bucket(c, pi, hi, b))) return st;
+    }
+    if (do_off && (st = off_end(c, po, ho))) return st;
+    if (do_on && (st = on_end(c, pi, hi))) return st;
+    CK(cudaEventRecord(c->ev_pack_done, c->pack2));
+    CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
+    CK(cudaEventRecord(c->ev_pack_done, c->copy2));
+    CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
+    CK(cudaStreamSynchronize(c->pack2));
+    CK(cudaStreamSynchronize(c->copy2));
+    if ((st = finish(c, caller))) return st;
+    if (do_off) {
+        slab_out->cks.swap(ho.cks);
+        slab_out->residency = PLEX_RES_HOST;
+        slab_out->written = true;
+    }
+    if (do_on) {
+        if (*c->h_flag) {
+            set_error("switch onload: %d segment checksum(s) differ from offload", *c->h_flag);
+            return PLEX_E_CHECKSUM;
+        }
+        slab_in->residency = PLEX_RES_DEVICE;
+    }
     return PLEX_OK;
 }
 
@@ -593,7 +772,7 @@ static plex_status push_rank(plex_ctx_s* c, const Plan& p, int32_t rank, const v
     CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, (nt + p.world) * 8, cudaMemcpyHostToDevice, s));
     cudaEvent_t ta = nullptr;
     if ((st = timed_begin(c, s, &ta))) return st;
-    CK(launch_push(d_items, R.push.size(), c->d_ptrs, c->d_ptrs + nt, s));
+    CK(launch_push(true, d_items, R.push.size(), c->d_ptrs, c->d_ptrs + nt, s));
     if ((st = timed_end(c, s, ta, PLEX_STAT_PUSH, R.src_read_bytes + R.src_read_bytes / 2))) return st;
     return PLEX_OK;
 }
@@ -743,9 +922,192 @@ plex_status plex_cast_rne(const void* src_f32, void* dst_bf16, uint64_t count, v
 }  // extern "C"
 
 namespace plex {
-plex_status nccl_sync(plex_ctx_s* c, const Plan& p, const void* const* src, void* arena, cudaStream_t caller) {
-    (void)c; (void)p; (void)src; (void)arena; (void)caller;
-    set_error("PLEX_CTX_SYNC_NCCL transport not built yet");
-    return PLEX_E_INVAL;
+
+// ---- NCCL baseline transport of the weight sync (PLEX_CTX_SYNC_NCCL) --------
+// K4 casts every (source = me, destination d) rectangle into d's contiguous
+// send segment, one grouped ncclSend/ncclRecv per round exchanges all
+// segments (N1), K5 copies received rectangles into the arena.  Rounds bound
+// staging: the ctx staging is split into send/recv x double buffer, each with
+// (world-1) per-pair regions of Q bytes.  K4(k+1) and the exchange of round k
+// overlap; K5(k) follows the exchange.  Same bytes as the fused push (the
+// ledger), so the two transports are measured against each other.
+static uint64_t pad16(uint64_t b) { return (b + 15) & ~15ull; }
+
+static plex_status build_nccl_sched(plex_ctx_s* c, const Plan& p, DevPlan* d, uint64_t Q) {
+    const int W = p.world, me = c->rank;
+    auto slot = [&](int x) { return x < me ? x : x - 1; };
+    std::vector<PushItem> local, rp, ru;
+    std::vector<std::vector<PushItem>> rp_r, ru_r;
+    std::vector<uint64_t> rpb, rub, sb, rb;
+    int R = 0;
+    // pass 1: rounds of every pair (needs every rank's list, identical on all ranks)
+    std::vector<int> rounds_pair((size_t)W * W, 0);
+    for (int src = 0; src < W; ++src) {
+        std::vector<uint64_t> cum(W, 0);
+        std::vector<int> rnd(W, 0), any(W, 0);
+        for (const PushItem& it : p.ranks[src].push) {
+            const int dst = (int)it.dst_rank;
+            if (dst == src) continue;
+            const uint64_t b = pad16((uint64_t)it.rows * it.cols * 2);
+            if (cum[dst] + b > Q && cum[dst] > 0) { ++rnd[dst]; cum[dst] = 0; }
+            cum[dst] += b;
+            any[dst] = 1;
+        }
+        for (int dst = 0; dst < W; ++dst)
+            if (any[dst]) { rounds_pair[(size_t)src * W + dst] = rnd[dst] + 1; R = std::max(R, rnd[dst] + 1); }
+    }
+    rp_r.assign(R, {});
+    ru_r.assign(R, {});
+    rpb.assign(R, 0);
+    rub.assign(R, 0);
+    sb.assign((size_t)R * W, 0);
+    rb.assign((size_t)R * W, 0);
+    uint64_t local_bytes = 0;
+    // pass 2: my send items (K4) and my local items
+    {
+        std::vector<uint64_t> cum(W, 0);
+        std::vector<int> rnd(W, 0);
+        for (const PushItem& it : p.ranks[me].push) {
+            const int dst = (int)it.dst_rank;
+            const uint64_t n = (uint64_t)it.rows * it.cols;
+            if (dst == me) { local.push_back(it); local_bytes += 6 * n; continue; }
+            const uint64_t b = pad16(n * 2);
+            if (cum[dst] + b > Q && cum[dst] > 0) { ++rnd[dst]; cum[dst] = 0; }
+            PushItem q = it;
+            q.dst_elem = ((uint64_t)slot(dst) * Q + cum[dst]) / 2;
+            q.dst_rank = (uint32_t)(W + (rnd[dst] & 1));
+            q.dst_stride = it.cols;
+            rp_r[rnd[dst]].push_back(q);
+            rpb[rnd[dst]] += 6 * n;
+            cum[dst] += b;
+            sb[(size_t)rnd[dst] * W + dst] = cum[dst];
+        }
+    }
+    // pass 3: what every peer sends me (K5), in the sender's order
+    for (int src = 0; src < W; ++src) {
+        if (src == me) continue;
+        uint64_t cum = 0;
+        int rnd = 0;
+        for (const PushItem& it : p.ranks[src].push) {
+            if ((int)it.dst_rank != me) continue;
+            const uint64_t n = (uint64_t)it.rows * it.cols;
+            const uint64_t b = pad16(n * 2);
+            if (cum + b > Q && cum > 0) { ++rnd; cum = 0; }
+            PushItem q = it;
+            q.src_elem = ((uint64_t)slot(src) * Q + cum) / 2;
+            q.src_stride = it.cols;
+            q.tensor = (uint32_t)(rnd & 1);
+            q.dst_rank = (uint32_t)me;
+            ru_r[rnd].push_back(q);
+            rub[rnd] += 4 * n;
+            cum += b;
+            rb[(size_t)rnd * W + src] = cum;
+        }
+    }
+    std::vector<uint64_t> rps(R + 1, 0), rus(R + 1, 0);
+    for (int k = 0; k < R; ++k) {
+        rps[k + 1] = rps[k] + rp_r[k].size();
+        rus[k + 1] = rus[k] + ru_r[k].size();
+        rp.insert(rp.end(), rp_r[k].begin(), rp_r[k].end());
+        ru.insert(ru.end(), ru_r[k].begin(), ru_r[k].end());
+    }
+    cudaFree(d->local);
+    cudaFree(d->rpack);
+    cudaFree(d->runpack);
+    d->local = d->rpack = d->runpack = nullptr;
+    plex_status st;
+    if ((st = upload(&d->local, local)) || (st = upload(&d->rpack, rp)) || (st = upload(&d->runpack, ru))) return st;
+    d->n_local = local.size();
+    d->local_bytes = local_bytes;
+    d->rounds = R;
+    d->rpack_start = rps;
+    d->runpack_start = rus;
+    d->rpack_bytes = rpb;
+    d->runpack_bytes = rub;
+    d->send_bytes = sb;
+    d->recv_bytes = rb;
+    d->nq = Q;
+    return PLEX_OK;
 }
+
+plex_status nccl_sync(plex_ctx_s* c, const Plan& p, const void* const* src, void* arena, cudaStream_t caller) {
+    const int W = p.world, me = c->rank;
+    const size_t nt = p.tensors.size();
+    if (!src) { set_error("NULL master pointers"); return PLEX_E_INVAL; }
+    plex_status st;
+    DevPlan* d;
+    if ((st = get_devplan(c, p, &d))) return st;
+    const uint64_t Q = W > 1 ? (c->staging_bytes / (4ull * (W - 1))) & ~255ull : 0;
+    if (W > 1 && Q < 4096) { set_error("staging too small for the NCCL sync transport"); return PLEX_E_INVAL; }
+    if (d->nq != Q && (st = build_nccl_sched(c, p, d, std::max<uint64_t>(Q, 256)))) return st;
+    uint8_t* send[2] = {c->staging, c->staging + (uint64_t)(W - 1) * Q};
+    uint8_t* recv[2] = {c->staging + 2ull * (W - 1) * Q, c->staging + 3ull * (W - 1) * Q};
+    // pointer table: [nt masters][W + 2 destinations][2 receive buffers]
+    if ((st = ensure_ptrs(c, nt + W + 4))) return st;
+    for (size_t t = 0; t < nt; ++t) c->h_ptrs[t] = reinterpret_cast<uint64_t>(src[t]);
+    uint64_t* hd = c->h_ptrs + nt;
+    for (int g = 0; g < W; ++g) hd[g] = 0;
+    hd[me] = reinterpret_cast<uint64_t>(arena);
+    hd[W] = reinterpret_cast<uint64_t>(send[0]);
+    hd[W + 1] = reinterpret_cast<uint64_t>(send[1]);
+    hd[W + 2] = reinterpret_cast<uint64_t>(recv[0]);
+    hd[W + 3] = reinterpret_cast<uint64_t>(recv[1]);
+    const uint64_t* d_src = c->d_ptrs;
+    const uint64_t* d_dst = c->d_ptrs + nt;
+    const uint64_t* d_rcv = c->d_ptrs + nt + W + 2;
+    CK(cudaEventRecord(c->ev_caller, caller));
+    CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, (nt + W + 4) * 8, cudaMemcpyHostToDevice, c->pack));
+    CK(cudaEventRecord(c->ev_sync[0], c->pack));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_sync[0], 0));      // pointer table visible before any K5
+    cudaEvent_t ta = nullptr;
+    if ((st = timed_begin(c, c->pack, &ta))) return st;
+    CK(launch_push(true, d->local, d->n_local, d_src, d_dst, c->pack));
+    if ((st = timed_end(c, c->pack, ta, PLEX_STAT_PUSH, d->local_bytes))) return st;
+    cudaEvent_t* evR = c->ev_sync;       // K4 done, per buffer
+    cudaEvent_t* evN = c->ev_sync + 2;   // exchange done
+    cudaEvent_t* evU = c->ev_sync + 4;   // K5 done
+    const int R = d->rounds;
+    auto rpack = [&](int k) -> plex_status {
+        const uint64_t i0 = d->rpack_start[k], i1 = d->rpack_start[k + 1];
+        cudaEvent_t t = nullptr;
+        plex_status s2;
+        if ((s2 = timed_begin(c, c->pack, &t))) return s2;
+        CK(launch_push(true, d->rpack + i0, i1 - i0, d_src, d_dst, c->pack));
+        if ((s2 = timed_end(c, c->pack, t, PLEX_STAT_RPACK, d->rpack_bytes[k]))) return s2;
+        CK(cudaEventRecord(evR[k & 1], c->pack));
+        return PLEX_OK;
+    };
+    if (R > 0 && (st = rpack(0))) return st;
+    for (int k = 0; k < R; ++k) {
+        const int b = k & 1;
+        CK(cudaStreamWaitEvent(c->copy, evR[b], 0));
+        if (k >= 2) CK(cudaStreamWaitEvent(c->copy, evU[b], 0));
+        if ((st = timed_begin(c, c->copy, &ta))) return st;
+        uint64_t ssum = 0, rsum = 0;
+        NK(ncclGroupStart());
+        for (int g = 0; g < W; ++g) {
+            if (g == me) continue;
+            const int sl = g < me ? g : g - 1;
+            const uint64_t sbytes = d->send_bytes[(size_t)k * W + g], rbytes = d->recv_bytes[(size_t)k * W + g];
+            if (sbytes) NK(ncclSend(send[b] + (uint64_t)sl * Q, sbytes, ncclUint8, g, c->comm, c->copy));
+            if (rbytes) NK(ncclRecv(recv[b] + (uint64_t)sl * Q, rbytes, ncclUint8, g, c->comm, c->copy));
+            ssum += sbytes;
+            rsum += rbytes;
+        }
+        NK(ncclGroupEnd());
+        if ((st = timed_end(c, c->copy, ta, PLEX_STAT_NCCL, std::max(ssum, rsum)))) return st;
+        CK(cudaEventRecord(evN[b], c->copy));
+        if (k + 1 < R && (st = rpack(k + 1))) return st;
+        CK(cudaStreamWaitEvent(c->pack, evN[b], 0));
+        const uint64_t i0 = d->runpack_start[k], i1 = d->runpack_start[k + 1];
+        if ((st = timed_begin(c, c->pack, &ta))) return st;
+        CK(launch_push(false, d->runpack + i0, i1 - i0, d_rcv, d_dst, c->pack));
+        if ((st = timed_end(c, c->pack, ta, PLEX_STAT_RUNPACK, d->runpack_bytes[k]))) return st;
+        CK(cudaEventRecord(evU[b], c->pack));
+    }
+    return finish(c, caller);
+}
+
 }  // namespace plex

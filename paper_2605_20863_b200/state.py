@@ -89,7 +89,7 @@ class Plan:
     def __init__(self, manifest, head_dim: int = 1, world: int = 1, tp: int = 0, dp: int = 0, ep: int = 1,
                  rank_map: int = L.RANKMAP_TP_FAST, slab_layout: int = L.SLAB_KIND_MAJOR,
                  kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
-                 bucket_bytes: int = 64 << 20, tile_bytes: int = 64 << 10,
+                 bucket_bytes: int = 256 << 20, tile_bytes: int = 64 << 10,
                  resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
@@ -116,6 +116,7 @@ class Plan:
         self.world, self.tp, self.dp, self.ep = world, tp, dp, ep
         self.kind_mask = kind_mask
         self.bucket_bytes = bucket_bytes
+        self.subset = None if subset is None else frozenset(subset)
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -234,9 +235,9 @@ def _stream_ptr(s) -> int:
 class StateManager:
     """One per rank process: the ctx (streams, staging, NCCL communicator)."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 64 << 20,
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 256 << 20,
                  n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, duplex: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("StateManager needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -246,7 +247,9 @@ class StateManager:
         self.n_slots = n_slots
         self.pack_stream = torch.cuda.Stream(device)
         self.copy_stream = torch.cuda.Stream(device)
-        self.staging = torch.empty(n_slots * bucket_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+        # duplex: room for both rings of a switch (offload || onload)
+        self.staging = torch.empty((2 if duplex else 1) * n_slots * bucket_bytes, dtype=torch.uint8,
+                                   device=f"cuda:{device}")
         idbuf = None
         if world > 1 and bootstrap:
             if nccl_id is None:
@@ -304,6 +307,14 @@ class StateManager:
     def onload(self, plan: Plan, slab: Slab, shards, stream=None) -> None:
         arr, n = self._state_ptrs(plan, shards)
         check(lib.plex_state_onload(self.h, plan.h, slab.h, arr, n, _stream_ptr(stream)))
+
+    def switch(self, plan_out: Plan, shards_out, slab_out: Slab, plan_in: Plan, slab_in: Slab, shards_in,
+               stream=None) -> None:
+        """Duplex context switch: offload one job while onloading another (NEXT-1)."""
+        a, na = self._state_ptrs(plan_out, shards_out)
+        b, nb = self._state_ptrs(plan_in, shards_in)
+        check(lib.plex_state_switch(self.h, plan_out.h, a, na, slab_out.h, plan_in.h, slab_in.h, b, nb,
+                                    _stream_ptr(stream)))
 
     def sync(self, plan: Plan, masters: Sequence[torch.Tensor], arena: torch.Tensor, stream=None) -> None:
         arr = ptr_array([m.data_ptr() if m.numel() else 0 for m in masters])
@@ -398,8 +409,10 @@ class Job:
         return self
 
     def slab_shards(self):
-        mask = self.plan.kind_mask
-        return OrderedDict((kk, v) for kk, v in self.shards.items() if mask & (1 << kk[1]))
+        """The shards the plan's slab carries (kind mask and optional key subset)."""
+        mask, sub = self.plan.kind_mask, self.plan.subset
+        return OrderedDict((kk, v) for kk, v in self.shards.items()
+                           if mask & (1 << kk[1]) and (sub is None or kk[0] in sub))
 
     def masters(self) -> List[torch.Tensor]:
         return [self.shards[(k, 1)] for k, _ in self.plan.manifest]
@@ -407,15 +420,32 @@ class Job:
     def suspend(self, stream=None, release: bool = True) -> None:
         self.mgr.offload(self.plan, self.slab_shards(), self.slab, stream)
         if release:
-            for v in self.slab_shards().values():
-                v.untyped_storage().resize_(0)
+            self.release()
 
-    def resume(self, stream=None) -> None:
+    def release(self) -> None:
+        """a5: give the slab-carried shards' device storage back to PyTorch."""
+        for v in self.slab_shards().values():
+            v.untyped_storage().resize_(0)
+
+    def acquire(self) -> None:
+        """a5: re-allocate the slab-carried shards' device storage."""
         for v in self.slab_shards().values():
             need = v.numel() * v.element_size()
             if v.untyped_storage().nbytes() != need:
                 v.untyped_storage().resize_(need)
+
+    def resume(self, stream=None) -> None:
+        self.acquire()
         self.mgr.onload(self.plan, self.slab, self.slab_shards(), stream)
+
+    def switch_to(self, other: "Job", stream=None, release: bool = True) -> None:
+        """PAPER.md:555 context switch self -> other with both host-link
+        directions busy at once (offload self || onload other)."""
+        other.acquire()
+        self.mgr.switch(self.plan, self.slab_shards(), self.slab, other.plan, other.slab, other.slab_shards(),
+                        stream)
+        if release:
+            self.release()
 
     def sync(self, arena: torch.Tensor, stream=None) -> None:
         self.mgr.sync(self.plan, self.masters(), arena, stream)

@@ -32,6 +32,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=1 << 16, n_slots=2)
+    # NCCL-baseline transport; tiny staging forces many exchange rounds
+    mgr_nccl = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=1 << 16, n_slots=2, sync_nccl=True)
     bad = 0
     cases = [("mid", 2 if world % 2 == 0 else 1, 1), ("mid-moe", 2 if world % 2 == 0 else 1, world),
              ("toy-odd", 1, 1)]
@@ -51,6 +53,13 @@ def main():
                 if not np.array_equal(bits_np(v), want[name]):
                     print(f"[rank {rank}] sync mismatch {model} map={rank_map} {name}", flush=True)
                     bad += 1
+            arena.fill_(0xCD)
+            for _ in range(2):
+                mgr_nccl.sync(plan, job.masters(), arena)
+            for name, v in P.StateManager.rollout_views(plan, rank, arena).items():
+                if not np.array_equal(bits_np(v), want[name]):
+                    print(f"[rank {rank}] nccl-sync mismatch {model} map={rank_map} {name}", flush=True)
+                    bad += 1
             # suspend / resume of this rank's shards
             before = {k: bits_np(v) for k, v in job.shards.items()}
             job.suspend()
@@ -68,6 +77,7 @@ def main():
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()
+    mgr_nccl.close()
     dist.destroy_process_group()
     if rank == 0:
         print(f"mp_worker world={world} mismatches={int(t.item())}", flush=True)

@@ -275,3 +275,33 @@ def test_multiplex_emulated():
         for r in range(W):
             for k, x in jobs[j][r].shards.items():
                 assert np.array_equal(bits_np(x), final[j][r][k]), (j, r, k)
+
+
+# ---- NEXT-1 duplex switch --------------------------------------------------------------------------
+@pytest.mark.parametrize("models,buckets", [(("mid", "mid-moe"), (1 << 14, 1 << 16)), (("toy-odd", "toy"), (512, 1024)),
+                                            (("mid", "mid"), (1 << 15, 1 << 15))])
+def test_duplex_switch_matches_oracle(models, buckets):
+    W = 2
+    plans = [P.Plan(manifest(mo), world=W, bucket_bytes=b, tile_bytes=512) for mo, b in zip(models, buckets)]
+    for r in range(W):
+        m = P.StateManager(device=0, rank=r, world=W, bucket_bytes=max(buckets), n_slots=2, bootstrap=False)
+        a = P.Job(m, plans[0], seed=30).alloc().init_synthetic(special_bits=3)
+        b = P.Job(m, plans[1], seed=31).alloc().init_synthetic(special_bits=3)
+        b.suspend()                                   # B waits in its slab, A resident
+        for kk, v in b.shards.items():
+            assert v.untyped_storage().nbytes() == 0
+        for step in range(3):                         # A -> B -> A -> B
+            src, dst = (a, b) if step % 2 == 0 else (b, a)
+            src.switch_to(dst)
+            assert src.slab.residency == L.RES_HOST and dst.slab.residency == L.RES_DEVICE
+            for j, (mo, sd) in enumerate(zip(models, (30, 31))):
+                full = full_state(mo, seed=sd, special_bits=3)
+                osh = fsdp_shards(full, W, r, O.fsdp_rows)
+                job = (a, b)[j]
+                if job is dst:
+                    for kk, x in job.shards.items():
+                        assert np.array_equal(bits_np(x), osh[kk]), (step, kk)
+                else:
+                    segs, size = O.slab_layout(manifest(mo), W, r)
+                    assert np.array_equal(job.slab.host_bytes(), O.pack_slab(segs, size, osh))
+        m.close()

@@ -1,0 +1,256 @@
+#!/usr/bin/env python
+"""Measurements of the other BASELINE.json configs.
+
+bench.py times the headline workload; this script times the rest, one JSON
+line per run (rank 0), device-timed with CUDA events on the caller stream and
+max over ranks:
+
+  duplex     two jobs of --model: step = switch A->B (offload A || onload B,
+             NEXT-1) + sync B, alternating; reports the switch latency against
+             the sequential C_setup = T_offload + T_load (Eq. 3)
+  optim      configs[2]: optimizer kinds only (master/m/v) of rank r's FSDP-8
+             shard of --model (default Qwen2.5-32B), offload + onload with k =
+             WORLD_SIZE GPUs at once (each process is rank r of the 8-rank plan)
+  moe        configs[3]: Qwen3-30B-A3B, FSDP-N -> attention TP-2 x DP + experts
+             EP-N weight sync, plus per-expert KEY_MAJOR pack/offload/onload of
+             --units expert units
+  multiplex  configs[4]: 4 jobs (0.5B/1.5B/3B/7B, seeds 0..3) time-slicing
+             the group, R rounds round-robin; each visit = transition ops of
+             PAPER.md:555 (offload resident, onload incoming) + mutation + sync
+
+    torchrun --nproc-per-node N tools/scenarios.py --scenario duplex --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2605_20863_b200 as P  # noqa: E402
+from paper_2605_20863_b200 import _lib as L  # noqa: E402
+from plexgen import MODELS, manifest  # noqa: E402
+
+from bench import Clocks  # noqa: E402
+
+
+class Ctx:
+    def __init__(self, gpus: int):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        assert self.world == gpus, (gpus, self.world)
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+
+    def barrier(self):
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    def emit(self, line: dict, out: str):
+        if self.rank == 0:
+            print(json.dumps(line), flush=True)
+            if out:
+                with open(out, "a") as f:
+                    f.write(json.dumps(line) + "\n")
+
+
+def timed(c: Ctx, fn, steps: int, warmup: int):
+    for _ in range(warmup):
+        fn()
+    clocks = Clocks(c.local)
+    c.barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    c.barrier()
+    clk = clocks.stop()
+    return c.allmax(e0.elapsed_time(e1) / steps), clk
+
+
+def scen_duplex(a, c: Ctx):
+    shape = MODELS[a.model]
+    tp = a.tp or min(2, c.world)
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp) for _ in range(2)]
+    jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic() for pl, s in zip(plans, (1, 2))]
+    arena = mgr.arena(plans[0])
+    jobs[1].suspend()
+    state = {"cur": 0}
+
+    def seq_step():                                  # sequential C_setup = T_off + T_load
+        i = state["cur"]
+        jobs[i].suspend()
+        jobs[1 - i].resume()
+        jobs[1 - i].sync(arena)
+        state["cur"] = 1 - i
+
+    def duplex_step():
+        i = state["cur"]
+        jobs[i].switch_to(jobs[1 - i])
+        jobs[1 - i].sync(arena)
+        state["cur"] = 1 - i
+
+    ms_seq, _ = timed(c, seq_step, a.steps, a.warmup)
+    ms_dup, clk = timed(c, duplex_step, a.steps, a.warmup)
+    S = plans[0].rank_info(c.rank).payload_bytes
+    tot = c.allsum(2.0 * S)
+    c.emit({"scenario": "duplex", "model": a.model, "n_gpus": c.world, "layout": f"FSDP-{c.world}->TP-{tp}",
+            "state_bytes_per_rank_per_job": S,
+            "sequential_switch_ms": round(ms_seq, 2), "duplex_switch_ms": round(ms_dup, 2),
+            "speedup": round(ms_seq / ms_dup, 3),
+            "host_link_GBs_aggregate": round(tot / (ms_dup * 1e-3) / 1e9, 2), "clocks": clk,
+            "note": "step = context switch (offload A, onload B) + sync B; both jobs fully resident on device "
+                    "during the switch"}, a.out)
+
+
+def scen_optim(a, c: Ctx):
+    # each process = rank c.rank of an FSDP-8 plan; k = world processes copy at once
+    W = 8
+    shape = MODELS[a.model]
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=W, bucket_bytes=a.bucket_mb << 20, bootstrap=False,
+                         timing=True)
+    plan = mgr.plan(manifest(a.model), world=W, kind_mask=L.KINDMASK_OPTIM)
+    job = P.Job(mgr, plan, seed=2).alloc(kinds=(1, 2, 3)).init_synthetic()
+
+    def step():
+        job.suspend(release=False)
+        job.resume()
+
+    ms, clk = timed(c, step, a.steps, a.warmup)
+    S = plan.rank_info(c.rank).payload_bytes
+    st = mgr.stats()
+    d2h = st["d2h"]["bytes"] / (st["d2h"]["ms"] * 1e-3) / 1e9
+    h2d = st["h2d"]["bytes"] / (st["h2d"]["ms"] * 1e-3) / 1e9
+    c.emit({"scenario": "optim-offload", "model": a.model, "k_gpus": c.world, "fsdp": W,
+            "optimizer_bytes_per_gpu": S, "aggregate_bytes": c.allsum(float(S)),
+            "ms_offload_plus_onload": round(ms, 2),
+            "per_gpu_GBs_each_way": round(2 * S / (ms * 1e-3) / 1e9, 2),
+            "rank0_copy_engine_GBs": {"d2h": round(d2h, 2), "h2d": round(h2d, 2)}, "clocks": clk,
+            "note": "paper's context: 19.0 s optimizer-state load for 30B (PAPER.md:604), bytes/ranks unstated"},
+           a.out)
+    _ = shape
+
+
+def scen_moe(a, c: Ctx):
+    model = "qwen3-30b-a3b"
+    shape = MODELS[model]
+    tp = min(2, c.world)
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, ep=c.world)
+    job = P.Job(mgr, plan, seed=3, slab=False).alloc(kinds=(1,)).init_synthetic()
+    arena = mgr.arena(plan)
+    ms_sync, clk = timed(c, lambda: job.sync(arena), a.steps, a.warmup)
+    info = plan.rank_info(c.rank)
+    nv = c.allmax(float(max(info.send_bytes, info.recv_bytes)))
+    # per-expert units: KEY_MAJOR slab of the first --units (layer, expert) units
+    from plexgen.models import expert_keys
+    units = [(l, e) for l in range(shape.layers) for e in range(shape.experts)][:a.units]
+    keys = expert_keys(model, units)
+    uplan = mgr.plan(manifest(model), slab_layout=L.SLAB_KEY_MAJOR, subset=keys)
+    ujob = P.Job(mgr, uplan, seed=3)
+    for k in keys:                                    # share the master shards, add the other kinds
+        t = uplan.index[k]
+        shp = uplan.shard_shape(c.rank, t)
+        for kd in range(4):
+            ujob.shards[(k, kd)] = job.shards[(k, 1)] if kd == 1 else \
+                torch.empty(shp, dtype=P.state.KIND_TORCH[kd], device=f"cuda:{c.local}")
+    ms_unit, _ = timed(c, lambda: (ujob.suspend(release=False), ujob.resume()), a.steps, a.warmup)
+    ub = uplan.rank_info(c.rank).payload_bytes
+    c.emit({"scenario": "moe", "model": model, "n_gpus": c.world, "layout": f"attn TP-{tp}xDP-{c.world // tp}, EP-{c.world}",
+            "sync_ms": round(ms_sync, 3), "nvlink_bytes_max_rank": nv,
+            "nvlink_GBs": round(nv / (ms_sync * 1e-3) / 1e9, 1) if c.world > 1 else None,
+            "units": a.units, "unit_bytes_per_gpu": ub // max(1, a.units),
+            "unit_offload_onload_ms": round(ms_unit, 3), "clocks": clk}, a.out)
+
+
+def scen_multiplex(a, c: Ctx):
+    models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    plans, jobs, arenas = [], [], []
+    for j, mo in enumerate(models):
+        tp = 1 if mo == "qwen2.5-0.5b" or c.world == 1 else 2
+        pl = mgr.plan(manifest(mo), head_dim=MODELS[mo].head_dim, tp=tp, dp=c.world // tp)
+        plans.append(pl)
+        jb = P.Job(mgr, pl, seed=j).alloc().init_synthetic()
+        jb.suspend()
+        jobs.append(jb)
+        arenas.append(mgr.arena(pl))
+    schedule = list(range(4)) * a.rounds
+    res = {"r": None}
+    from paper_2605_20863_b200.state import synth_mutate  # noqa: F401  (mutation = simulated train step)
+
+    def run_trace():
+        resident = res["r"]
+        for j in schedule:
+            if resident is not None and resident != j:
+                if a.duplex:
+                    jobs[resident].switch_to(jobs[j])
+                else:
+                    jobs[resident].suspend()
+                    jobs[j].resume()
+            elif resident is None:
+                jobs[j].resume()
+            resident = j
+            jobs[j].sync(arenas[j])
+        jobs[resident].suspend()
+        res["r"] = None
+
+    ms, clk = timed(c, run_trace, 1, 0)
+    switches = len(schedule) - 1
+    c.emit({"scenario": "multiplex", "jobs": models, "n_gpus": c.world, "rounds": a.rounds,
+            "visits": len(schedule), "switches": switches, "duplex": a.duplex, "trace_ms": round(ms, 1),
+            "ms_per_visit": round(ms / len(schedule), 1), "clocks": clk}, a.out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scenario", required=True, choices=["duplex", "optim", "moe", "multiplex"])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--model", default="")
+    ap.add_argument("--tp", type=int, default=0)
+    ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--units", type=int, default=64)
+    ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--duplex", action="store_true")
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    c = Ctx(a.gpus)
+    if not a.model:
+        a.model = {"duplex": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
+    {"duplex": scen_duplex, "optim": scen_optim, "moe": scen_moe, "multiplex": scen_multiplex}[a.scenario](a, c)
+    c.barrier()
+    if c.world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
