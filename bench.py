@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--slots", type=int, default=3)
     ap.add_argument("--hugepage", action="store_true")
     ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")
+    ap.add_argument("--single-job", action="store_true", help="step = suspend + resume + sync of one job")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=2)
@@ -252,17 +253,34 @@ def run_plex(a):
     plan = plans[0]
     info = plan.rank_info(rank)
     # two jobs of the same shape (seeds 1, 2): B starts suspended in its slab,
-    # A resident -- one resident job per GPU group (R17)
-    job_b = P.Job(mgr, plans[1], seed=2, hugepage=a.hugepage).alloc().init_synthetic()
-    job_b.suspend()
-    job_a = P.Job(mgr, plans[0], seed=1, hugepage=a.hugepage).alloc().init_synthetic()
-    jobs = [job_a, job_b]
+    # A resident -- one resident job per GPU group (R17).  If the host cannot
+    # pin both jobs' slabs (N=1: 2 x 106.6 GB), the step is the single-job
+    # round trip (suspend A, resume A, sync A) over the same bytes.
+    two_jobs = not a.single_job
+    job_b = None
+    if two_jobs:
+        try:
+            job_b = P.Job(mgr, plans[1], seed=2, hugepage=a.hugepage).alloc().init_synthetic()
+            job_b.suspend()
+            job_a = P.Job(mgr, plans[0], seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+            ok = 1.0
+        except P.PlexError as e:
+            if e.code != P._lib.E_TIER_FULL:
+                raise
+            ok = 0.0
+        two_jobs = allmin(ok) > 0.5
+        if not two_jobs:
+            job_b = job_a = None
+            torch.cuda.empty_cache()
+    if not two_jobs:
+        job_a = P.Job(mgr, plans[0], seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+    jobs = [job_a, job_b] if two_jobs else [job_a, job_a]
     arena = mgr.arena(plan)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     # duplex switch (offload A || onload B) needs both jobs on the device at once
     free, total = torch.cuda.mem_get_info(local)
-    duplex = (not a.no_duplex) and (info.payload_bytes + (4 << 30) < free)
+    duplex = two_jobs and (not a.no_duplex) and (info.payload_bytes + (4 << 30) < free)
     duplex = allmin(1.0 if duplex else 0.0) > 0.5
 
     # host-link roofline BW_host(k = world): pinned copy of 4 GiB, all ranks at once
@@ -297,7 +315,7 @@ def run_plex(a):
         if duplex:
             out.switch_to(inc)
         else:
-            out.suspend()
+            out.suspend(release=out is not inc)
             inc.resume()
         if ev:
             ev[1].record()
@@ -395,10 +413,14 @@ def run_plex(a):
             "warmup": a.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16/fp32 bits (byte copy; fp32->bf16 RNE integer cast)",
             "data": "synthetic (counter-based generator, DESIGN.md §3); random-init Qwen2.5-7B-shaped state",
-            "config": {"workload": f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
-                                   f"rollout TP-{tp}xDP-{dp}; step = context switch A->B (full suspend of A + full "
-                                   f"resume of B, {'duplex: offload || onload' if duplex else 'sequential'}) + "
-                                   f"weight sync of B",
+            "config": {"workload": (f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
+                                    f"rollout TP-{tp}xDP-{dp}; step = context switch A->B (full suspend of A + full "
+                                    f"resume of B, {'duplex: offload || onload' if duplex else 'sequential'}) + "
+                                    f"weight sync of B") if two_jobs else
+                                   (f"one {a.model}-shaped job (bf16 param + fp32 master/m/v) FSDP-{world} -> rollout "
+                                    f"TP-{tp}xDP-{dp}; step = full suspend + full resume + weight sync (two jobs' "
+                                    f"slabs exceed the host's pinnable memory)"),
+                       "jobs": 2 if two_jobs else 1,
                        "model_shape": a.model, "state_bytes_per_rank_per_job": info.payload_bytes,
                        "bytes_switched_per_step": int(S_total), "duplex": duplex,
                        "bucket_bytes": bucket, "staging_slots": a.slots,

@@ -181,9 +181,17 @@ struct TmaCfg {
     static constexpr int kConsumers = CWARPS * 32;
     static constexpr int kThreads = kConsumers + 32;
     static constexpr int kCtasPerSm = CTAS;
-    static constexpr size_t kSmem = (size_t)STAGES * kChunk + 2 * STAGES * sizeof(uint64_t);
+    static constexpr int kBatch = 128;                      // item descriptors staged per batch
+    static constexpr size_t kBarOff = (size_t)STAGES * kChunk;
+    static constexpr size_t kGeoOff = kBarOff + 2 * STAGES * sizeof(uint64_t);
+    static constexpr size_t kSmem = kGeoOff + kBatch * sizeof(ItemGeo);
 };
 
+// The CTA's work items (i = blockIdx.x + k * gridDim.x) are resolved in batches
+// of kBatch: every thread of the CTA fetches one item's PackItem -> SegDev ->
+// shard pointer chain in parallel and the resulting geometry is staged in
+// shared memory, so neither the TMA producer nor the consumers ever stall on
+// that dependent-load chain inside the streaming loop.
 template <bool kPack, class Cfg>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
@@ -192,11 +200,14 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     constexpr int kStages = Cfg::kStages;
     constexpr uint32_t kChunk = Cfg::kChunk;
     constexpr int kConsumers = Cfg::kConsumers;
+    constexpr int kBatch = Cfg::kBatch;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kChunk);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
     uint64_t* empty = full + kStages;
+    ItemGeo* geo = reinterpret_cast<ItemGeo*>(smem + Cfg::kGeoOff);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const bool producer = tid >= kConsumers;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
@@ -205,87 +216,93 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-
-    if (tid >= kConsumers) {
-        // ---------------- producer warp: TMA loads ----------------
-        if (tid != kConsumers) return;
-        uint32_t q = 0;
-        for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
-            const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+    const uint32_t mine = n_items > blockIdx.x ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    uint32_t q = 0;                                       // chunk sequence number (ring position)
+    for (uint32_t b0 = 0; b0 < mine; b0 += kBatch) {
+        const uint32_t nb_items = mine - b0 < (uint32_t)kBatch ? mine - b0 : (uint32_t)kBatch;
+        __syncthreads();                                  // previous batch fully consumed
+        for (uint32_t k = tid; k < nb_items; k += Cfg::kThreads)
+            geo[k] = item_geo(items[blockIdx.x + (b0 + k) * gridDim.x], segs, ptrs, staging, bucket_lo);
+        __syncthreads();
+        if (producer) {
+            // ---------------- producer warp: TMA loads ----------------
+            if (tid == kConsumers) {
+                for (uint32_t k = 0; k < nb_items; ++k) {
+                    const ItemGeo g = geo[k];
+                    const uint8_t* src = kPack ? g.tens : g.buf;
+                    for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
+                        const int st = (int)(q % kStages);
+                        if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+                        const uint32_t nb = chunk_bulk(g, co, kChunk);
+                        if (nb) {
+                            mbar_arrive_tx(&full[st], nb);
+                            bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
+                        } else {
+                            mbar_arrive(&full[st]);
+                        }
+                    }
+                }
+            }
+            continue;
+        }
+        // ---------------- consumer warps: checksum + TMA stores ----------------
+        for (uint32_t k = 0; k < nb_items; ++k) {
+            const ItemGeo g = geo[k];
             const uint8_t* src = kPack ? g.tens : g.buf;
+            uint8_t* dst = kPack ? g.buf : g.tens;
+            Cks c;
             for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
                 const int st = (int)(q % kStages);
-                if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+                const uint8_t* sm = smem + (size_t)st * kChunk;
                 const uint32_t nb = chunk_bulk(g, co, kChunk);
-                if (nb) {
-                    mbar_arrive_tx(&full[st], nb);
-                    bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
-                } else {
-                    mbar_arrive(&full[st]);
+                const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
+                const uint32_t dend = g.data < cend ? g.data : cend;    // data end within chunk
+                mbar_wait(&full[st], (q / kStages) & 1);
+                if (tid == 0 && nb) {
+                    bulk_store(dst + co, sm, nb);                       // write back while we checksum
+                    bulk_commit();
                 }
-            }
-        }
-        return;
-    }
-    // ---------------- consumer warps: checksum + TMA stores ----------------
-    uint32_t q = 0;
-    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
-        const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
-        const uint8_t* src = kPack ? g.tens : g.buf;
-        uint8_t* dst = kPack ? g.buf : g.tens;
-        Cks c;
-        for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
-            const int st = (int)(q % kStages);
-            const uint8_t* sm = smem + (size_t)st * kChunk;
-            const uint32_t nb = chunk_bulk(g, co, kChunk);
-            const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
-            const uint32_t dend = g.data < cend ? g.data : cend;        // data end within chunk
-            mbar_wait(&full[st], (q / kStages) & 1);
-            if (tid == 0 && nb) {
-                bulk_store(dst + co, sm, nb);                           // write back while we checksum
-                bulk_commit();
-            }
-            // checksum of the bulk part, read back from shared memory
-            for (uint32_t v = tid; v < nb / 16; v += kConsumers)
-                c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
-            // non-bulk data (misaligned tensor or <16-B tail): element by element
-            const uint32_t t0 = co + nb;
-            if (t0 < dend) {
-                const uint32_t ne = (dend - t0) / g.es;
-                for (uint32_t e = tid; e < ne; e += kConsumers) {
-                    const uint32_t off = t0 + e * g.es;
-                    uint32_t b;
-                    if (g.es == 4) {
-                        b = *reinterpret_cast<const uint32_t*>(src + off);
-                        *reinterpret_cast<uint32_t*>(dst + off) = b;
-                    } else {
-                        b = *reinterpret_cast<const uint16_t*>(src + off);
-                        *reinterpret_cast<uint16_t*>(dst + off) = (uint16_t)b;
+                // checksum of the bulk part, read back from shared memory
+                for (uint32_t v = tid; v < nb / 16; v += kConsumers)
+                    c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
+                // non-bulk data (misaligned tensor or <16-B tail): element by element
+                const uint32_t t0 = co + nb;
+                if (t0 < dend) {
+                    const uint32_t ne = (dend - t0) / g.es;
+                    for (uint32_t e = tid; e < ne; e += kConsumers) {
+                        const uint32_t off = t0 + e * g.es;
+                        uint32_t b;
+                        if (g.es == 4) {
+                            b = *reinterpret_cast<const uint32_t*>(src + off);
+                            *reinterpret_cast<uint32_t*>(dst + off) = b;
+                        } else {
+                            b = *reinterpret_cast<const uint16_t*>(src + off);
+                            *reinterpret_cast<uint16_t*>(dst + off) = (uint16_t)b;
+                        }
+                        c.add_elem(b, g.ib + off / g.es);
                     }
-                    c.add_elem(b, g.ib + off / g.es);
+                }
+                if (kPack && dend < cend) {
+                    const uint32_t p0 = co > g.data ? co : g.data;
+                    for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);                 // this warp is done with stage st
+                if (tid == 0) {
+                    if (nb) bulk_wait_read_all();                       // the bulk store has read stage st
+                    mbar_arrive(&empty[st]);
                 }
             }
-            if (kPack && dend < cend) {
-                const uint32_t p0 = co > g.data ? co : g.data;
-                for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);                     // this warp is done with stage st
-            if (tid == 0) {
-                if (nb) bulk_wait_read_all();                           // the bulk store has read stage st
-                mbar_arrive(&empty[st]);
-            }
-        }
-        if (g.data) {
+            if (g.data) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
-                c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
-            }
-            if (lane == 0) {
-                atomicAdd(cks + 2 * g.seg, c.s1);
-                atomicAdd(cks + 2 * g.seg + 1, c.s2);
+                for (int o = 16; o > 0; o >>= 1) {
+                    c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
+                    c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
+                }
+                if (lane == 0) {
+                    atomicAdd(cks + 2 * g.seg, c.s1);
+                    atomicAdd(cks + 2 * g.seg + 1, c.s2);
+                }
             }
         }
     }
@@ -531,8 +548,9 @@ static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const 
                                                                               bucket_lo, cks);
             return cudaGetLastError();
         }
-        case 5: return launch_tma<kPack, TmaCfg<3, 32, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        default: return launch_tma<kPack, TmaCfg<6, 32, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 5: return launch_tma<kPack, TmaCfg<6, 32, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 6: return launch_tma<kPack, TmaCfg<4, 24, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        default: return launch_tma<kPack, TmaCfg<3, 32, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
     }
 }
 

@@ -720,8 +720,10 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         }
     }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
+    // Both halves' kernels share the ctx pack stream: they are ~100x faster
+    // than the copies, and serialising them keeps each launch's SMs to itself.
     Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
-            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2};
+            c->ev_copy2.data(), c->pack, c->copy2, c->h_ptrs2, c->d_ptrs2};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));

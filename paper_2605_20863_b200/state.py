@@ -226,6 +226,31 @@ class Slab:
         return np.frombuffer(buf, dtype=np.uint64)[:n].reshape(-1, 2).copy()
 
 
+def bootstrap_nccl_id(rank: int) -> bytes:
+    """Rank 0 draws the library communicator's 128-byte NCCL id; every rank
+    receives it over the default torch.distributed group (any backend)."""
+    import torch.distributed as dist
+    buf = C.create_string_buffer(128)
+    if rank == 0:
+        check(lib.plex_nccl_unique_id(buf))
+    obj = [bytes(buf.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def plan_digest(plan: "Plan", rank: int) -> str:
+    """Hash of everything rank-specific a plan holds (slab segments, rollout
+    tensors, ledger): identical requests must give identical plans on every rank."""
+    import hashlib
+    h = hashlib.sha256()
+    for sg in plan.segments(rank):
+        h.update(bytes(sg))
+    for name, off, shape in plan.dst_tensors(rank):
+        h.update(f"{name}:{off}:{shape}".encode())
+    h.update(plan.ledger().tobytes())
+    return h.hexdigest()
+
+
 def _stream_ptr(s) -> int:
     if s is None:
         return torch.cuda.current_stream().cuda_stream
@@ -263,13 +288,7 @@ class StateManager:
         self.h = h
 
     def _bootstrap_id(self) -> bytes:
-        import torch.distributed as dist
-        buf = C.create_string_buffer(128)
-        if self.rank == 0:
-            check(lib.plex_nccl_unique_id(buf))
-        obj = [bytes(buf.raw) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        return obj[0]
+        return bootstrap_nccl_id(self.rank)
 
     def close(self):
         h = getattr(self, "h", None)

@@ -30,3 +30,16 @@ def test_collective_sync_multi_gpu(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_fullsize_7b_multi_gpu(n):
+    """bench.py's workload at N GPUs: duplex switches + collective sync, sampled parity."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mp_fullsize_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
