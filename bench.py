@@ -45,9 +45,10 @@ def parse():
     ap.add_argument("--model", default="qwen2.5-7b")
     ap.add_argument("--tp", type=int, default=0, help="rollout TP (default min(2, N))")
     ap.add_argument("--ep", type=int, default=1)
-    ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--bucket-mb", type=int, default=1024)
     ap.add_argument("--slots", type=int, default=3)
-    ap.add_argument("--hugepage", action="store_true")
+    ap.add_argument("--no-hugepage", dest="hugepage", action="store_false",
+                    help="pin slabs with cudaHostAlloc instead of mmap(MADV_HUGEPAGE) + cudaHostRegister")
     ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")
     ap.add_argument("--single-job", action="store_true", help="step = suspend + resume + sync of one job")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")

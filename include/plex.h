@@ -140,7 +140,19 @@ typedef struct {
     int64_t resident_job;
     int64_t incoming_job;
     int32_t op;
+    uint32_t flags;              /* PLEX_PLAN_* */
 } plex_plan_req;
+
+/* Plan flags. */
+/* NEXT-2 derived-state elision (canonical non-redundant
+ * offloaded state): with KIND_MAJOR slabs carrying PARAM and MASTER, offload
+ * first checks on the device that every bf16 param of the leading buckets
+ * equals RNE(master) (R8) -- true after every mixed-precision optimizer step
+ * -- and if so neither packs nor copies those buckets; onload re-derives them
+ * from the restored master.  Checksums cover the derived params, so a failed
+ * derivation is still caught (E_CHECKSUM).  Falls back to a full offload when
+ * any element differs. */
+#define PLEX_PLAN_ELIDE_PARAM 0x1u
 
 typedef struct {
     int32_t n_ops;               /* transition op list       */
@@ -164,6 +176,8 @@ typedef struct {
     uint64_t recv_bytes;         /* bf16 bytes peers push to this rank      */
     uint64_t local_bytes;        /* bf16 bytes cast locally (no transfer)   */
     uint64_t src_read_bytes;     /* fp32 bytes read by this rank's push     */
+    int32_t elide_buckets;       /* leading buckets elidable (PLEX_PLAN_ELIDE_PARAM) */
+    uint64_t elide_bytes;        /* slab bytes those buckets span           */
 } plex_rank_info;
 
 typedef struct {
@@ -196,7 +210,8 @@ typedef struct {
 #define PLEX_STAT_NCCL    5      /* NCCL exchange (sync baseline) */
 #define PLEX_STAT_RPACK   6      /* K4 reshard-pack (NCCL path) */
 #define PLEX_STAT_RUNPACK 7      /* K5 reshard-unpack (NCCL path) */
-#define PLEX_NUM_STATS    8
+#define PLEX_STAT_DERIVE  8      /* NEXT-2 param check / re-derivation */
+#define PLEX_NUM_STATS    9
 
 /* ---- errors / version ---------------------------------------------------- */
 PLEX_API const char* plex_last_error(void);
@@ -240,6 +255,8 @@ PLEX_API plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t f
 PLEX_API plex_status plex_slab_destroy(plex_slab_t slab);
 /* host_ptr: the slab bytes (read/write, for verification and fault injection) */
 PLEX_API plex_status plex_slab_info(plex_slab_t slab, void** host_ptr, uint64_t* bytes, int32_t* residency);
+/* *elided = 1 if the last offload elided the derived PARAM buckets. */
+PLEX_API plex_status plex_slab_elided(plex_slab_t slab, int32_t* elided);
 /* out[2*i], out[2*i+1] = (S1, S2) of segment i recorded at offload (R14). */
 PLEX_API plex_status plex_slab_checksums(plex_slab_t slab, uint64_t* out, int32_t n);
 

@@ -23,15 +23,16 @@ OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
 RES_DEVICE, RES_HOST = 0, 1
 CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
 SLAB_HUGEPAGE = 0x1
-STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK = range(8)
-STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack")
-NUM_STATS = 8
+STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE = range(9)
+STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive")
+NUM_STATS = 9
+PLAN_ELIDE_PARAM = 0x1
 
 EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
-    "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_checksums",
+    "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
@@ -54,7 +55,7 @@ class PlanReq(C.Structure):
                 ("tp", C.c_int32), ("dp", C.c_int32), ("ep", C.c_int32), ("rank_map", C.c_int32),
                 ("slab_layout", C.c_int32), ("kind_mask", C.c_uint32), ("n_subset", C.c_int32),
                 ("subset", C.POINTER(C.c_int32)), ("bucket_bytes", C.c_uint64), ("tile_bytes", C.c_uint64),
-                ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32)]
+                ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32), ("flags", C.c_uint32)]
 
 
 class PlanStats(C.Structure):
@@ -67,7 +68,8 @@ class RankInfo(C.Structure):
     _fields_ = [("slab_bytes", C.c_uint64), ("payload_bytes", C.c_uint64), ("n_segments", C.c_int32),
                 ("n_buckets", C.c_int32), ("n_pack_items", C.c_uint64), ("dst_arena_bytes", C.c_uint64),
                 ("n_dst_tensors", C.c_int32), ("n_push_items", C.c_uint64), ("send_bytes", C.c_uint64),
-                ("recv_bytes", C.c_uint64), ("local_bytes", C.c_uint64), ("src_read_bytes", C.c_uint64)]
+                ("recv_bytes", C.c_uint64), ("local_bytes", C.c_uint64), ("src_read_bytes", C.c_uint64),
+                ("elide_buckets", C.c_int32), ("elide_bytes", C.c_uint64)]
 
 
 class SegDesc(C.Structure):
@@ -108,6 +110,7 @@ def _load() -> C.CDLL:
         "plex_slab_create": (C.c_int, [VP, I32, U32, P(VP)]),
         "plex_slab_destroy": (C.c_int, [VP]),
         "plex_slab_info": (C.c_int, [VP, P(VP), P(U64), P(I32)]),
+        "plex_slab_elided": (C.c_int, [VP, P(I32)]),
         "plex_slab_checksums": (C.c_int, [VP, P(U64), I32]),
         "plex_state_offload": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_state_onload": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),

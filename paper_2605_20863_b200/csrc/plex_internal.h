@@ -82,6 +82,7 @@ struct RankPlan {
     std::vector<PackItem> items;
     std::vector<uint64_t> bucket_item_start;    // n_buckets + 1
     uint64_t slab_bytes = 0, payload_bytes = 0;
+    int32_t elide_buckets = 0;                  // NEXT-2: leading buckets inside the PARAM region
     // rollout
     std::vector<DstTensor> dst;
     uint64_t arena_bytes = 0;
@@ -94,6 +95,7 @@ struct Plan {
     int32_t world = 1, tp = 0, dp = 0, ep = 1, rank_map = 0, layout = 0;
     uint32_t kind_mask = PLEX_KINDMASK_ALL;
     uint64_t bucket = kDefaultBucket, tile = kDefaultTile;
+    uint32_t flags = 0;
     std::vector<int32_t> subset;                // sorted tensor indices in the slab
     std::vector<RankPlan> ranks;
     std::vector<uint64_t> ledger;               // world * world

@@ -442,6 +442,63 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
     }
 }
 
+// ---- NEXT-2: derived-param check / re-derivation -------------------------------
+// Over PackItems of PARAM segments: kCheck -> count elements whose bf16 param
+// differs from RNE(master) (R8) and checksum the params; !kCheck -> write
+// param = RNE(master) and checksum what was written.  The master shard of
+// tensor t sits at pointer slot ptr_slot + n_tensors (kind 1 vs kind 0).
+template <bool kCheck>
+__global__ void __launch_bounds__(kThreads) derive_kernel(const PackItem* __restrict__ items,
+                                                          const SegDev* __restrict__ segs,
+                                                          const uint64_t* __restrict__ ptrs, uint32_t n_tensors,
+                                                          unsigned long long* __restrict__ cks, int* __restrict__ bad) {
+    const PackItem it = items[blockIdx.x];
+    const SegDev s = segs[it.seg];
+    const uint64_t o0 = it.slab_lo - s.slab_off;
+    if (o0 >= s.bytes) return;                                  // padding only
+    const uint64_t nbytes = (s.bytes - o0 < it.len ? s.bytes - o0 : it.len);
+    const uint64_t n = nbytes / 2;                              // bf16 elements
+    uint16_t* param = reinterpret_cast<uint16_t*>(ptrs[s.ptr_slot] + o0);
+    const uint32_t* master = reinterpret_cast<const uint32_t*>(ptrs[s.ptr_slot + n_tensors] + 2 * o0);
+    const uint64_t ib = s.index_base + o0 / 2;
+    Cks c;
+    int miss = 0;
+    const bool vec = ((reinterpret_cast<uintptr_t>(param) & 15) == 0) && ((reinterpret_cast<uintptr_t>(master) & 15) == 0);
+    const uint64_t nv = vec ? n / 8 : 0;
+    for (uint64_t v = threadIdx.x; v < nv; v += kThreads) {
+        const uint4 r = rne_8(ld_stream(master + 8 * v), ld_stream(master + 8 * v + 4));
+        if (kCheck) {
+            const uint4 x = ld_stream(param + 8 * v);
+            miss |= (x.x != r.x) | (x.y != r.y) | (x.z != r.z) | (x.w != r.w);
+            c.add_vec(x, 2, ib + 8 * v);
+        } else {
+            st_v4(param + 8 * v, r);
+            c.add_vec(r, 2, ib + 8 * v);
+        }
+    }
+    for (uint64_t e = nv * 8 + threadIdx.x; e < n; e += kThreads) {
+        const uint32_t r = rne_bf16(master[e]);
+        uint32_t b = r;
+        if (kCheck) {
+            b = param[e];
+            miss |= (b != r);
+        } else {
+            param[e] = (uint16_t)r;
+        }
+        c.add_elem(b, ib + e);
+    }
+    if (kCheck && __syncthreads_or(miss) && threadIdx.x == 0) atomicAdd(bad, 1);
+    block_reduce_add(c, cks + 2 * it.seg);
+}
+
+cudaError_t launch_derive(bool check, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                          uint32_t n_tensors, unsigned long long* cks, int* bad, cudaStream_t s) {
+    if (!n_items) return cudaSuccess;
+    if (check) derive_kernel<true><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, n_tensors, cks, bad);
+    else derive_kernel<false><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, n_tensors, cks, bad);
+    return cudaGetLastError();
+}
+
 __global__ void cast_kernel(const uint32_t* __restrict__ src, uint16_t* __restrict__ dst, uint64_t n) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);

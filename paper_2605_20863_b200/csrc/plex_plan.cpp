@@ -97,6 +97,15 @@ static plex_status build_slab(Plan& p, int32_t r) {
         R.bucket_item_start[b] = it;
     }
     R.bucket_item_start[nb] = R.items.size();
+    // NEXT-2: buckets lying entirely inside the leading PARAM region of a
+    // KIND_MAJOR slab that also carries MASTER can be derived instead of moved.
+    if ((p.flags & PLEX_PLAN_ELIDE_PARAM) && p.layout == PLEX_SLAB_KIND_MAJOR &&
+        (p.kind_mask & (1u << PLEX_KIND_PARAM)) && (p.kind_mask & (1u << PLEX_KIND_MASTER))) {
+        uint64_t param_end = R.slab_bytes;
+        for (const plex_seg_desc& d : R.seg_desc)
+            if (d.kind != PLEX_KIND_PARAM) { param_end = d.slab_offset; break; }
+        R.elide_buckets = (int32_t)(param_end / B);
+    }
     return PLEX_OK;
 }
 
@@ -224,6 +233,7 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
     p.kind_mask = q->kind_mask ? q->kind_mask : PLEX_KINDMASK_ALL;
     p.bucket = q->bucket_bytes ? q->bucket_bytes : kDefaultBucket;
     p.tile = q->tile_bytes ? q->tile_bytes : kDefaultTile;
+    p.flags = q->flags;
     if (p.bucket % kSegAlign || p.tile % kSegAlign || p.tile > (1ull << 31)) {
         set_error("bucket/tile must be multiples of 256 B (tile < 2 GiB)"); return PLEX_E_INVAL;
     }
@@ -374,6 +384,8 @@ plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* 
     o.recv_bytes = R.recv_bytes;
     o.local_bytes = R.local_bytes;
     o.src_read_bytes = R.src_read_bytes;
+    o.elide_buckets = R.elide_buckets;
+    o.elide_bytes = std::min<uint64_t>(R.slab_bytes, (uint64_t)R.elide_buckets * p.bucket);
     *out = o;
     return PLEX_OK;
 }

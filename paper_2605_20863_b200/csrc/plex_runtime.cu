@@ -34,6 +34,8 @@ cudaError_t launch_synth(void* dst, int kind, uint64_t base, uint64_t index_base
 cudaError_t launch_mutate(void* buf, int esize, uint64_t base, uint64_t index_base, uint64_t n, cudaStream_t s);
 cudaError_t launch_checksum(const void* src, int es, uint64_t index_base, uint64_t n, unsigned long long* out,
                             cudaStream_t s);
+cudaError_t launch_derive(bool check, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
+                          uint32_t n_tensors, unsigned long long* cks, int* bad, cudaStream_t s);
 // NCCL-baseline sync kernels (plex_nccl_sync.cu)
 plex_status nccl_sync(plex_ctx_s* ctx, const Plan& p, const void* const* src, void* arena, cudaStream_t caller);
 
@@ -42,6 +44,7 @@ plex_status nccl_sync(plex_ctx_s* ctx, const Plan& p, const void* const* src, vo
         cudaError_t e_ = (x);                                                                  \
         if (e_ != cudaSuccess) {                                                               \
             set_error("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));         \
+            (void)cudaGetLastError(); /* do not leak a handled error into the next launch */   \
             return PLEX_E_CUDA;                                                                \
         }                                                                                      \
     } while (0)
@@ -63,6 +66,7 @@ struct DevPlan {
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
     unsigned long long* cks_in = nullptr;     // recomputed at onload
     std::vector<uint64_t> bucket_payload;     // data bytes per bucket (stats)
+    uint64_t elide_payload = 0;               // PARAM data bytes in the elidable buckets
     // NCCL-baseline schedule (built lazily for one per-pair round quota Q)
     uint64_t nq = 0;                          // Q it was built for (0 = none)
     int rounds = 0;
@@ -132,6 +136,7 @@ struct plex_slab_s {
     size_t map_bytes = 0;
     int residency = PLEX_RES_DEVICE;
     bool written = false;
+    bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
 };
 
@@ -187,6 +192,7 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
         const uint64_t de = std::min(o1, sg.bytes);
         if (de > o0) d.bucket_payload[it.slab_lo / p.bucket] += de - o0;
     }
+    for (int32_t b = 0; b < R.elide_buckets; ++b) d.elide_payload += d.bucket_payload[b];
     *out = &(c->dev[p.id] = d);
     return PLEX_OK;
 }
@@ -317,14 +323,35 @@ struct Half {           // one offload or onload in flight
     plex_slab_s* slab;
     int32_t nb;
     std::vector<uint64_t> cks;     // offload: recorded checksums (host)
+    int32_t b0 = 0;                // first bucket moved (NEXT-2: earlier ones derived)
 };
 
 static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     const size_t np = PLEX_NUM_KINDS * h.p->tensors.size();
+    const size_t ckb = 16 * std::max<size_t>(1, h.R->segs.size());
     CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
-    CK(cudaMemsetAsync(h.d->cks, 0, 16 * std::max<size_t>(1, h.R->segs.size()), pp.kern));
+    CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));
     h.nb = n_buckets(*h.p, *h.R);
     h.cks.assign(2 * h.R->segs.size(), 0);
+    h.b0 = 0;
+    if (h.R->elide_buckets > 0) {
+        // NEXT-2: do the leading PARAM buckets hold exactly RNE(master)?
+        const uint32_t ni = (uint32_t)h.R->bucket_item_start[h.R->elide_buckets];
+        CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
+        cudaEvent_t ta = nullptr;
+        plex_status st;
+        if ((st = timed_begin(c, pp.kern, &ta))) return st;
+        CK(launch_derive(true, h.d->items, ni, h.d->segs, pp.d_ptrs, (uint32_t)h.p->tensors.size(), h.d->cks,
+                         c->d_flag, pp.kern));
+        if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
+        CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
+        CK(cudaStreamSynchronize(pp.kern));
+        if (*c->h_flag == 0) {
+            h.b0 = h.R->elide_buckets;
+        } else {
+            CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));    // full offload after all
+        }
+    }
     return PLEX_OK;
 }
 
@@ -365,6 +392,7 @@ static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     if (nck) CK(cudaMemcpyAsync(h.d->cks_want, h.slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, pp.kern));
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
     h.nb = n_buckets(*h.p, *h.R);
+    h.b0 = h.slab->elided ? h.R->elide_buckets : 0;
     return PLEX_OK;
 }
 
@@ -392,6 +420,15 @@ static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
 }
 
 static plex_status on_end(plex_ctx_s* c, Pipe& pp, Half& h) {
+    if (h.b0 > 0) {   // NEXT-2: re-derive the elided params from the restored master
+        const uint32_t ni = (uint32_t)h.R->bucket_item_start[h.b0];
+        cudaEvent_t ta = nullptr;
+        plex_status st;
+        if ((st = timed_begin(c, pp.kern, &ta))) return st;
+        CK(launch_derive(false, h.d->items, ni, h.d->segs, pp.d_ptrs, (uint32_t)h.p->tensors.size(), h.d->cks_in,
+                         c->d_flag, pp.kern));
+        if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
+    }
     CK(launch_verify(h.d->cks_in, h.d->cks_want, (uint32_t)h.R->segs.size(), c->d_flag, pp.kern));
     CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
     return PLEX_OK;
@@ -569,13 +606,14 @@ plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, ple
         s->map_bytes = align_up(alloc, huge);
         void* p = mmap(nullptr, s->map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
         if (p == MAP_FAILED) {
-            delete s;
             set_error("mmap of %zu B failed", s->map_bytes);
+            delete s;
             return PLEX_E_TIER_FULL;
         }
         madvise(p, s->map_bytes, MADV_HUGEPAGE);
         cudaError_t e = cudaHostRegister(p, s->map_bytes, cudaHostRegisterDefault);
         if (e != cudaSuccess) {
+            (void)cudaGetLastError();
             munmap(p, s->map_bytes);
             delete s;
             set_error("cudaHostRegister(%zu B): %s", alloc, cudaGetErrorString(e));
@@ -586,6 +624,7 @@ plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, ple
     } else {
         cudaError_t e = cudaHostAlloc(&s->host, alloc, cudaHostAllocPortable);
         if (e != cudaSuccess) {
+            (void)cudaGetLastError();
             delete s;
             set_error("cudaHostAlloc(%zu B): %s", alloc, cudaGetErrorString(e));
             return PLEX_E_TIER_FULL;
@@ -615,6 +654,12 @@ plex_status plex_slab_info(plex_slab_t s, void** host_ptr, uint64_t* bytes, int3
     return PLEX_OK;
 }
 
+plex_status plex_slab_elided(plex_slab_t s, int32_t* elided) {
+    if (!s || !elided) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    *elided = s->elided ? 1 : 0;
+    return PLEX_OK;
+}
+
 plex_status plex_slab_checksums(plex_slab_t s, uint64_t* out, int32_t n) {
     if (!s || !out || (size_t)n != s->cks.size()) { set_error("need %zu entries", s ? s->cks.size() : 0); return PLEX_E_INVAL; }
     std::memcpy(out, s->cks.data(), 8 * s->cks.size());
@@ -636,12 +681,13 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
     if ((st = off_begin(c, pp, h))) return st;
-    for (int32_t b = 0; b < h.nb; ++b)
+    for (int32_t b = h.b0; b < h.nb; ++b)
         if ((st = off_bucket(c, pp, h, b))) return st;
     if ((st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
     slab->cks.swap(h.cks);
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
+    slab->elided = h.b0 > 0;
     return PLEX_OK;
 }
 
@@ -665,7 +711,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
     if ((st = on_begin(c, pp, h))) return st;
-    for (int32_t b = 0; b < h.nb; ++b)
+    for (int32_t b = h.b0; b < h.nb; ++b)
         if ((st = on_bucket(c, pp, h, b))) return st;
     if ((st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
     if (*c->h_flag) {
@@ -729,10 +775,10 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
     if (do_off && (st = off_begin(c, po, ho))) return st;
     if (do_on && (st = on_begin(c, pi, hi))) return st;
-    const int32_t nb = std::max(do_off ? ho.nb : 0, do_on ? hi.nb : 0);
-    for (int32_t b = 0; b < nb; ++b) {        // interleave so both directions start at once
-        if (do_off && b < ho.nb && (st = off_bucket(c, po, ho, b))) return st;
-        if (do_on && b < hi.nb && (st = on_bucket(c, pi, hi, b))) return st;
+    const int32_t no = do_off ? ho.nb - ho.b0 : 0, ni = do_on ? hi.nb - hi.b0 : 0;
+    for (int32_t k = 0; k < std::max(no, ni); ++k) {   // interleave so both directions start at once
+        if (k < no && (st = off_bucket(c, po, ho, ho.b0 + k))) return st;
+        if (k < ni && (st = on_bucket(c, pi, hi, hi.b0 + k))) return st;
     }
     if (do_off && (st = off_end(c, po, ho))) return st;
     if (do_on && (st = on_end(c, pi, hi))) return st;
@@ -747,6 +793,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         slab_out->cks.swap(ho.cks);
         slab_out->residency = PLEX_RES_HOST;
         slab_out->written = true;
+        slab_out->elided = ho.b0 > 0;
     }
     if (do_on) {
         if (*c->h_flag) {

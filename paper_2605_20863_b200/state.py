@@ -89,8 +89,8 @@ class Plan:
     def __init__(self, manifest, head_dim: int = 1, world: int = 1, tp: int = 0, dp: int = 0, ep: int = 1,
                  rank_map: int = L.RANKMAP_TP_FAST, slab_layout: int = L.SLAB_KIND_MAJOR,
                  kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
-                 bucket_bytes: int = 256 << 20, tile_bytes: int = 64 << 10,
-                 resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE):
+                 bucket_bytes: int = 1 << 30, tile_bytes: int = 64 << 10,
+                 resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE, elide_param: bool = False):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
         descs, self.group_names = describe(self.manifest, head_dim)
@@ -109,7 +109,8 @@ class Plan:
             n_sub = len(idx)
         self._sub = sub
         req = L.PlanReq(len(descs), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
-                        bucket_bytes, tile_bytes, resident_job, incoming_job, op)
+                        bucket_bytes, tile_bytes, resident_job, incoming_job, op,
+                        L.PLAN_ELIDE_PARAM if elide_param else 0)
         h = C.c_void_p()
         check(lib.plex_transition_plan(C.byref(req), C.byref(h)))
         self.h = h
@@ -212,6 +213,13 @@ class Slab:
     def residency(self) -> int:
         return self.info()[2]
 
+    @property
+    def elided(self) -> bool:
+        """The last offload derived (did not store) the leading PARAM buckets (NEXT-2)."""
+        v = C.c_int32()
+        check(lib.plex_slab_elided(self.h, C.byref(v)))
+        return bool(v.value)
+
     def host_bytes(self) -> np.ndarray:
         """Writable NumPy view of the pinned slab bytes."""
         p, n, _ = self.info()
@@ -260,7 +268,7 @@ def _stream_ptr(s) -> int:
 class StateManager:
     """One per rank process: the ctx (streams, staging, NCCL communicator)."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 256 << 20,
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 1 << 30,
                  n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
                  nccl_id: Optional[bytes] = None, duplex: bool = True):
         if not torch.cuda.is_available():
@@ -404,7 +412,7 @@ class Job:
     a5 (device storage freed while HOST-resident)."""
 
     def __init__(self, mgr: StateManager, plan: Plan, seed: int = 0, rank: Optional[int] = None,
-                 hugepage: bool = False, slab: bool = True):
+                 hugepage: bool = True, slab: bool = True):
         self.mgr, self.plan, self.seed = mgr, plan, seed
         self.rank = mgr.rank if rank is None else rank
         self.slab = Slab(plan, self.rank, hugepage) if slab else None
@@ -418,13 +426,20 @@ class Job:
                 self.shards[(key, kd)] = torch.empty(shp, dtype=KIND_TORCH[kd], device=self.dev)
         return self
 
-    def init_synthetic(self, special_bits: int = 0) -> "Job":
+    def init_synthetic(self, special_bits: int = 0, derived_param: bool = False) -> "Job":
+        """Counter-based synthetic state.  derived_param: the bf16
+        params are RNE(master) -- what a mixed-precision optimizer step leaves --
+        computed by this library's cast kernel instead of drawn independently."""
         for t, (key, shape) in enumerate(self.plan.manifest):
             r0, _ = self.plan.shard_rows(self.rank, t)
             re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
             for (k2, kd), x in self.shards.items():
-                if k2 == key:
+                if k2 == key and not (derived_param and kd == 0):
                     synth_fill(x, kd, self.seed, key, r0 * re_, special_bits)
+            if derived_param and (key, 0) in self.shards and (key, 1) in self.shards:
+                p, m = self.shards[(key, 0)], self.shards[(key, 1)]
+                if p.numel():
+                    cast_rne(m, p)
         return self
 
     def slab_shards(self):

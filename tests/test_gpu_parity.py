@@ -305,3 +305,45 @@ def test_duplex_switch_matches_oracle(models, buckets):
                     segs, size = O.slab_layout(manifest(mo), W, r)
                     assert np.array_equal(job.slab.host_bytes(), O.pack_slab(segs, size, osh))
         m.close()
+
+
+# ---- NEXT-2 derived-param elision ----------------------------------------------------------------
+@pytest.mark.parametrize("model,W,bucket", [("mid", 1, 4096), ("mid", 3, 1 << 14), ("toy-odd", 2, 512)])
+def test_param_elision(model, W, bucket):
+    man = manifest(model)
+    plan = P.Plan(man, world=W, bucket_bytes=bucket, tile_bytes=512, elide_param=True)
+    for r in range(W):
+        m = mgr(W, r, bucket=bucket)
+        info = plan.rank_info(r)
+        assert info.elide_buckets >= 1
+        # params == RNE(master): the leading buckets are derived, not moved
+        job = P.Job(m, plan, seed=40, rank=r).alloc().init_synthetic(special_bits=3, derived_param=True)
+        before = {k: bits_np(v) for k, v in job.shards.items()}
+        full = full_state(model, seed=40, kinds=(1, 2, 3), special_bits=3)
+        for (k, kd) in list(full):
+            if kd == 1:
+                full[(k, 0)] = O.rne_bf16(full[(k, 1)])
+        osh = fsdp_shards(full, W, r, O.fsdp_rows)
+        for kk, x in before.items():
+            assert np.array_equal(x, osh[kk]), kk            # GPU inputs == oracle inputs
+        job.suspend()
+        assert job.slab.elided
+        segs, size = O.slab_layout(man, W, r)
+        want = O.pack_slab(segs, size, osh)
+        cut = info.elide_bytes
+        assert np.array_equal(job.slab.host_bytes()[cut:], want[cut:])     # stored part
+        want_ck = np.array(O.segment_checksums(segs, osh), dtype=np.uint64).reshape(-1, 2)
+        assert np.array_equal(job.slab.checksums(), want_ck)
+        job.resume()
+        for kk, x in job.shards.items():
+            assert np.array_equal(bits_np(x), osh[kk]), kk
+        # break the invariant on one element: full offload, still bit-exact
+        p0 = next(v for (k, kd), v in job.shards.items() if kd == 0 and v.numel())
+        p0.view(-1)[0:1].view(torch.int16).add_(1)
+        state = {k: bits_np(v) for k, v in job.shards.items()}
+        job.suspend()
+        assert not job.slab.elided
+        job.resume()
+        for kk, x in job.shards.items():
+            assert np.array_equal(bits_np(x), state[kk]), kk
+        m.close()

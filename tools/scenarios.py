@@ -130,6 +130,39 @@ def scen_duplex(a, c: Ctx):
                     "during the switch"}, a.out)
 
 
+def scen_elide(a, c: Ctx):
+    """NEXT-2: the duplex switch of `duplex` with bf16 params = RNE(master) (what a
+    mixed-precision optimizer step leaves) and PLEX_PLAN_ELIDE_PARAM: the param
+    buckets are checked on the device and re-derived on resume instead of moved."""
+    shape = MODELS[a.model]
+    tp = a.tp or min(2, c.world)
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    out = {}
+    for elide in (False, True):
+        plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, elide_param=elide)
+                 for _ in range(2)]
+        jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic(derived_param=True) for pl, s in zip(plans, (1, 2))]
+        arena = mgr.arena(plans[0])
+        jobs[1].suspend()
+        state = {"cur": 0}
+
+        def step():
+            i = state["cur"]
+            jobs[i].switch_to(jobs[1 - i])
+            jobs[1 - i].sync(arena)
+            state["cur"] = 1 - i
+
+        ms, clk = timed(c, step, a.steps, a.warmup)
+        out["elided" if elide else "full"] = {"switch_plus_sync_ms": round(ms, 2),
+                                              "slab_elided": bool(jobs[1 - state["cur"]].slab.elided),
+                                              "elide_bytes_per_rank": plans[0].rank_info(c.rank).elide_bytes}
+        del jobs, arena, plans
+        torch.cuda.empty_cache()
+    c.emit({"scenario": "elide", "model": a.model, "n_gpus": c.world, "layout": f"FSDP-{c.world}->TP-{tp}",
+            **out, "speedup": round(out["full"]["switch_plus_sync_ms"] / out["elided"]["switch_plus_sync_ms"], 3)},
+           a.out)
+
+
 def scen_optim(a, c: Ctx):
     # each process = rank c.rank of an FSDP-8 plan; k = world processes copy at once
     W = 8
@@ -231,13 +264,13 @@ def scen_multiplex(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "optim", "moe", "multiplex"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--model", default="")
     ap.add_argument("--tp", type=int, default=0)
-    ap.add_argument("--bucket-mb", type=int, default=256)
+    ap.add_argument("--bucket-mb", type=int, default=1024)
     ap.add_argument("--units", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--duplex", action="store_true")
@@ -245,8 +278,9 @@ def main():
     a = ap.parse_args()
     c = Ctx(a.gpus)
     if not a.model:
-        a.model = {"duplex": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
-    {"duplex": scen_duplex, "optim": scen_optim, "moe": scen_moe, "multiplex": scen_multiplex}[a.scenario](a, c)
+        a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
+    {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
+     "multiplex": scen_multiplex}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
