@@ -312,6 +312,19 @@ PLEX_API plex_status plex_weight_sync(plex_ctx_t ctx, plex_plan_t plan, const vo
 PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, const void* const* src_master,
                                   int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream);
 
+/* ---- NEXT-3: sync from the offloaded canonical state ---------------------- */
+/* The sync of a SUSPENDED job, materialised "directly from managed memory"
+ * (PAPER.md:510, :576): each rank's fp32 master rows are read by the push
+ * kernel straight from its pinned slab (zero-copy over the host link) instead
+ * of device shards.  slab: this rank's HOST-resident slab of `plan` carrying
+ * MASTER for every tensor (E_STATE if not offloaded, E_INVAL if a tensor is
+ * missing).  Output, collectives and blocking contract as plex_weight_sync. */
+PLEX_API plex_status plex_weight_sync_from_slab(plex_ctx_t ctx, plex_plan_t plan, plex_slab_t slab, void* dst_arena,
+                                                void* caller_stream);
+/* Single-process emulation counterpart of plex_weight_sync_rank. */
+PLEX_API plex_status plex_weight_sync_rank_from_slab(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, plex_slab_t slab,
+                                                     void* const* dst_arenas, int32_t n_arenas, void* stream);
+
 /* ---- infrastructure (synthetic inputs / verification; not the method) ---- */
 /* K6: counter-based generator of DESIGN.md §3 (D2) writing `count` elements of
  * the logical tensor `key` starting at logical flat index `index_base`. */

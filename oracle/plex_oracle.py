@@ -471,3 +471,54 @@ def multiplex_replay(jobs: Sequence[dict], schedule: Sequence[int], world: int,
         else:
             final.append([parse_slab(slabs[i][r], layouts[i][r][0], shapes[i]) for r in range(world)])
     return visits, final
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4 — HRRS runtime ordering (Alg. 1; Eq. 3-4, :468-480)
+# ---------------------------------------------------------------------------
+@dataclass
+class Request:
+    job: int
+    arrival: float
+    exec_time: float            # E_i
+    remaining: float = 0.0      # for the running request
+
+
+def hrrs_score(req: Request, t_now: float, running: Optional[Request], t_load: float, t_offload: float) -> float:
+    """Eq. 3: S_i = E_i + 1_switch(i, curr) (T_offload + T_load); Eq. 4:
+    P_i = (W_i + S_i) / S_i.  The running request uses its remaining time
+    (Alg. 1 line 4).  1_switch = 1 iff the request's job differs from the
+    running request's job (reading H1: Alg. 1 line 7 charges every
+    non-running request; Eq. 3 only switching ones -- we follow Eq. 3)."""
+    t_wait = t_now - req.arrival
+    if running is not None and req is running:
+        t_req = req.remaining
+    else:
+        switch = running is None or req.job != running.job
+        t_req = req.exec_time + (t_load + t_offload if switch else 0.0)
+    return (t_wait + t_req) / t_req
+
+
+def hrrs_schedule(t_now: float, new: Request, running: Optional[Request], scheduled: Sequence[Request],
+                  t_load: float, t_offload: float) -> List[Tuple[Request, float, float]]:
+    """Alg. 1: score Omega = {new} + {running} + scheduled, sort by score
+    descending (stable), then lay the timeline out from t_now, inserting a
+    setup gap of T_offload + T_load before a request whose job differs from
+    the job resident at that point (reading H2: Alg. 1 lines 12-14 insert it
+    once, before the first non-running request; Eq. 3's indicator and
+    PAPER.md:555 imply one per job change).  Returns [(request, start, end)]."""
+    omega = [new] + ([running] if running is not None else []) + list(scheduled)
+    scores = [hrrs_score(r, t_now, running, t_load, t_offload) for r in omega]
+    order = sorted(range(len(omega)), key=lambda i: -scores[i])
+    t_cursor = t_now
+    resident = running.job if running is not None else None
+    out = []
+    for i in order:
+        r = omega[i]
+        if r.job != resident:
+            t_cursor += t_offload + t_load if resident is not None else t_load
+            resident = r.job
+        t_req = r.remaining if (running is not None and r is running) else r.exec_time
+        out.append((r, t_cursor, t_cursor + t_req))
+        t_cursor += t_req
+    return out

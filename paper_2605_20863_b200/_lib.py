@@ -34,6 +34,7 @@ EXPORTS = [
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
+    "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
 
@@ -117,6 +118,8 @@ def _load() -> C.CDLL:
         "plex_state_switch": (C.c_int, [VP, VP, P(VP), I32, VP, VP, VP, P(VP), I32, VP]),
         "plex_weight_sync": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_weight_sync_rank": (C.c_int, [VP, VP, I32, P(VP), I32, P(VP), I32, VP]),
+        "plex_weight_sync_from_slab": (C.c_int, [VP, VP, VP, VP, VP]),
+        "plex_weight_sync_rank_from_slab": (C.c_int, [VP, VP, I32, VP, P(VP), I32, VP]),
         "plex_synth_fill": (C.c_int, [VP, I32, U64, C.c_char_p, U64, U64, I32, VP]),
         "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
         "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),

@@ -192,7 +192,7 @@ struct TmaCfg {
 // shard pointer chain in parallel and the resulting geometry is staged in
 // shared memory, so neither the TMA producer nor the consumers ever stall on
 // that dependent-load chain inside the streaming loop.
-template <bool kPack, class Cfg>
+template <bool kPack, class Cfg, bool kCks = true>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
                 const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
@@ -263,8 +263,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
                     bulk_commit();
                 }
                 // checksum of the bulk part, read back from shared memory
-                for (uint32_t v = tid; v < nb / 16; v += kConsumers)
-                    c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
+                if (kCks)
+                    for (uint32_t v = tid; v < nb / 16; v += kConsumers)
+                        c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
                 // non-bulk data (misaligned tensor or <16-B tail): element by element
                 const uint32_t t0 = co + nb;
                 if (t0 < dend) {
@@ -576,19 +577,20 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 static int g_num_sms = 0;
 static int g_variant = -1;
 
-template <bool kPack, class Cfg>
+template <bool kPack, class Cfg, bool kCks = true>
 static cudaError_t launch_tma(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                               uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, Cfg, kCks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)Cfg::kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const uint32_t cap = (uint32_t)g_num_sms * Cfg::kCtasPerSm;
     const uint32_t grid = n_items < cap ? n_items : cap;
-    pack_kernel<kPack, Cfg><<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo, cks);
+    pack_kernel<kPack, Cfg, kCks><<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo,
+                                                                        cks);
     return cudaGetLastError();
 }
 
@@ -607,6 +609,10 @@ static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const 
         }
         case 5: return launch_tma<kPack, TmaCfg<6, 32, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
         case 6: return launch_tma<kPack, TmaCfg<4, 24, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 7:   // probe: the default pipeline without the checksum (not a valid pack)
+            return launch_tma<kPack, TmaCfg<3, 32, 4, 2>, false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 8: return launch_tma<kPack, TmaCfg<4, 16, 4, 3>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+        case 9: return launch_tma<kPack, TmaCfg<2, 48, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
         default: return launch_tma<kPack, TmaCfg<3, 32, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
     }
 }

@@ -566,8 +566,10 @@ plex_status plex_plan_destroy(plex_plan_t plan) {
     if (!plan) return PLEX_OK;
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     for (plex_ctx_s* c : g_ctxs) {
-        auto it = c->dev.find(plan->p.id);
-        if (it != c->dev.end()) {
+        for (int32_t r = -1; r < plan->p.world; ++r) {     // r >= 0: per-rank emulation tables
+            const uint64_t key = r < 0 ? plan->p.id : plan->p.id ^ (0x9E3779B97F4A7C15ull * (uint64_t)(r + 1));
+            auto it = c->dev.find(key);
+            if (it == c->dev.end()) continue;
             DeviceGuard g(c->device);
             cudaStreamSynchronize(c->pack);
             free_devplan(it->second);
@@ -920,6 +922,54 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
     if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push))) return st;
     if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all pushes landed
     return finish(c, caller);
+}
+
+// ---- NEXT-3: sync from the offloaded canonical state ------------------------------------
+// the StateManager "can materialize rollout-visible shards
+// directly from managed memory".  Each rank's fp32 master rows are read by the
+// push kernel straight out of its pinned slab (zero-copy over the host link)
+// while the job stays suspended; destinations and bytes are those of
+// plex_weight_sync.
+static plex_status slab_master_ptrs(const Plan& p, plex_slab_t slab, std::vector<const void*>& src) {
+    if (!slab || slab->plan_id != p.id) { set_error("slab does not belong to this plan"); return PLEX_E_INVAL; }
+    if (slab->residency != PLEX_RES_HOST || !slab->written) {
+        set_error("sync from slab needs HOST-resident offloaded state");
+        return PLEX_E_STATE;
+    }
+    void* dev = nullptr;
+    CK(cudaHostGetDevicePointer(&dev, slab->host, 0));
+    const RankPlan& R = p.ranks[slab->rank];
+    src.assign(p.tensors.size(), nullptr);
+    std::vector<char> seen(p.tensors.size(), 0);
+    for (const plex_seg_desc& d : R.seg_desc)
+        if (d.kind == PLEX_KIND_MASTER) {
+            src[d.tensor] = d.nbytes ? reinterpret_cast<uint8_t*>(dev) + d.slab_offset : nullptr;
+            seen[d.tensor] = 1;
+        }
+    for (size_t t = 0; t < seen.size(); ++t)
+        if (!seen[t]) { set_error("slab carries no master rows of tensor %zu", t); return PLEX_E_INVAL; }
+    return PLEX_OK;
+}
+
+plex_status plex_weight_sync_from_slab(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, void* dst_arena,
+                                       void* caller_stream) {
+    if (!c || !plan) { set_error("NULL ctx/plan"); return PLEX_E_INVAL; }
+    if (slab && slab->rank != c->rank) { set_error("slab belongs to rank %d, ctx is rank %d", slab->rank, c->rank); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    std::vector<const void*> src;
+    plex_status st = slab_master_ptrs(plan->p, slab, src);
+    if (st) return st;
+    return plex_weight_sync(c, plan, src.data(), (int32_t)src.size(), dst_arena, caller_stream);
+}
+
+plex_status plex_weight_sync_rank_from_slab(plex_ctx_t c, plex_plan_t plan, int32_t rank, plex_slab_t slab,
+                                            void* const* dst_arenas, int32_t n_arenas, void* stream) {
+    if (!c || !plan || !slab || slab->rank != rank) { set_error("bad ctx/plan/slab"); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    std::vector<const void*> src;
+    plex_status st = slab_master_ptrs(plan->p, slab, src);
+    if (st) return st;
+    return plex_weight_sync_rank(c, plan, rank, src.data(), (int32_t)src.size(), dst_arenas, n_arenas, stream);
 }
 
 // ---- infrastructure --------------------------------------------------------------------

@@ -354,6 +354,15 @@ class StateManager:
         check(lib.plex_weight_sync_rank(self.h, plan.h, rank, arr, len(masters), ar, len(arenas),
                                         _stream_ptr(stream)))
 
+    def sync_from_slab(self, plan: Plan, slab: Slab, arena: torch.Tensor, stream=None) -> None:
+        """NEXT-3: sync a suspended job straight from its pinned slab."""
+        check(lib.plex_weight_sync_from_slab(self.h, plan.h, slab.h, arena.data_ptr(), _stream_ptr(stream)))
+
+    def sync_rank_from_slab(self, plan: Plan, rank: int, slab: Slab, arenas: Sequence[torch.Tensor],
+                            stream=None) -> None:
+        ar = ptr_array([a.data_ptr() for a in arenas])
+        check(lib.plex_weight_sync_rank_from_slab(self.h, plan.h, rank, slab.h, ar, len(arenas), _stream_ptr(stream)))
+
     # ---- helpers ---------------------------------------------------------------------
     def arena(self, plan: Plan, rank: Optional[int] = None) -> torch.Tensor:
         n = plan.rank_info(self.rank if rank is None else rank).dst_arena_bytes

@@ -347,3 +347,33 @@ def test_param_elision(model, W, bucket):
         for kk, x in job.shards.items():
             assert np.array_equal(bits_np(x), state[kk]), kk
         m.close()
+
+
+# ---- NEXT-3 sync straight from the offloaded slab ----------------------------------------------------
+@pytest.mark.parametrize("model,W,tp,dp,ep,elide", [("mid", 4, 2, 2, 1, False), ("mid-moe", 4, 2, 2, 4, True),
+                                                     ("toy-odd", 3, 1, 3, 1, False)])
+def test_sync_from_slab(model, W, tp, dp, ep, elide):
+    man = manifest(model)
+    hd = MODELS[model].head_dim
+    plan = P.Plan(man, head_dim=hd, world=W, tp=tp, dp=dp, ep=ep, bucket_bytes=1 << 14, tile_bytes=1024,
+                  elide_param=elide)
+    mgrs = [mgr(W, r, bucket=1 << 14) for r in range(W)]
+    jobs = [P.Job(mgrs[r], plan, seed=50, rank=r).alloc().init_synthetic(special_bits=3, derived_param=elide)
+            for r in range(W)]
+    for j in jobs:
+        j.suspend()                                   # training state leaves the GPU
+    arenas = [torch.full((max(256, plan.rank_info(g).dst_arena_bytes),), 0xEE, dtype=torch.uint8, device="cuda")
+              for g in range(W)]
+    with pytest.raises(P.PlexError):                  # wrong rank's slab
+        mgrs[0].sync_rank_from_slab(plan, 1, jobs[0].slab, arenas)
+    for r in range(W):
+        mgrs[r].sync_rank_from_slab(plan, r, jobs[r].slab, arenas)
+    full = full_state(model, seed=50, kinds=(1,), special_bits=3)
+    want = O.weight_sync(master_shards(full, W, O.fsdp_rows), tp, dp, ep, O.TP_FAST, hd)
+    for g in range(W):
+        for name, v in P.StateManager.rollout_views(plan, g, arenas[g]).items():
+            assert np.array_equal(bits_np(v), want[g][name]), (g, name)
+    jobs[0].resume()
+    with pytest.raises(P.PlexError) as e:             # device-resident again: nothing to read in the slab
+        mgrs[0].sync_rank_from_slab(plan, 0, jobs[0].slab, arenas)
+    assert e.value.code == L.E_STATE
