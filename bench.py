@@ -340,8 +340,10 @@ def run_plex(a):
     e1.record()
     barrier()
     clk = clocks.stop()
-    phases = {n: allmax(sum(ev[i].elapsed_time(ev[i + 1]) for ev in phase_ev) / a.steps)
-              for i, n in enumerate(("switch", "sync"))}
+    local_ph = {n: sum(ev[i].elapsed_time(ev[i + 1]) for ev in phase_ev) / a.steps
+                for i, n in enumerate(("switch", "sync"))}
+    phases = {n: allmax(v) for n, v in local_ph.items()}
+    phases_min = {n: allmin(v) for n, v in local_ph.items()}
     ms_local = e0.elapsed_time(e1) / a.steps
     ms = allmax(ms_local)
     st = mgr.stats()
@@ -391,18 +393,30 @@ def run_plex(a):
                      "frac": frac(gbs, peak_hbm), "launches_per_step": v["launches"] / a.steps,
                      "ms_per_step": round(v["ms"] / a.steps, 3)}
     for k, v, ref in (("d2h", d2h, bw["d2h"]), ("h2d", h2d, bw["h2d"])):
+        gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else 0.0
+        lo, hi = allmin(gbs), allmax(gbs)
+        ref_lo = allmin(ref)
         if v["ms"] > 0:
-            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
             rl["host_" + k] = {"bound": "host_link", "achieved": round(gbs, 2), "peak": round(ref, 2),
                                "unit": "GB/s", "frac": frac(gbs, ref),
-                               "peak_kind": f"measured pinned copy, {world} GPU(s) concurrently"}
+                               "achieved_min_max_over_ranks": [round(lo, 2), round(hi, 2)],
+                               "peak_min_over_ranks": round(ref_lo, 2),
+                               "peak_kind": f"measured pinned copy, {world} GPU(s) concurrently (rank 0)"}
     if world > 1:
-        # NVLink: max over ranks of max(send, recv) bytes over the whole sync call
+        # NVLink: max over ranks of max(send, recv) bytes ÷ the data-moving part
+        # of the sync (the push kernel, or the NCCL exchange rounds), max over ranks
         nv = allmax(float(max(info.send_bytes, info.recv_bytes)))
-        gbs = nv / (phases["sync"] * 1e-3) / 1e9
+        t_x = st["nccl"]["ms"] if st["nccl"]["launches"] else st["push"]["ms"]
+        t_x = allmax(t_x / a.steps)
+        gbs = nv / (t_x * 1e-3) / 1e9
         rl["nvlink"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s",
-                        "frac": frac(gbs, 900.0), "bytes_max_rank": nv, "over": "whole sync call (max over ranks)",
-                        "peak_kind": "nominal 900 GB/s/dir (measured peer copy ref 770)"}
+                        "frac": frac(gbs, 900.0), "frac_of_measured_peer_copy": frac(gbs, 770.0),
+                        "bytes_max_rank": nv, "ms": round(t_x, 3),
+                        "over": "NCCL exchange rounds" if st["nccl"]["launches"] else
+                                "fused cast+push kernel (local casts included)",
+                        "peak_kind": "nominal 900 GB/s/dir; measured peer copy 770 (B200_PROFILING.md)"}
+        if st["barrier"]["launches"]:
+            rl["sync_entry_barrier_ms"] = round(allmax(st["barrier"]["ms"] / a.steps), 3)
         if st["nccl"]["launches"]:
             rl["nccl_exchange"] = {"ms_per_step": round(st["nccl"]["ms"] / a.steps, 3),
                                    "rounds_per_step": st["nccl"]["launches"] / a.steps}
@@ -434,6 +448,7 @@ def run_plex(a):
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "rooflines": rl,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
+            "phases_ms_min_over_ranks": {k: round(v, 3) for k, v in phases_min.items()},
             "clocks": clk,
             "gpu_launches": int(launches),
         }

@@ -211,7 +211,8 @@ typedef struct {
 #define PLEX_STAT_RPACK   6      /* K4 reshard-pack (NCCL path) */
 #define PLEX_STAT_RUNPACK 7      /* K5 reshard-unpack (NCCL path) */
 #define PLEX_STAT_DERIVE  8      /* NEXT-2 param check / re-derivation */
-#define PLEX_NUM_STATS    9
+#define PLEX_STAT_BARRIER 9      /* sync entry barrier (time spent waiting for the slowest rank) */
+#define PLEX_NUM_STATS    10
 
 /* ---- errors / version ---------------------------------------------------- */
 PLEX_API const char* plex_last_error(void);

@@ -23,9 +23,10 @@ OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
 RES_DEVICE, RES_HOST = 0, 1
 CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
 SLAB_HUGEPAGE = 0x1
-STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE = range(9)
-STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive")
-NUM_STATS = 9
+STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE, \
+    STAT_BARRIER = range(10)
+STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive", "barrier")
+NUM_STATS = 10
 PLAN_ELIDE_PARAM = 0x1
 
 EXPORTS = [

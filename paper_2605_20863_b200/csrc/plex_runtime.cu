@@ -121,8 +121,10 @@ struct plex_ctx_s {
     uint8_t* d_scratch = nullptr;
     uint8_t* h_scratch = nullptr;
     size_t scratch_bytes = 0;
-    // peer arenas opened over CUDA IPC: rank -> (handle bytes, mapped base)
-    std::map<int, std::pair<std::vector<uint8_t>, void*>> peers;
+    // peer arenas opened over CUDA IPC: rank -> (peer's buffer id, mapped base)
+    std::map<int, std::pair<uint64_t, void*>> peers;
+    uint64_t my_buffer_id = 0;          // arena last exported (and its cached handle)
+    cudaIpcMemHandle_t my_handle{};
     std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
     cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
 };
@@ -768,10 +770,11 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         }
     }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
-    // Both halves' kernels share the ctx pack stream: they are ~100x faster
-    // than the copies, and serialising them keeps each launch's SMs to itself.
+    // Each half has its own kernel stream: on one shared stream a pack waiting
+    // for its D2H slot would hold back the other direction's unpack (and with
+    // it the H2D ring), lock-stepping the two directions of the host link.
     Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
-            c->ev_copy2.data(), c->pack, c->copy2, c->h_ptrs2, c->d_ptrs2};
+            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
@@ -851,30 +854,42 @@ plex_status plex_weight_sync_rank(plex_ctx_t c, plex_plan_t plan, int32_t rank, 
     return timed_collect(c);
 }
 
-typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+typedef int (*cuPointerGetAttribute_t)(void*, int, unsigned long long);
+static constexpr int kAttrBufferId = 7;      // CU_POINTER_ATTRIBUTE_BUFFER_ID
+static constexpr int kAttrRangeStart = 11;   // CU_POINTER_ATTRIBUTE_RANGE_START_ADDR
 
+// Every rank publishes (CUDA-IPC handle, process-unique buffer id, offset) of
+// its rollout arena; peers open a handle only when that (rank, buffer id) is
+// new, so steady-state syncs reuse their NVLink mappings.
 static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, std::vector<void*>& arenas) {
-    static cuMemGetAddressRange_t getrange = nullptr;
-    if (!getrange) {
+    (void)p;
+    static cuPointerGetAttribute_t getattr = nullptr;
+    if (!getattr) {
         cudaDriverEntryPointQueryResult q;
-        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&getrange), cudaEnableDefault, &q));
-        if (!getrange) { set_error("cuMemGetAddressRange unavailable"); return PLEX_E_CUDA; }
+        CK(cudaGetDriverEntryPoint("cuPointerGetAttribute", reinterpret_cast<void**>(&getattr), cudaEnableDefault, &q));
+        if (!getattr) { set_error("cuPointerGetAttribute unavailable"); return PLEX_E_CUDA; }
     }
-    unsigned long long base = 0;
-    size_t sz = 0;
-    if (getrange(&base, &sz, reinterpret_cast<unsigned long long>(arena)) != 0) {
-        set_error("cuMemGetAddressRange failed for the rollout arena");
+    unsigned long long base = 0, bid = 0;
+    const unsigned long long a = reinterpret_cast<unsigned long long>(arena);
+    if (getattr(&base, kAttrRangeStart, a) != 0 || getattr(&bid, kAttrBufferId, a) != 0) {
+        set_error("cuPointerGetAttribute failed for the rollout arena");
         return PLEX_E_CUDA;
     }
     struct Pub {
         cudaIpcMemHandle_t h;
         uint64_t offset;
-        uint64_t pad[7];
+        uint64_t buffer_id;
+        uint64_t pad[6];
     };
     static_assert(sizeof(Pub) <= 256, "Pub");
     Pub me{};
-    CK(cudaIpcGetMemHandle(&me.h, reinterpret_cast<void*>(base)));
-    me.offset = reinterpret_cast<uint64_t>(arena) - base;
+    if (c->my_buffer_id != bid) {
+        CK(cudaIpcGetMemHandle(&c->my_handle, reinterpret_cast<void*>(base)));
+        c->my_buffer_id = bid;
+    }
+    me.h = c->my_handle;
+    me.offset = a - base;
+    me.buffer_id = bid;
     std::memcpy(c->h_scratch, &me, sizeof(me));
     uint8_t* d_send = c->d_scratch;
     uint8_t* d_all = c->d_scratch + 256;
@@ -887,13 +902,13 @@ static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, st
         if (g == c->rank) { arenas[g] = arena; continue; }
         Pub pub;
         std::memcpy(&pub, c->h_scratch + 256 + 256 * (size_t)g, sizeof(pub));
-        std::vector<uint8_t> hb(reinterpret_cast<uint8_t*>(&pub.h), reinterpret_cast<uint8_t*>(&pub.h) + sizeof(pub.h));
         auto it = c->peers.find(g);
-        if (it == c->peers.end() || it->second.first != hb) {
+        if (it == c->peers.end() || it->second.first != pub.buffer_id) {
             if (it != c->peers.end() && it->second.second) cudaIpcCloseMemHandle(it->second.second);
+            c->peers.erase(g);
             void* mapped = nullptr;
             CK(cudaIpcOpenMemHandle(&mapped, pub.h, cudaIpcMemLazyEnablePeerAccess));
-            c->peers[g] = {hb, mapped};
+            c->peers[g] = {pub.buffer_id, mapped};
         }
         arenas[g] = reinterpret_cast<uint8_t*>(c->peers[g].second) + pub.offset;
     }
@@ -918,7 +933,12 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     int* d_bar = reinterpret_cast<int*>(c->d_scratch + 256 + 256 * (size_t)c->world);
-    if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all arenas free
+    if (c->world > 1) {                                   // all arenas free (waits for the slowest rank)
+        cudaEvent_t tb = nullptr;
+        if ((st = timed_begin(c, c->pack, &tb))) return st;
+        NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));
+        if ((st = timed_end(c, c->pack, tb, PLEX_STAT_BARRIER, 0))) return st;
+    }
     if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push))) return st;
     if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all pushes landed
     return finish(c, caller);

@@ -27,6 +27,8 @@ def bits_np(t):
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(900, exit=True)     # never hang a GPU box silently
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)

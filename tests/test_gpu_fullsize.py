@@ -84,7 +84,12 @@ def _fullsize(model: str, seed: int, sample_keys):
         want = O.rollout_tensors(cast, 1, 1, 1, 0)
         for name, x in want.items():
             assert np.array_equal(bits_np(views[name]), x), name
+    # give the device memory and the pinned slab back before the next test
+    del views, arena, job, plan
     mgr.close()
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
 
 
 def test_fullsize_qwen05_one_gpu():

@@ -40,6 +40,6 @@ def test_fullsize_7b_multi_gpu(n):
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mp_fullsize_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
