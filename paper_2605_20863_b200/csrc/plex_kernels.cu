@@ -14,7 +14,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 
 #include "plex_internal.h"
 
@@ -174,6 +173,16 @@ __device__ __forceinline__ uint32_t chunk_bulk(const ItemGeo& g, uint32_t co, ui
     return e & ~15u;
 }
 
+// One staged chunk: which item/offset it belongs to (written by the producer
+// before it arrives on the stage's full barrier, read by the consumers after
+// their wait: mbarrier arrive/wait order it).
+struct StageMeta {
+    ItemGeo g;
+    uint32_t co;        // chunk offset within the item
+    uint32_t flags;     // kMetaLast: last chunk of its item; kMetaDone: no more work
+};
+constexpr uint32_t kMetaLast = 1u, kMetaDone = 2u;
+
 template <int STAGES, int CHUNK_KB, int CWARPS, int CTAS>
 struct TmaCfg {
     static constexpr int kStages = STAGES;
@@ -181,33 +190,31 @@ struct TmaCfg {
     static constexpr int kConsumers = CWARPS * 32;
     static constexpr int kThreads = kConsumers + 32;
     static constexpr int kCtasPerSm = CTAS;
-    static constexpr int kBatch = 128;                      // item descriptors staged per batch
-    static constexpr size_t kBarOff = (size_t)STAGES * kChunk;
-    static constexpr size_t kGeoOff = kBarOff + 2 * STAGES * sizeof(uint64_t);
-    static constexpr size_t kSmem = kGeoOff + kBatch * sizeof(ItemGeo);
+    static constexpr size_t kMetaOff = (size_t)STAGES * kChunk;
+    static constexpr size_t kBarOff = kMetaOff + STAGES * sizeof(StageMeta);
+    static constexpr size_t kSmem = kBarOff + 2 * STAGES * sizeof(uint64_t);
 };
+using PackCfg = TmaCfg<3, 32, 4, 2>;     // 2 CTAs/SM x 3 stages x 32 KiB (see profiles/ kbench runs)
 
-// The CTA's work items (i = blockIdx.x + k * gridDim.x) are resolved in batches
-// of kBatch: every thread of the CTA fetches one item's PackItem -> SegDev ->
-// shard pointer chain in parallel and the resulting geometry is staged in
-// shared memory, so neither the TMA producer nor the consumers ever stall on
-// that dependent-load chain inside the streaming loop.
-template <bool kPack, class Cfg, bool kCks = true>
+// Work distribution is dynamic: each CTA's producer claims the next PackItem
+// from a per-launch counter (one claim ahead, so the claim + descriptor-fetch
+// latency hides behind the chunks already in flight) and tags every staged
+// chunk with its item geometry.  CTAs that run faster simply take more items,
+// which removes the static round-robin tail.
+template <bool kPack, class Cfg>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
                 const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
-                unsigned long long* __restrict__ cks) {
+                unsigned long long* __restrict__ cks, unsigned int* __restrict__ ctr) {
     constexpr int kStages = Cfg::kStages;
     constexpr uint32_t kChunk = Cfg::kChunk;
     constexpr int kConsumers = Cfg::kConsumers;
-    constexpr int kBatch = Cfg::kBatch;
     extern __shared__ __align__(128) uint8_t smem[];
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + Cfg::kMetaOff);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
     uint64_t* empty = full + kStages;
-    ItemGeo* geo = reinterpret_cast<ItemGeo*>(smem + Cfg::kGeoOff);
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const bool producer = tid >= kConsumers;
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], 1);
@@ -216,84 +223,91 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const uint32_t mine = n_items > blockIdx.x ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    uint32_t q = 0;                                       // chunk sequence number (ring position)
-    for (uint32_t b0 = 0; b0 < mine; b0 += kBatch) {
-        const uint32_t nb_items = mine - b0 < (uint32_t)kBatch ? mine - b0 : (uint32_t)kBatch;
-        __syncthreads();                                  // previous batch fully consumed
-        for (uint32_t k = tid; k < nb_items; k += Cfg::kThreads)
-            geo[k] = item_geo(items[blockIdx.x + (b0 + k) * gridDim.x], segs, ptrs, staging, bucket_lo);
-        __syncthreads();
-        if (producer) {
-            // ---------------- producer warp: TMA loads ----------------
-            if (tid == kConsumers) {
-                for (uint32_t k = 0; k < nb_items; ++k) {
-                    const ItemGeo g = geo[k];
-                    const uint8_t* src = kPack ? g.tens : g.buf;
-                    for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
-                        const int st = (int)(q % kStages);
-                        if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
-                        const uint32_t nb = chunk_bulk(g, co, kChunk);
-                        if (nb) {
-                            mbar_arrive_tx(&full[st], nb);
-                            bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
-                        } else {
-                            mbar_arrive(&full[st]);
-                        }
-                    }
-                }
-            }
-            continue;
-        }
-        // ---------------- consumer warps: checksum + TMA stores ----------------
-        for (uint32_t k = 0; k < nb_items; ++k) {
-            const ItemGeo g = geo[k];
+    __syncthreads();
+
+    if (tid >= kConsumers) {
+        // ---------------- producer: claim items, TMA-load their chunks ----------------
+        if (tid != kConsumers) return;
+        uint32_t q = 0;
+        uint32_t i = atomicAdd(ctr, 1u);
+        ItemGeo g;
+        if (i < n_items) g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+        while (i < n_items) {
+            const uint32_t inext = atomicAdd(ctr, 1u);          // claim ahead
             const uint8_t* src = kPack ? g.tens : g.buf;
-            uint8_t* dst = kPack ? g.buf : g.tens;
-            Cks c;
             for (uint32_t co = 0; co < g.len; co += kChunk, ++q) {
                 const int st = (int)(q % kStages);
-                const uint8_t* sm = smem + (size_t)st * kChunk;
+                if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+                meta[st].g = g;
+                meta[st].co = co;
+                meta[st].flags = (g.len - co <= kChunk) ? kMetaLast : 0u;
                 const uint32_t nb = chunk_bulk(g, co, kChunk);
-                const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
-                const uint32_t dend = g.data < cend ? g.data : cend;    // data end within chunk
-                mbar_wait(&full[st], (q / kStages) & 1);
-                if (tid == 0 && nb) {
-                    bulk_store(dst + co, sm, nb);                       // write back while we checksum
-                    bulk_commit();
-                }
-                // checksum of the bulk part, read back from shared memory
-                if (kCks)
-                    for (uint32_t v = tid; v < nb / 16; v += kConsumers)
-                        c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
-                // non-bulk data (misaligned tensor or <16-B tail): element by element
-                const uint32_t t0 = co + nb;
-                if (t0 < dend) {
-                    const uint32_t ne = (dend - t0) / g.es;
-                    for (uint32_t e = tid; e < ne; e += kConsumers) {
-                        const uint32_t off = t0 + e * g.es;
-                        uint32_t b;
-                        if (g.es == 4) {
-                            b = *reinterpret_cast<const uint32_t*>(src + off);
-                            *reinterpret_cast<uint32_t*>(dst + off) = b;
-                        } else {
-                            b = *reinterpret_cast<const uint16_t*>(src + off);
-                            *reinterpret_cast<uint16_t*>(dst + off) = (uint16_t)b;
-                        }
-                        c.add_elem(b, g.ib + off / g.es);
-                    }
-                }
-                if (kPack && dend < cend) {
-                    const uint32_t p0 = co > g.data ? co : g.data;
-                    for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);                 // this warp is done with stage st
-                if (tid == 0) {
-                    if (nb) bulk_wait_read_all();                       // the bulk store has read stage st
-                    mbar_arrive(&empty[st]);
+                if (nb) {
+                    mbar_arrive_tx(&full[st], nb);
+                    bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
+                } else {
+                    mbar_arrive(&full[st]);
                 }
             }
+            i = inext;
+            if (i < n_items) g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
+        }
+        const int st = (int)(q % kStages);
+        if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+        meta[st].flags = kMetaDone;
+        mbar_arrive(&full[st]);
+        return;
+    }
+    // ---------------- consumers: checksum + TMA stores ----------------
+    Cks c;
+    for (uint32_t q = 0;; ++q) {
+        const int st = (int)(q % kStages);
+        mbar_wait(&full[st], (q / kStages) & 1);
+        const uint32_t flags = meta[st].flags;
+        if (flags & kMetaDone) break;
+        const ItemGeo g = meta[st].g;
+        const uint32_t co = meta[st].co;
+        const uint8_t* src = kPack ? g.tens : g.buf;
+        uint8_t* dst = kPack ? g.buf : g.tens;
+        const uint8_t* sm = smem + (size_t)st * kChunk;
+        const uint32_t nb = chunk_bulk(g, co, kChunk);
+        const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
+        const uint32_t dend = g.data < cend ? g.data : cend;            // data end within chunk
+        if (tid == 0 && nb) {
+            bulk_store(dst + co, sm, nb);                               // write back while we checksum
+            bulk_commit();
+        }
+        // checksum of the bulk part, read back from shared memory
+        for (uint32_t v = tid; v < nb / 16; v += kConsumers)
+            c.add_vec(lds128(sm + 16 * v), g.es, g.ib + (co + 16 * v) / g.es);
+        // non-bulk data (misaligned tensor or <16-B tail): element by element
+        const uint32_t t0 = co + nb;
+        if (t0 < dend) {
+            const uint32_t ne = (dend - t0) / g.es;
+            for (uint32_t e = tid; e < ne; e += kConsumers) {
+                const uint32_t off = t0 + e * g.es;
+                uint32_t b;
+                if (g.es == 4) {
+                    b = *reinterpret_cast<const uint32_t*>(src + off);
+                    *reinterpret_cast<uint32_t*>(dst + off) = b;
+                } else {
+                    b = *reinterpret_cast<const uint16_t*>(src + off);
+                    *reinterpret_cast<uint16_t*>(dst + off) = (uint16_t)b;
+                }
+                c.add_elem(b, g.ib + off / g.es);
+            }
+        }
+        if (kPack && dend < cend) {
+            const uint32_t p0 = co > g.data ? co : g.data;
+            for (uint32_t b = p0 + tid; b < cend; b += kConsumers) dst[b] = 0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);                         // this warp is done with stage st
+        if (tid == 0) {
+            if (nb) bulk_wait_read_all();                               // the bulk store has read stage st
+            mbar_arrive(&empty[st]);
+        }
+        if (flags & kMetaLast) {                                        // item complete: fold its checksum
             if (g.data) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -305,68 +319,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
                     atomicAdd(cks + 2 * g.seg + 1, c.s2);
                 }
             }
+            c = Cks();
         }
     }
     if (tid == 0) bulk_wait_all();                 // every bulk store complete before exit
-}
-
-// LDG/STG variant (experiment): persistent CTAs, 8 independent 16-B loads in
-// flight per thread, checksum in registers, warp-level atomics per item.
-template <bool kPack>
-__global__ void __launch_bounds__(256, 4)
-    pack_ldg_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
-                    const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
-                    unsigned long long* __restrict__ cks) {
-    constexpr int U = 8;
-    const int tid = threadIdx.x, lane = tid & 31;
-    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
-        const ItemGeo g = item_geo(items[i], segs, ptrs, staging, bucket_lo);
-        const uint8_t* src = kPack ? g.tens : g.buf;
-        uint8_t* dst = kPack ? g.buf : g.tens;
-        Cks c;
-        const uint32_t nv = g.vec ? g.data / 16 : 0;
-        const uint32_t epv = 16 / g.es;
-        uint32_t v = tid;
-        for (; v + (U - 1) * 256 < nv; v += U * 256) {
-            uint4 x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) x[u] = ld_stream(src + 16ull * (v + u * 256));
-#pragma unroll
-            for (int u = 0; u < U; ++u) st_v4(dst + 16ull * (v + u * 256), x[u]);
-#pragma unroll
-            for (int u = 0; u < U; ++u) c.add_vec(x[u], g.es, g.ib + (uint64_t)(v + u * 256) * epv);
-        }
-        for (; v < nv; v += 256) {
-            const uint4 x = ld_stream(src + 16ull * v);
-            st_v4(dst + 16ull * v, x);
-            c.add_vec(x, g.es, g.ib + (uint64_t)v * epv);
-        }
-        const uint32_t ne = g.data / g.es;
-        for (uint32_t e = nv * epv + tid; e < ne; e += 256) {
-            uint32_t b;
-            if (g.es == 4) {
-                b = reinterpret_cast<const uint32_t*>(src)[e];
-                reinterpret_cast<uint32_t*>(dst)[e] = b;
-            } else {
-                b = reinterpret_cast<const uint16_t*>(src)[e];
-                reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)b;
-            }
-            c.add_elem(b, g.ib + e);
-        }
-        if (kPack)
-            for (uint32_t b = g.data + tid; b < g.len; b += 256) dst[b] = 0;
-        if (g.data) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
-                c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
-            }
-            if (lane == 0) {
-                atomicAdd(cks + 2 * g.seg, c.s1);
-                atomicAdd(cks + 2 * g.seg + 1, c.s2);
-            }
-        }
-    }
 }
 
 __global__ void verify_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
@@ -575,50 +531,30 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 
 // ---- launchers ----------------------------------------------------------------
 static int g_num_sms = 0;
-static int g_variant = -1;
-
-template <bool kPack, class Cfg, bool kCks = true>
-static cudaError_t launch_tma(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
-                              uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, Cfg, kCks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Cfg::kSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    const uint32_t cap = (uint32_t)g_num_sms * Cfg::kCtasPerSm;
-    const uint32_t grid = n_items < cap ? n_items : cap;
-    pack_kernel<kPack, Cfg, kCks><<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(items, n_items, segs, ptrs, staging, bucket_lo,
-                                                                        cks);
-    return cudaGetLastError();
-}
 
 template <bool kPack>
 static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
-                                 uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
-    switch (g_variant) {
-        case 1: return launch_tma<kPack, TmaCfg<12, 16, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 2: return launch_tma<kPack, TmaCfg<6, 16, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 3: return launch_tma<kPack, TmaCfg<4, 48, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 4: {
-            const uint32_t cap = (uint32_t)g_num_sms * 4;
-            pack_ldg_kernel<kPack><<<n_items < cap ? n_items : cap, 256, 0, s>>>(items, n_items, segs, ptrs, staging,
-                                                                              bucket_lo, cks);
-            return cudaGetLastError();
-        }
-        case 5: return launch_tma<kPack, TmaCfg<6, 32, 8, 1>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 6: return launch_tma<kPack, TmaCfg<4, 24, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 7:   // probe: the default pipeline without the checksum (not a valid pack)
-            return launch_tma<kPack, TmaCfg<3, 32, 4, 2>, false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 8: return launch_tma<kPack, TmaCfg<4, 16, 4, 3>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        case 9: return launch_tma<kPack, TmaCfg<2, 48, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
-        default: return launch_tma<kPack, TmaCfg<3, 32, 4, 2>>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+                                 uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
+                                 cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, PackCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)PackCfg::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
     }
+    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    const uint32_t cap = (uint32_t)g_num_sms * PackCfg::kCtasPerSm;
+    const uint32_t grid = n_items < cap ? n_items : cap;
+    pack_kernel<kPack, PackCfg><<<grid, PackCfg::kThreads, PackCfg::kSmem, s>>>(items, n_items, segs, ptrs, staging,
+                                                                                bucket_lo, cks, ctr);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
-                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s) {
+                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
+                        cudaStream_t s) {
     if (n_items == 0) return cudaSuccess;
     if (!g_num_sms) {
         int dev = 0;
@@ -626,12 +562,8 @@ cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, cons
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
     }
-    if (g_variant < 0) {
-        const char* v = getenv("PLEX_PACK_VARIANT");
-        g_variant = v ? atoi(v) : 0;
-    }
-    return pack ? launch_pack_t<true>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s)
-                : launch_pack_t<false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, s);
+    return pack ? launch_pack_t<true>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s)
+                : launch_pack_t<false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s);
 }
 
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,

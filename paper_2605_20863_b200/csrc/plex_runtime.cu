@@ -23,7 +23,8 @@
 namespace plex {
 
 cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
-                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, cudaStream_t s);
+                        uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
+                        cudaStream_t s);
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
                           cudaStream_t s);
 cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
@@ -117,6 +118,7 @@ struct plex_ctx_s {
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
+    unsigned int* d_ctr = nullptr;      // pack/unpack work counters, one per pipe
     // small device scratch for NCCL barriers and handle exchange
     uint8_t* d_scratch = nullptr;
     uint8_t* h_scratch = nullptr;
@@ -316,6 +318,7 @@ struct Pipe {
     cudaStream_t copy;
     uint64_t* h_ptrs;
     uint64_t* d_ptrs;
+    unsigned int* ctr;      // per-launch work counter of the pack/unpack kernel
 };
 
 struct Half {           // one offload or onload in flight
@@ -369,7 +372,7 @@ static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     cudaEvent_t ta = nullptr;
     plex_status st;
     if ((st = timed_begin(c, pp.kern, &ta))) return st;
-    CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.kern));
+    CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.ctr, pp.kern));
     if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_PACK, 2 * h.d->bucket_payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
@@ -415,7 +418,7 @@ static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
     const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
     if ((st = timed_begin(c, pp.kern, &ta))) return st;
-    CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.kern));
+    CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.ctr, pp.kern));
     if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.d->bucket_payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     return PLEX_OK;
@@ -503,6 +506,7 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
         }
     c->scratch_bytes = 256 * (size_t)world + 256;
     if (cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&c->d_flag, 64) != cudaSuccess ||
+        cudaMalloc(&c->d_ctr, 64) != cudaSuccess ||
         cudaMalloc(&c->d_scratch, 2 * c->scratch_bytes) != cudaSuccess ||
         cudaHostAlloc(&c->h_scratch, 2 * c->scratch_bytes, cudaHostAllocDefault) != cudaSuccess) {
         set_error("ctx scratch allocation failed");
@@ -558,6 +562,7 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     if (c->copy2) cudaStreamDestroy(c->copy2);
     cudaFreeHost(c->h_flag);
     cudaFree(c->d_flag);
+    cudaFree(c->d_ctr);
     cudaFree(c->d_scratch);
     cudaFreeHost(c->h_scratch);
     delete c;
@@ -679,7 +684,8 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     DeviceGuard g(c->device);
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}};
     if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
-    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
+    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
+            c->d_ctr};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
@@ -709,7 +715,8 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     if ((st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst)) ||
         (st = get_devplan(c, plan->p, &h.d)))
         return st;
-    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
+    Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
+            c->d_ctr};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
@@ -769,12 +776,13 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
             CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
         }
     }
-    Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs};
+    Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
+            c->d_ctr};
     // Each half has its own kernel stream: on one shared stream a pack waiting
     // for its D2H slot would hold back the other direction's unpack (and with
     // it the H2D ring), lock-stepping the two directions of the host link.
     Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
-            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2};
+            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));

@@ -89,7 +89,7 @@ class Plan:
     def __init__(self, manifest, head_dim: int = 1, world: int = 1, tp: int = 0, dp: int = 0, ep: int = 1,
                  rank_map: int = L.RANKMAP_TP_FAST, slab_layout: int = L.SLAB_KIND_MAJOR,
                  kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
-                 bucket_bytes: int = 1 << 30, tile_bytes: int = 64 << 10,
+                 bucket_bytes: int = 2 << 30, tile_bytes: int = 64 << 10,
                  resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE, elide_param: bool = False):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
@@ -268,7 +268,7 @@ def _stream_ptr(s) -> int:
 class StateManager:
     """One per rank process: the ctx (streams, staging, NCCL communicator)."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 1 << 30,
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 2 << 30,
                  n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
                  nccl_id: Optional[bytes] = None, duplex: bool = True):
         if not torch.cuda.is_available():

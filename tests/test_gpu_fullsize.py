@@ -1,5 +1,5 @@
 """Full-size parity at BASELINE.json's configs, in the launch configuration
-bench.py times (1 GiB buckets, 64 KiB work items, one rank per GPU).
+bench.py times (2 GiB buckets, 64 KiB work items, one rank per GPU).
 
 The oracle cannot materialise 100 GB of state, so the check is split:
 * sampled outputs the oracle computes one by one: the slab bytes and R14
@@ -32,7 +32,7 @@ def _fullsize(model: str, seed: int, sample_keys):
     torch.cuda.set_device(0)
     man = manifest(model)
     shape = MODELS[model]
-    mgr = P.StateManager(device=0, bucket_bytes=1 << 30, n_slots=2, bootstrap=False)
+    mgr = P.StateManager(device=0, bucket_bytes=2 << 30, n_slots=2, bootstrap=False)
     plan = mgr.plan(man, head_dim=shape.head_dim, tp=1, dp=1)
     job = P.Job(mgr, plan, seed=seed).alloc().init_synthetic()
     torch.cuda.synchronize()

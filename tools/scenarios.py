@@ -270,7 +270,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--model", default="")
     ap.add_argument("--tp", type=int, default=0)
-    ap.add_argument("--bucket-mb", type=int, default=1024)
+    ap.add_argument("--bucket-mb", type=int, default=2048)
     ap.add_argument("--units", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--duplex", action="store_true")
