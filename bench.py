@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--tp", type=int, default=0, help="rollout TP (default min(2, N))")
     ap.add_argument("--ep", type=int, default=1)
     ap.add_argument("--bucket-mb", type=int, default=2048)
-    ap.add_argument("--slots", type=int, default=3)
+    ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--no-hugepage", dest="hugepage", action="store_false",
                     help="pin slabs with cudaHostAlloc instead of mmap(MADV_HUGEPAGE) + cudaHostRegister")
     ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")

@@ -146,10 +146,10 @@ typedef struct {
 /* Plan flags. */
 /* NEXT-2 derived-state elision (canonical non-redundant
  * offloaded state): with KIND_MAJOR slabs carrying PARAM and MASTER, offload
- * first checks on the device that every bf16 param of the leading buckets
- * equals RNE(master) (R8) -- true after every mixed-precision optimizer step
- * -- and if so neither packs nor copies those buckets; onload re-derives them
- * from the restored master.  Checksums cover the derived params, so a failed
+ * first checks on the device that every bf16 param equals RNE(master) (R8) -- true after every mixed-precision optimizer step
+ * -- and if so neither packs nor copies the PARAM prefix (the remaining
+ * slab moves on a bucket grid starting at the first MASTER byte); onload
+ * re-derives the params from the restored master.  Checksums cover the derived params, so a failed
  * derivation is still caught (E_CHECKSUM).  Falls back to a full offload when
  * any element differs. */
 #define PLEX_PLAN_ELIDE_PARAM 0x1u
@@ -176,8 +176,8 @@ typedef struct {
     uint64_t recv_bytes;         /* bf16 bytes peers push to this rank      */
     uint64_t local_bytes;        /* bf16 bytes cast locally (no transfer)   */
     uint64_t src_read_bytes;     /* fp32 bytes read by this rank's push     */
-    int32_t elide_buckets;       /* leading buckets elidable (PLEX_PLAN_ELIDE_PARAM) */
-    uint64_t elide_bytes;        /* slab bytes those buckets span           */
+    int32_t elide_buckets;       /* PLEX_PLAN_ELIDE_PARAM: buckets still moved when eliding */
+    uint64_t elide_bytes;        /* ... and the PARAM prefix derived instead (0 = none) */
 } plex_rank_info;
 
 typedef struct {

@@ -82,7 +82,12 @@ struct RankPlan {
     std::vector<PackItem> items;
     std::vector<uint64_t> bucket_item_start;    // n_buckets + 1
     uint64_t slab_bytes = 0, payload_bytes = 0;
-    int32_t elide_buckets = 0;                  // NEXT-2: leading buckets inside the PARAM region
+    // NEXT-2 derived-param elision: the PARAM prefix [0, elide_start) is derived
+    // on the device; the rest moves on its own bucket grid starting there.
+    uint64_t elide_start = 0;                   // 0 = no elision possible
+    uint64_t n_param_items = 0;                 // items[0, n) cover [0, elide_start)
+    std::vector<PackItem> items_el;             // items of [elide_start, slab_bytes)
+    std::vector<uint64_t> bstart_el;            // n_buckets_el + 1
     // rollout
     std::vector<DstTensor> dst;
     uint64_t arena_bytes = 0;

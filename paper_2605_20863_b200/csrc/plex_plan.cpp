@@ -97,14 +97,35 @@ static plex_status build_slab(Plan& p, int32_t r) {
         R.bucket_item_start[b] = it;
     }
     R.bucket_item_start[nb] = R.items.size();
-    // NEXT-2: buckets lying entirely inside the leading PARAM region of a
-    // KIND_MAJOR slab that also carries MASTER can be derived instead of moved.
+    // NEXT-2: with a KIND_MAJOR slab that also carries MASTER, the leading PARAM
+    // region can be derived instead of moved; the remainder gets its own bucket
+    // grid starting at the first MASTER byte.
     if ((p.flags & PLEX_PLAN_ELIDE_PARAM) && p.layout == PLEX_SLAB_KIND_MAJOR &&
         (p.kind_mask & (1u << PLEX_KIND_PARAM)) && (p.kind_mask & (1u << PLEX_KIND_MASTER))) {
-        uint64_t param_end = R.slab_bytes;
-        for (const plex_seg_desc& d : R.seg_desc)
-            if (d.kind != PLEX_KIND_PARAM) { param_end = d.slab_offset; break; }
-        R.elide_buckets = (int32_t)(param_end / B);
+        uint32_t first = 0;
+        while (first < R.seg_desc.size() && R.seg_desc[first].kind == PLEX_KIND_PARAM) ++first;
+        if (first > 0 && first < R.seg_desc.size()) {
+            const uint64_t e0 = R.segs[first].slab_off;
+            R.elide_start = e0;
+            while (R.n_param_items < R.items.size() && R.items[R.n_param_items].slab_lo < e0) ++R.n_param_items;
+            for (uint32_t si = first; si < R.segs.size(); ++si) {
+                const SegDev& sg = R.segs[si];
+                uint64_t lo = sg.slab_off, hi = sg.slab_off + align_up(sg.bytes, kSegAlign);
+                while (lo < hi) {
+                    const uint64_t nb_edge = e0 + ((lo - e0) / B + 1) * B;
+                    uint64_t cut = std::min(hi, std::min(nb_edge, lo + TL));
+                    R.items_el.push_back(PackItem{lo, (uint32_t)(cut - lo), si});
+                    lo = cut;
+                }
+            }
+            const int32_t nbe = (int32_t)((R.slab_bytes - e0 + B - 1) / B);
+            R.bstart_el.assign(nbe + 1, R.items_el.size());
+            size_t k = 0;
+            for (int32_t b = 0; b < nbe; ++b) {
+                while (k < R.items_el.size() && R.items_el[k].slab_lo < e0 + (uint64_t)b * B) ++k;
+                R.bstart_el[b] = k;
+            }
+        }
     }
     return PLEX_OK;
 }
@@ -384,8 +405,8 @@ plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* 
     o.recv_bytes = R.recv_bytes;
     o.local_bytes = R.local_bytes;
     o.src_read_bytes = R.src_read_bytes;
-    o.elide_buckets = R.elide_buckets;
-    o.elide_bytes = std::min<uint64_t>(R.slab_bytes, (uint64_t)R.elide_buckets * p.bucket);
+    o.elide_buckets = R.elide_start ? (int32_t)R.bstart_el.size() - 1 : 0;
+    o.elide_bytes = R.elide_start;
     *out = o;
     return PLEX_OK;
 }

@@ -67,7 +67,9 @@ struct DevPlan {
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
     unsigned long long* cks_in = nullptr;     // recomputed at onload
     std::vector<uint64_t> bucket_payload;     // data bytes per bucket (stats)
-    uint64_t elide_payload = 0;               // PARAM data bytes in the elidable buckets
+    uint64_t elide_payload = 0;               // PARAM data bytes (derived when eliding)
+    PackItem* items_el = nullptr;             // NEXT-2 shifted grid
+    std::vector<uint64_t> bucket_payload_el;
     // NCCL-baseline schedule (built lazily for one per-pair round quota Q)
     uint64_t nq = 0;                          // Q it was built for (0 = none)
     int rounds = 0;
@@ -156,6 +158,7 @@ static void free_devplan(DevPlan& d) {
     cudaFree(d.cks);
     cudaFree(d.cks_want);
     cudaFree(d.cks_in);
+    cudaFree(d.items_el);
     cudaFree(d.local);
     cudaFree(d.rpack);
     cudaFree(d.runpack);
@@ -177,7 +180,8 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     const RankPlan& R = p.ranks[c->rank];
     DevPlan d;
     plex_status s;
-    if ((s = upload(&d.segs, R.segs)) || (s = upload(&d.items, R.items)) || (s = upload(&d.push, R.push))) {
+    if ((s = upload(&d.segs, R.segs)) || (s = upload(&d.items, R.items)) || (s = upload(&d.push, R.push)) ||
+        (s = upload(&d.items_el, R.items_el))) {
         free_devplan(d);
         return s;
     }
@@ -196,7 +200,23 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
         const uint64_t de = std::min(o1, sg.bytes);
         if (de > o0) d.bucket_payload[it.slab_lo / p.bucket] += de - o0;
     }
-    for (int32_t b = 0; b < R.elide_buckets; ++b) d.elide_payload += d.bucket_payload[b];
+    if (R.elide_start) {
+        const int32_t nbe = (int32_t)R.bstart_el.size() - 1;
+        d.bucket_payload_el.assign(nbe, 0);
+        for (const PackItem& it : R.items_el) {
+            const SegDev& sg = R.segs[it.seg];
+            const uint64_t o0 = it.slab_lo - sg.slab_off, o1 = o0 + it.len;
+            const uint64_t de = std::min(o1, sg.bytes);
+            if (de > o0) d.bucket_payload_el[(it.slab_lo - R.elide_start) / p.bucket] += de - o0;
+        }
+        for (uint64_t k = 0; k < R.n_param_items; ++k) {
+            const PackItem& it = R.items[k];
+            const SegDev& sg = R.segs[it.seg];
+            const uint64_t o0 = it.slab_lo - sg.slab_off, o1 = o0 + it.len;
+            const uint64_t de = std::min(o1, sg.bytes);
+            if (de > o0) d.elide_payload += de - o0;
+        }
+    }
     *out = &(c->dev[p.id] = d);
     return PLEX_OK;
 }
@@ -328,34 +348,52 @@ struct Half {           // one offload or onload in flight
     plex_slab_s* slab;
     int32_t nb;
     std::vector<uint64_t> cks;     // offload: recorded checksums (host)
-    int32_t b0 = 0;                // first bucket moved (NEXT-2: earlier ones derived)
+    bool elide = false;            // NEXT-2: PARAM prefix derived, not moved
+    // bucket grid in use: buckets b cover [base + b*B, ...) with items
+    // grid_items[bstart[b] .. bstart[b+1])
+    uint64_t base = 0;
+    const PackItem* grid_items = nullptr;
+    const uint64_t* bstart = nullptr;
+    const uint64_t* payload = nullptr;
 };
+
+static void use_grid(Half& h, bool elide) {
+    h.elide = elide;
+    if (elide) {
+        h.base = h.R->elide_start;
+        h.grid_items = h.d->items_el;
+        h.bstart = h.R->bstart_el.data();
+        h.payload = h.d->bucket_payload_el.data();
+        h.nb = (int32_t)h.R->bstart_el.size() - 1;
+    } else {
+        h.base = 0;
+        h.grid_items = h.d->items;
+        h.bstart = h.R->bucket_item_start.data();
+        h.payload = h.d->bucket_payload.data();
+        h.nb = n_buckets(*h.p, *h.R);
+    }
+}
 
 static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     const size_t np = PLEX_NUM_KINDS * h.p->tensors.size();
     const size_t ckb = 16 * std::max<size_t>(1, h.R->segs.size());
     CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
     CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));
-    h.nb = n_buckets(*h.p, *h.R);
     h.cks.assign(2 * h.R->segs.size(), 0);
-    h.b0 = 0;
-    if (h.R->elide_buckets > 0) {
-        // NEXT-2: do the leading PARAM buckets hold exactly RNE(master)?
-        const uint32_t ni = (uint32_t)h.R->bucket_item_start[h.R->elide_buckets];
+    use_grid(h, false);
+    if (h.R->elide_start) {
+        // NEXT-2: does every bf16 param equal RNE(master)?  (checksums the params)
         CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
         cudaEvent_t ta = nullptr;
         plex_status st;
         if ((st = timed_begin(c, pp.kern, &ta))) return st;
-        CK(launch_derive(true, h.d->items, ni, h.d->segs, pp.d_ptrs, (uint32_t)h.p->tensors.size(), h.d->cks,
-                         c->d_flag, pp.kern));
+        CK(launch_derive(true, h.d->items, (uint32_t)h.R->n_param_items, h.d->segs, pp.d_ptrs,
+                         (uint32_t)h.p->tensors.size(), h.d->cks, c->d_flag, pp.kern));
         if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
         CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
         CK(cudaStreamSynchronize(pp.kern));
-        if (*c->h_flag == 0) {
-            h.b0 = h.R->elide_buckets;
-        } else {
-            CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));    // full offload after all
-        }
+        if (*c->h_flag == 0) use_grid(h, true);
+        else CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));    // full offload after all
     }
     return PLEX_OK;
 }
@@ -365,15 +403,16 @@ static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     const RankPlan& R = *h.R;
     const int slot = b % pp.n_slots;
     uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
-    const uint64_t lo = (uint64_t)b * p.bucket;
+    const uint64_t lo = h.base + (uint64_t)b * p.bucket;
     const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
     if (b >= pp.n_slots) CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
-    const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+    const uint64_t i0 = h.bstart[b], i1 = h.bstart[b + 1];
     cudaEvent_t ta = nullptr;
     plex_status st;
     if ((st = timed_begin(c, pp.kern, &ta))) return st;
-    CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.ctr, pp.kern));
-    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_PACK, 2 * h.d->bucket_payload[b]))) return st;
+    CK(launch_pack(true, h.grid_items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.ctr,
+                   pp.kern));
+    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_PACK, 2 * h.payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
     if ((st = timed_begin(c, pp.copy, &ta))) return st;
@@ -396,8 +435,7 @@ static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     CK(cudaMemsetAsync(h.d->cks_in, 0, 8 * std::max<size_t>(2, nck), pp.kern));
     if (nck) CK(cudaMemcpyAsync(h.d->cks_want, h.slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, pp.kern));
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
-    h.nb = n_buckets(*h.p, *h.R);
-    h.b0 = h.slab->elided ? h.R->elide_buckets : 0;
+    use_grid(h, h.slab->elided);
     return PLEX_OK;
 }
 
@@ -406,7 +444,7 @@ static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     const RankPlan& R = *h.R;
     const int slot = b % pp.n_slots;
     uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
-    const uint64_t lo = (uint64_t)b * p.bucket;
+    const uint64_t lo = h.base + (uint64_t)b * p.bucket;
     const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
     if (b >= pp.n_slots) CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
     cudaEvent_t ta = nullptr;
@@ -416,22 +454,22 @@ static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     if ((st = timed_end(c, pp.copy, ta, PLEX_STAT_H2D, len))) return st;
     CK(cudaEventRecord(pp.ev_c[slot], pp.copy));
     CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
-    const uint64_t i0 = R.bucket_item_start[b], i1 = R.bucket_item_start[b + 1];
+    const uint64_t i0 = h.bstart[b], i1 = h.bstart[b + 1];
     if ((st = timed_begin(c, pp.kern, &ta))) return st;
-    CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.ctr, pp.kern));
-    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.d->bucket_payload[b]))) return st;
+    CK(launch_pack(false, h.grid_items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.ctr,
+                   pp.kern));
+    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     return PLEX_OK;
 }
 
 static plex_status on_end(plex_ctx_s* c, Pipe& pp, Half& h) {
-    if (h.b0 > 0) {   // NEXT-2: re-derive the elided params from the restored master
-        const uint32_t ni = (uint32_t)h.R->bucket_item_start[h.b0];
+    if (h.elide) {   // NEXT-2: re-derive the elided params from the restored master
         cudaEvent_t ta = nullptr;
         plex_status st;
         if ((st = timed_begin(c, pp.kern, &ta))) return st;
-        CK(launch_derive(false, h.d->items, ni, h.d->segs, pp.d_ptrs, (uint32_t)h.p->tensors.size(), h.d->cks_in,
-                         c->d_flag, pp.kern));
+        CK(launch_derive(false, h.d->items, (uint32_t)h.R->n_param_items, h.d->segs, pp.d_ptrs,
+                         (uint32_t)h.p->tensors.size(), h.d->cks_in, c->d_flag, pp.kern));
         if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
     }
     CK(launch_verify(h.d->cks_in, h.d->cks_want, (uint32_t)h.R->segs.size(), c->d_flag, pp.kern));
@@ -682,7 +720,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     if (st || (st = check_slab(c, plan, slab))) return st;
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
     DeviceGuard g(c->device);
-    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}};
+    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
     Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
             c->d_ctr};
@@ -691,13 +729,13 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
     if ((st = off_begin(c, pp, h))) return st;
-    for (int32_t b = h.b0; b < h.nb; ++b)
+    for (int32_t b = 0; b < h.nb; ++b)
         if ((st = off_bucket(c, pp, h, b))) return st;
     if ((st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
     slab->cks.swap(h.cks);
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
-    slab->elided = h.b0 > 0;
+    slab->elided = h.elide;
     return PLEX_OK;
 }
 
@@ -711,7 +749,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
         return PLEX_OK;                                     // idempotent
     }
     DeviceGuard g(c->device);
-    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}};
+    Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst)) ||
         (st = get_devplan(c, plan->p, &h.d)))
         return st;
@@ -722,7 +760,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
     if ((st = on_begin(c, pp, h))) return st;
-    for (int32_t b = h.b0; b < h.nb; ++b)
+    for (int32_t b = 0; b < h.nb; ++b)
         if ((st = on_bucket(c, pp, h, b))) return st;
     if ((st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
     if (*c->h_flag) {
@@ -759,8 +797,8 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     DeviceGuard g(c->device);
     const bool do_off = slab_out->residency == PLEX_RES_DEVICE;
     const bool do_on = slab_in->residency == PLEX_RES_HOST;
-    Half ho{&plan_out->p, &plan_out->p.ranks[c->rank], nullptr, slab_out, 0, {}};
-    Half hi{&plan_in->p, &plan_in->p.ranks[c->rank], nullptr, slab_in, 0, {}};
+    Half ho{&plan_out->p, &plan_out->p.ranks[c->rank], nullptr, slab_out, 0, {}, false, 0, nullptr, nullptr, nullptr};
+    Half hi{&plan_in->p, &plan_in->p.ranks[c->rank], nullptr, slab_in, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if (do_off && ((st = fill_state_ptrs(c, plan_out->p, src_out, n_src, 0)) || (st = get_devplan(c, plan_out->p, &ho.d))))
         return st;
     if (do_on && ((st = fill_state_ptrs(c, plan_in->p, reinterpret_cast<const void* const*>(dst_in), n_dst, 1)) ||
@@ -788,10 +826,10 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
     if (do_off && (st = off_begin(c, po, ho))) return st;
     if (do_on && (st = on_begin(c, pi, hi))) return st;
-    const int32_t no = do_off ? ho.nb - ho.b0 : 0, ni = do_on ? hi.nb - hi.b0 : 0;
+    const int32_t no = do_off ? ho.nb : 0, ni = do_on ? hi.nb : 0;
     for (int32_t k = 0; k < std::max(no, ni); ++k) {   // interleave so both directions start at once
-        if (k < no && (st = off_bucket(c, po, ho, ho.b0 + k))) return st;
-        if (k < ni && (st = on_bucket(c, pi, hi, hi.b0 + k))) return st;
+        if (k < no && (st = off_bucket(c, po, ho, k))) return st;
+        if (k < ni && (st = on_bucket(c, pi, hi, k))) return st;
     }
     if (do_off && (st = off_end(c, po, ho))) return st;
     if (do_on && (st = on_end(c, pi, hi))) return st;
@@ -806,7 +844,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         slab_out->cks.swap(ho.cks);
         slab_out->residency = PLEX_RES_HOST;
         slab_out->written = true;
-        slab_out->elided = ho.b0 > 0;
+        slab_out->elided = ho.elide;
     }
     if (do_on) {
         if (*c->h_flag) {
