@@ -63,6 +63,13 @@ class Ctx:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def allmin(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
+
     def allsum(self, x: float) -> float:
         if self.world == 1:
             return x
@@ -239,12 +246,19 @@ def scen_multiplex(a, c: Ctx):
     res = {"r": None}
     from paper_2605_20863_b200.state import synth_mutate  # noqa: F401  (mutation = simulated train step)
 
+    sizes = [pl.rank_info(c.rank).payload_bytes for pl in plans]
+    dup_used = {"n": 0}
+
     def run_trace():
         resident = res["r"]
         for j in schedule:
             if resident is not None and resident != j:
-                if a.duplex:
+                # duplex needs both jobs on the device during the switch
+                free = torch.cuda.mem_get_info(c.local)[0]
+                dup = a.duplex and c.allmin(1.0 if sizes[j] + (2 << 30) < free else 0.0) > 0.5
+                if dup:
                     jobs[resident].switch_to(jobs[j])
+                    dup_used["n"] += 1
                 else:
                     jobs[resident].suspend()
                     jobs[j].resume()
@@ -258,7 +272,8 @@ def scen_multiplex(a, c: Ctx):
     ms, clk = timed(c, run_trace, 1, 0)
     switches = len(schedule) - 1
     c.emit({"scenario": "multiplex", "jobs": models, "n_gpus": c.world, "rounds": a.rounds,
-            "visits": len(schedule), "switches": switches, "duplex": a.duplex, "trace_ms": round(ms, 1),
+            "visits": len(schedule), "switches": switches, "duplex": a.duplex, "duplex_switches": dup_used["n"],
+            "trace_ms": round(ms, 1),
             "ms_per_visit": round(ms / len(schedule), 1), "clocks": clk}, a.out)
 
 
