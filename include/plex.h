@@ -85,6 +85,7 @@ typedef int plex_status;
 /* Residency of a slab's job state (PAPER.md:505-506 hierarchical residency). */
 #define PLEX_RES_DEVICE  0
 #define PLEX_RES_HOST    1
+#define PLEX_RES_DISK    2   /* NEXT-4 cold tier */
 
 /* Context flags. */
 #define PLEX_CTX_TIMING    0x1u  /* record CUDA events around every kernel/copy */
@@ -256,6 +257,15 @@ PLEX_API plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t f
 PLEX_API plex_status plex_slab_destroy(plex_slab_t slab);
 /* host_ptr: the slab bytes (read/write, for verification and fault injection) */
 PLEX_API plex_status plex_slab_info(plex_slab_t slab, void** host_ptr, uint64_t* bytes, int32_t* residency);
+/* NEXT-4 cold tier (PAPER.md:505-506 GPU/host/NVMe residency; :574 "the NVMe
+ * tier bypasses the page cache through direct I/O"): write a HOST-resident
+ * slab's bytes to `path` with O_DIRECT using `threads` parallel writers, fsync,
+ * and release its pinned memory (residency DISK).  fill re-pins, reads the
+ * file back (residency HOST); onload then verifies the recorded checksums.
+ * E_STATE on a wrong residency, E_INVAL if the file cannot be opened with
+ * O_DIRECT, E_TIER_FULL on I/O or pinning failure (state unchanged). */
+PLEX_API plex_status plex_slab_spill(plex_slab_t slab, const char* path, int32_t threads);
+PLEX_API plex_status plex_slab_fill(plex_slab_t slab, const char* path, int32_t threads);
 /* *elided = 1 if the last offload elided the derived PARAM buckets. */
 PLEX_API plex_status plex_slab_elided(plex_slab_t slab, int32_t* elided);
 /* out[2*i], out[2*i+1] = (S1, S2) of segment i recorded at offload (R14). */

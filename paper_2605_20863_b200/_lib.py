@@ -20,7 +20,7 @@ ROLE_REPLICATED, ROLE_COL, ROLE_ROW, ROLE_EXPERT = 0, 1, 2, 3
 SLAB_KIND_MAJOR, SLAB_KEY_MAJOR = 0, 1
 RANKMAP_TP_FAST, RANKMAP_DP_FAST = 0, 1
 OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
-RES_DEVICE, RES_HOST = 0, 1
+RES_DEVICE, RES_HOST, RES_DISK = 0, 1, 2
 CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
 SLAB_HUGEPAGE = 0x1
 STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE, \
@@ -34,6 +34,7 @@ EXPORTS = [
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
+    "plex_slab_spill", "plex_slab_fill",
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
     "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
@@ -113,6 +114,8 @@ def _load() -> C.CDLL:
         "plex_slab_destroy": (C.c_int, [VP]),
         "plex_slab_info": (C.c_int, [VP, P(VP), P(U64), P(I32)]),
         "plex_slab_elided": (C.c_int, [VP, P(I32)]),
+        "plex_slab_spill": (C.c_int, [VP, C.c_char_p, I32]),
+        "plex_slab_fill": (C.c_int, [VP, C.c_char_p, I32]),
         "plex_slab_checksums": (C.c_int, [VP, P(U64), I32]),
         "plex_state_offload": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_state_onload": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),

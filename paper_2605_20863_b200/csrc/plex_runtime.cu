@@ -8,7 +8,13 @@
 // stream").
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <errno.h>
+#include <fcntl.h>
 #include <sys/mman.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <thread>
 
 #include <algorithm>
 #include <cstdio>
@@ -138,8 +144,9 @@ struct plex_slab_s {
     int rank = 0;
     uint64_t bytes = 0;
     uint8_t* host = nullptr;
+    uint32_t flags = 0;        // PLEX_SLAB_* used to pin
     bool registered = false;   // mmap + cudaHostRegister path
-    size_t map_bytes = 0;
+    size_t map_bytes = 0;      // pinned bytes (>= bytes, 4 KiB / 2 MiB aligned)
     int residency = PLEX_RES_DEVICE;
     bool written = false;
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
@@ -638,6 +645,53 @@ plex_status plex_ctx_reset_stats(plex_ctx_t c) {
 }
 
 // ---- slabs ("the host tier uses pinned memory") ---------------
+static plex_status slab_pin(plex_slab_s* s) {
+    const size_t want = std::max<uint64_t>(s->bytes, 4096);
+    if (s->flags & PLEX_SLAB_HUGEPAGE) {
+        const size_t huge = 2ull << 20;
+        const size_t n = align_up(want, huge);
+        void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) {
+            set_error("mmap of %zu B failed", n);
+            return PLEX_E_TIER_FULL;
+        }
+        madvise(p, n, MADV_HUGEPAGE);
+        cudaError_t e = cudaHostRegister(p, n, cudaHostRegisterDefault);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            munmap(p, n);
+            set_error("cudaHostRegister(%zu B): %s", n, cudaGetErrorString(e));
+            return PLEX_E_TIER_FULL;
+        }
+        s->host = reinterpret_cast<uint8_t*>(p);
+        s->map_bytes = n;
+        s->registered = true;
+    } else {
+        const size_t n = align_up(want, 4096);
+        cudaError_t e = cudaHostAlloc(&s->host, n, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            s->host = nullptr;
+            set_error("cudaHostAlloc(%zu B): %s", n, cudaGetErrorString(e));
+            return PLEX_E_TIER_FULL;
+        }
+        s->map_bytes = n;
+        s->registered = false;
+    }
+    return PLEX_OK;
+}
+
+static void slab_unpin(plex_slab_s* s) {
+    if (!s->host) return;
+    if (s->registered) {
+        cudaHostUnregister(s->host);
+        munmap(s->host, s->map_bytes);
+    } else {
+        cudaFreeHost(s->host);
+    }
+    s->host = nullptr;
+}
+
 plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, plex_slab_t* out) {
     if (!plan || !out || rank < 0 || rank >= plan->p.world) { set_error("bad slab arguments"); return PLEX_E_INVAL; }
     *out = nullptr;
@@ -646,36 +700,12 @@ plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, ple
     s->plan_id = plan->p.id;
     s->rank = rank;
     s->bytes = R.slab_bytes;
+    s->flags = flags;
     s->cks.assign(2 * R.segs.size(), 0);
-    const size_t alloc = std::max<uint64_t>(R.slab_bytes, 256);
-    if (flags & PLEX_SLAB_HUGEPAGE) {
-        const size_t huge = 2ull << 20;
-        s->map_bytes = align_up(alloc, huge);
-        void* p = mmap(nullptr, s->map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-        if (p == MAP_FAILED) {
-            set_error("mmap of %zu B failed", s->map_bytes);
-            delete s;
-            return PLEX_E_TIER_FULL;
-        }
-        madvise(p, s->map_bytes, MADV_HUGEPAGE);
-        cudaError_t e = cudaHostRegister(p, s->map_bytes, cudaHostRegisterDefault);
-        if (e != cudaSuccess) {
-            (void)cudaGetLastError();
-            munmap(p, s->map_bytes);
-            delete s;
-            set_error("cudaHostRegister(%zu B): %s", alloc, cudaGetErrorString(e));
-            return PLEX_E_TIER_FULL;
-        }
-        s->host = reinterpret_cast<uint8_t*>(p);
-        s->registered = true;
-    } else {
-        cudaError_t e = cudaHostAlloc(&s->host, alloc, cudaHostAllocPortable);
-        if (e != cudaSuccess) {
-            (void)cudaGetLastError();
-            delete s;
-            set_error("cudaHostAlloc(%zu B): %s", alloc, cudaGetErrorString(e));
-            return PLEX_E_TIER_FULL;
-        }
+    plex_status st = slab_pin(s);
+    if (st) {
+        delete s;
+        return st;
     }
     *out = s;
     return PLEX_OK;
@@ -683,13 +713,76 @@ plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, ple
 
 plex_status plex_slab_destroy(plex_slab_t s) {
     if (!s) return PLEX_OK;
-    if (s->registered) {
-        cudaHostUnregister(s->host);
-        munmap(s->host, s->map_bytes);
-    } else {
-        cudaFreeHost(s->host);
-    }
+    slab_unpin(s);
     delete s;
+    return PLEX_OK;
+}
+
+// ---- NEXT-4 cold tier: spill / fill a slab to NVMe with direct I/O -------------------
+// PAPER.md:505-506 (GPU / host / NVMe residency) and :574 ("the NVMe tier
+// bypasses the page cache through direct I/O").  The slab's canonical bytes
+// go to `path` with O_DIRECT (pinned slab memory is page-aligned and the
+// transfer is padded to 4 KiB) by several threads at disjoint offsets, and
+// the pinned memory is released: residency DISK.  fill re-pins and reads it
+// back: residency HOST; the checksums recorded at offload travel with the
+// slab object, so a corrupted file is caught by the next onload.
+static plex_status pio(bool write, int fd, uint8_t* buf, size_t n, int threads) {
+    const size_t chunk = 64ull << 20;
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{0};
+    auto work = [&]() {
+        for (;;) {
+            const size_t o = next.fetch_add(chunk);
+            if (o >= n || err.load()) return;
+            size_t len = std::min(chunk, n - o), done = 0;
+            while (done < len) {
+                const ssize_t r = write ? pwrite(fd, buf + o + done, len - done, (off_t)(o + done))
+                                        : pread(fd, buf + o + done, len - done, (off_t)(o + done));
+                if (r <= 0) { err.store(r == 0 ? EIO : errno); return; }
+                done += (size_t)r;
+            }
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int i = 1; i < threads; ++i) ts.emplace_back(work);
+    work();
+    for (auto& t : ts) t.join();
+    if (err.load()) {
+        set_error("%s: %s", write ? "pwrite" : "pread", strerror(err.load()));
+        return PLEX_E_TIER_FULL;
+    }
+    return PLEX_OK;
+}
+
+plex_status plex_slab_spill(plex_slab_t s, const char* path, int32_t threads) {
+    if (!s || !path) { set_error("NULL slab/path"); return PLEX_E_INVAL; }
+    if (s->residency != PLEX_RES_HOST || !s->host) { set_error("spill needs a HOST-resident slab"); return PLEX_E_STATE; }
+    const size_t n = align_up(std::max<uint64_t>(s->bytes, 1), 4096);
+    int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | O_DIRECT, 0600);
+    if (fd < 0) { set_error("open(%s, O_DIRECT): %s", path, strerror(errno)); return PLEX_E_INVAL; }
+    plex_status st = pio(true, fd, s->host, n, std::max(1, threads));
+    if (!st && fsync(fd) != 0) { set_error("fsync: %s", strerror(errno)); st = PLEX_E_TIER_FULL; }
+    close(fd);
+    if (st) return st;
+    slab_unpin(s);
+    s->residency = PLEX_RES_DISK;
+    return PLEX_OK;
+}
+
+plex_status plex_slab_fill(plex_slab_t s, const char* path, int32_t threads) {
+    if (!s || !path) { set_error("NULL slab/path"); return PLEX_E_INVAL; }
+    if (s->residency != PLEX_RES_DISK) { set_error("fill needs a DISK-resident slab"); return PLEX_E_STATE; }
+    const size_t n = align_up(std::max<uint64_t>(s->bytes, 1), 4096);
+    int fd = open(path, O_RDONLY | O_DIRECT);
+    if (fd < 0) { set_error("open(%s, O_DIRECT): %s", path, strerror(errno)); return PLEX_E_INVAL; }
+    plex_status st = slab_pin(s);
+    if (!st) st = pio(false, fd, s->host, n, std::max(1, threads));
+    close(fd);
+    if (st) {                   // no partial state change: stay on disk
+        slab_unpin(s);
+        return st;
+    }
+    s->residency = PLEX_RES_HOST;
     return PLEX_OK;
 }
 
@@ -719,6 +812,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     plex_status st = check_common(c, plan);
     if (st || (st = check_slab(c, plan, slab))) return st;
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
+    if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
@@ -748,6 +842,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
         if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
         return PLEX_OK;                                     // idempotent
     }
+    if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier: plex_slab_fill first"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst)) ||

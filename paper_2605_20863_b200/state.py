@@ -223,9 +223,17 @@ class Slab:
     def host_bytes(self) -> np.ndarray:
         """Writable NumPy view of the pinned slab bytes."""
         p, n, _ = self.info()
-        if n == 0:
+        if n == 0 or not p:                      # empty, or spilled to the NVMe tier
             return np.zeros(0, dtype=np.uint8)
         return np.ctypeslib.as_array((C.c_uint8 * n).from_address(p))
+
+    def spill(self, path: str, threads: int = 8) -> None:
+        """NEXT-4: move the slab to the NVMe tier (O_DIRECT) and unpin it."""
+        check(lib.plex_slab_spill(self.h, path.encode(), threads))
+
+    def fill(self, path: str, threads: int = 8) -> None:
+        """NEXT-4: bring a spilled slab back into pinned host memory."""
+        check(lib.plex_slab_fill(self.h, path.encode(), threads))
 
     def checksums(self) -> np.ndarray:
         n = 2 * self.plan.rank_info(self.rank).n_segments

@@ -377,3 +377,42 @@ def test_sync_from_slab(model, W, tp, dp, ep, elide):
     with pytest.raises(P.PlexError) as e:             # device-resident again: nothing to read in the slab
         mgrs[0].sync_rank_from_slab(plan, 0, jobs[0].slab, arenas)
     assert e.value.code == L.E_STATE
+
+
+# ---- NEXT-4 NVMe cold tier ----------------------------------------------------------------------
+def test_slab_nvme_tier(tmp_path):
+    man = manifest("mid")
+    plan = P.Plan(man, world=2, bucket_bytes=1 << 16, tile_bytes=1024)
+    m = mgr(2, 1, bucket=1 << 16)
+    job = P.Job(m, plan, seed=60, rank=1).alloc().init_synthetic(special_bits=3)
+    before = {k: bits_np(v) for k, v in job.shards.items()}
+    job.suspend()
+    slab_bytes = job.slab.host_bytes().copy()
+    path = str(tmp_path / "slab.bin")
+    try:
+        job.slab.spill(path, threads=4)
+    except P.PlexError as e:                        # filesystem without O_DIRECT
+        pytest.skip(f"O_DIRECT unavailable here: {e}")
+    assert job.slab.residency == L.RES_DISK and job.slab.host_bytes().size == 0
+    with pytest.raises(P.PlexError) as e:
+        job.resume()
+    assert e.value.code == L.E_STATE
+    job.slab.fill(path, threads=3)
+    assert job.slab.residency == L.RES_HOST
+    assert np.array_equal(job.slab.host_bytes(), slab_bytes)
+    job.resume()
+    for k, v in job.shards.items():
+        assert np.array_equal(bits_np(v), before[k])
+    # a corrupted file is caught by the onload checksum
+    job.suspend()
+    job.slab.spill(path)
+    with open(path, "r+b") as f:
+        f.seek(plan.segments(1)[5].slab_offset + 3)
+        b = f.read(1)
+        f.seek(-1, 1)
+        f.write(bytes([b[0] ^ 0x40]))
+    job.slab.fill(path)
+    with pytest.raises(P.PlexError) as e:
+        job.resume()
+    assert e.value.code == L.E_CHECKSUM
+    m.close()
