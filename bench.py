@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--model", default="qwen2.5-7b")
     ap.add_argument("--tp", type=int, default=0, help="rollout TP (default min(2, N))")
     ap.add_argument("--ep", type=int, default=1)
+    ap.add_argument("--rank-map", default="auto", choices=["tp", "dp", "auto"],
+                    help="rollout rank placement (R10): g = dp*TP+tp, g = tp*DP+dp, or the lighter ledger")
     ap.add_argument("--bucket-mb", type=int, default=2048)
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--no-hugepage", dest="hugepage", action="store_false",
@@ -249,7 +251,9 @@ def run_plex(a):
     mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=a.slots, timing=True,
                          sync_nccl=a.sync_nccl)
     t0 = time.perf_counter()
-    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep) for _ in range(2)]
+    rank_map = {"tp": 0, "dp": 1, "auto": 2}[a.rank_map]
+    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map)
+             for _ in range(2)]
     plan_s = (time.perf_counter() - t0) / 2
     plan = plans[0]
     info = plan.rank_info(rank)
@@ -441,7 +445,8 @@ def run_plex(a):
                        "bucket_bytes": bucket, "staging_slots": a.slots,
                        "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
                        "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
-                       "sync_transport": "nccl" if a.sync_nccl else "nvlink-push"},
+                       "sync_transport": "nccl" if a.sync_nccl else "nvlink-push",
+                       "rank_map": ["tp_fast (g = dp*TP + tp)", "dp_fast (g = tp*DP + dp)"][plan.stats().rank_map]},
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
                          "unit": "GB/s", "frac": frac(achieved, peak_hbm), "traffic": traffic,
                          "algorithmic_bytes_per_launch": int(per_launch_bytes), "avg_launch_ms": round(avg_ms, 4),

@@ -75,6 +75,8 @@ typedef int plex_status;
 
 #define PLEX_RANKMAP_TP_FAST  0   /* R10: g = dp*TP + tp (default) */
 #define PLEX_RANKMAP_DP_FAST  1   /* R10: g = tp*DP + dp           */
+#define PLEX_RANKMAP_AUTO     2   /* R10: whichever of the two moves fewer bytes over the
+                                     busiest link (plan_stats.rank_map reports it) */
 
 /* Transition ops. */
 #define PLEX_OP_NONE     0
@@ -162,6 +164,7 @@ typedef struct {
     int32_t n_tensors;
     int32_t world, tp, dp, ep;
     uint64_t total_params;       /* sum of numel over the manifest         */
+    int32_t rank_map;            /* rank map in use (AUTO resolved)         */
 } plex_plan_stats;
 
 typedef struct {

@@ -18,7 +18,7 @@ NUM_KINDS = 4
 KINDMASK_ALL, KINDMASK_OPTIM = 0xF, 0xE
 ROLE_REPLICATED, ROLE_COL, ROLE_ROW, ROLE_EXPERT = 0, 1, 2, 3
 SLAB_KIND_MAJOR, SLAB_KEY_MAJOR = 0, 1
-RANKMAP_TP_FAST, RANKMAP_DP_FAST = 0, 1
+RANKMAP_TP_FAST, RANKMAP_DP_FAST, RANKMAP_AUTO = 0, 1, 2
 OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
 RES_DEVICE, RES_HOST, RES_DISK = 0, 1, 2
 CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
@@ -64,7 +64,7 @@ class PlanReq(C.Structure):
 class PlanStats(C.Structure):
     _fields_ = [("n_ops", C.c_int32), ("ops", C.c_int32 * 4), ("op_jobs", C.c_int64 * 4),
                 ("n_tensors", C.c_int32), ("world", C.c_int32), ("tp", C.c_int32), ("dp", C.c_int32),
-                ("ep", C.c_int32), ("total_params", C.c_uint64)]
+                ("ep", C.c_int32), ("total_params", C.c_uint64), ("rank_map", C.c_int32)]
 
 
 class RankInfo(C.Structure):

@@ -244,6 +244,61 @@ static void emit_push(Plan& p, std::vector<std::vector<std::vector<PushItem>>>& 
     }
 }
 
+// a9-a11 layout: destination tensors of every rank, the push items of every
+// source rank and the ledger, for p.rank_map.
+static plex_status build_sync(Plan& p) {
+    std::vector<int32_t> order;
+    std::map<int32_t, std::vector<int32_t>> members;
+    std::map<int32_t, int32_t> n_experts;
+    for (int32_t i = 0; i < (int32_t)p.tensors.size(); ++i) {
+        const Tensor& T = p.tensors[i];
+        if (!members.count(T.group)) order.push_back(T.group);
+        members[T.group].push_back(i);
+        if (T.role == PLEX_ROLE_EXPERT) n_experts[T.group] = std::max(n_experts[T.group], T.expert + 1);
+    }
+    for (auto& kv : members)
+        std::stable_sort(kv.second.begin(), kv.second.end(),
+                         [&](int32_t a, int32_t b) { return p.tensors[a].slot < p.tensors[b].slot; });
+    for (int32_t g = 0; g < p.world; ++g) {
+        plex_status s = build_dst(p, g, order, members, n_experts);
+        if (s) return s;
+    }
+    std::vector<std::vector<std::vector<PushItem>>> per(p.world, std::vector<std::vector<PushItem>>(p.world));
+    for (int32_t g = 0; g < p.world; ++g) emit_push(p, per, g);
+    // Interleave each source's items round-robin over destinations starting
+    // at r+1 so that, at any moment, every sender spreads its NVLink stores
+    // over all peers instead of all senders converging on one receiver.
+    for (int32_t r = 0; r < p.world; ++r) {
+        RankPlan& R = p.ranks[r];
+        std::vector<size_t> pos(p.world, 0);
+        size_t left = 0;
+        for (int32_t g = 0; g < p.world; ++g) left += per[r][g].size();
+        R.push.reserve(left);
+        while (left) {
+            for (int32_t k = 1; k <= p.world; ++k) {
+                const int32_t g = (r + k) % p.world;
+                if (pos[g] < per[r][g].size()) { R.push.push_back(per[r][g][pos[g]++]); --left; }
+            }
+        }
+        for (const PushItem& it : R.push) R.src_read_bytes += (uint64_t)it.rows * it.cols * 4;
+    }
+    for (int32_t r = 0; r < p.world; ++r)
+        for (int32_t g = 0; g < p.world; ++g) {
+            const uint64_t b = p.ledger[(size_t)r * p.world + g];
+            if (r == g) p.ranks[r].local_bytes += b;
+            else { p.ranks[r].send_bytes += b; p.ranks[g].recv_bytes += b; }
+        }
+    return PLEX_OK;
+}
+
+// R10: the rollout rank map is a free placement choice; AUTO keeps the map
+// whose zero-redundancy ledger has the smaller max over ranks of max(send, recv).
+static uint64_t max_link_bytes(const Plan& p) {
+    uint64_t m = 0;
+    for (const RankPlan& R : p.ranks) m = std::max(m, std::max(R.send_bytes, R.recv_bytes));
+    return m;
+}
+
 static plex_status build(const plex_plan_req* q, Plan& p) {
     if (!q || q->n_tensors <= 0 || !q->tensors) { set_error("empty manifest"); return PLEX_E_INVAL; }
     if (q->world < 1) { set_error("world must be >= 1"); return PLEX_E_INVAL; }
@@ -260,7 +315,10 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
     }
     if (p.kind_mask & ~PLEX_KINDMASK_ALL) { set_error("bad kind mask"); return PLEX_E_INVAL; }
     if (p.layout != PLEX_SLAB_KIND_MAJOR && p.layout != PLEX_SLAB_KEY_MAJOR) { set_error("bad slab layout"); return PLEX_E_INVAL; }
-    if (p.rank_map != PLEX_RANKMAP_TP_FAST && p.rank_map != PLEX_RANKMAP_DP_FAST) { set_error("bad rank map"); return PLEX_E_INVAL; }
+    if (p.rank_map != PLEX_RANKMAP_TP_FAST && p.rank_map != PLEX_RANKMAP_DP_FAST && p.rank_map != PLEX_RANKMAP_AUTO) {
+        set_error("bad rank map");
+        return PLEX_E_INVAL;
+    }
     const bool sync = !(p.tp == 0 && p.dp == 0);
     if (sync && (p.tp < 1 || p.dp < 1 || p.tp * p.dp != p.world)) {
         set_error("tp*dp (%d*%d) must equal world %d", p.tp, p.dp, p.world); return PLEX_E_INVAL;
@@ -309,48 +367,27 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
     }
     p.ledger.assign((size_t)p.world * p.world, 0);
     if (sync) {
-        std::vector<int32_t> order;
-        std::map<int32_t, std::vector<int32_t>> members;
-        std::map<int32_t, int32_t> n_experts;
-        for (int32_t i = 0; i < q->n_tensors; ++i) {
-            const Tensor& T = p.tensors[i];
-            if (!members.count(T.group)) order.push_back(T.group);
-            members[T.group].push_back(i);
-            if (T.role == PLEX_ROLE_EXPERT) n_experts[T.group] = std::max(n_experts[T.group], T.expert + 1);
-        }
-        for (auto& kv : members)
-            std::stable_sort(kv.second.begin(), kv.second.end(),
-                             [&](int32_t a, int32_t b) { return p.tensors[a].slot < p.tensors[b].slot; });
-        for (int32_t g = 0; g < p.world; ++g) {
-            plex_status s = build_dst(p, g, order, members, n_experts);
-            if (s) return s;
-        }
-        std::vector<std::vector<std::vector<PushItem>>> per(p.world, std::vector<std::vector<PushItem>>(p.world));
-        for (int32_t g = 0; g < p.world; ++g) emit_push(p, per, g);
-        // Interleave each source's items round-robin over destinations starting
-        // at r+1 so that, at any moment, every sender spreads its NVLink stores
-        // over all peers instead of all senders converging on one receiver.
-        for (int32_t r = 0; r < p.world; ++r) {
-            RankPlan& R = p.ranks[r];
-            std::vector<size_t> pos(p.world, 0);
-            size_t left = 0;
-            for (int32_t g = 0; g < p.world; ++g) left += per[r][g].size();
-            R.push.reserve(left);
-            while (left) {
-                for (int32_t k = 1; k <= p.world; ++k) {
-                    const int32_t g = (r + k) % p.world;
-                    if (pos[g] < per[r][g].size()) { R.push.push_back(per[r][g][pos[g]++]); --left; }
-                }
+        if (q->rank_map == PLEX_RANKMAP_AUTO) {
+            int32_t best = PLEX_RANKMAP_TP_FAST;
+            uint64_t best_bytes = ~0ull;
+            for (int32_t m : {PLEX_RANKMAP_TP_FAST, PLEX_RANKMAP_DP_FAST}) {
+                Plan t;
+                t.tensors = p.tensors;
+                t.world = p.world; t.tp = p.tp; t.dp = p.dp; t.ep = p.ep; t.rank_map = m;
+                t.tile = p.tile;
+                t.ranks.resize(p.world);
+                t.ledger.assign((size_t)p.world * p.world, 0);
+                plex_status s2 = build_sync(t);
+                if (s2) return s2;
+                const uint64_t b = max_link_bytes(t);
+                if (b < best_bytes) { best_bytes = b; best = m; }
             }
-            for (const PushItem& it : R.push) R.src_read_bytes += (uint64_t)it.rows * it.cols * 4;
+            p.rank_map = best;
         }
-        for (int32_t r = 0; r < p.world; ++r)
-            for (int32_t g = 0; g < p.world; ++g) {
-                const uint64_t b = p.ledger[(size_t)r * p.world + g];
-                if (r == g) p.ranks[r].local_bytes += b;
-                else { p.ranks[r].send_bytes += b; p.ranks[g].recv_bytes += b; }
-            }
+        plex_status s2 = build_sync(p);
+        if (s2) return s2;
     }
+    st.rank_map = p.rank_map;
     p.id = g_plan_ids.fetch_add(1);
     return PLEX_OK;
 }

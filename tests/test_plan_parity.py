@@ -103,3 +103,24 @@ def test_plan_is_deterministic():
         assert a.dst_tensors(r) == b.dst_tensors(r)
         sa = [(s.slab_offset, s.nbytes) for s in a.segments(r)]
         assert sa == [(s.slab_offset, s.nbytes) for s in b.segments(r)]
+
+
+def _busiest(L):
+    off = L - np.diag(np.diag(L))
+    return max(off.sum(0).max(), off.sum(1).max())
+
+
+def test_rank_map_auto_picks_lighter_ledger():
+    """R10: AUTO resolves to the rank map with the smaller busiest-link bytes;
+    for Qwen2.5-7B FSDP-8 -> TP-2 x DP-4 that is DP_FAST (5.99 vs 7.33 GB)."""
+    man = manifest("qwen2.5-7b")
+    p = Plan(man, head_dim=128, world=8, tp=2, dp=4, rank_map=L.RANKMAP_AUTO)
+    assert p.stats().rank_map == L.RANKMAP_DP_FAST
+    assert np.array_equal(p.ledger(), O.ledger(man, 8, 2, 4, 1, O.DP_FAST))
+    for model, W, tp, dp, ep in CASES:
+        q = Plan(manifest(model), head_dim=MODELS[model].head_dim, world=W, tp=tp, dp=dp, ep=ep,
+                 rank_map=L.RANKMAP_AUTO)
+        m = q.stats().rank_map
+        assert np.array_equal(q.ledger(), O.ledger(manifest(model), W, tp, dp, ep, m))
+        other = O.ledger(manifest(model), W, tp, dp, ep, 1 - m)
+        assert _busiest(q.ledger()) <= _busiest(other)

@@ -100,9 +100,17 @@ def main():
             lines.append(f"| {m} | " + " | ".join(vals) + " |")
         lines.append(f"| kernel | " + " | ".join(d["kernel"][:60] for d in res) + " |")
         lines.append("")
-        rd = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in res]
-        traffic[which] = {"dram_bytes_per_launch": sum(rd) / len(rd), "source": f"gpurun_out/{tag}_{which}.ncu-rep",
-                          "duration_us": sum(d.get("gpu__time_duration.sum", 0) for d in res) / len(res)}
+        groups = {}
+        for d in res:      # pack_kernel<1,...> = K1 pack, pack_kernel<0,...> = K2 unpack
+            k = which
+            if which == "pack" and "pack_kernel<0" in d["kernel"].replace("(bool)0", "0").replace(" ", ""):
+                k = "unpack"
+            groups.setdefault(k, []).append(d)
+        for k, ds in groups.items():
+            rd = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in ds]
+            traffic[k] = {"dram_bytes_per_launch": sum(rd) / len(rd), "source": f"gpurun_out/{tag}_{which}.ncu-rep",
+                          "duration_us": sum(d.get("gpu__time_duration.sum", 0) for d in ds) / len(ds),
+                          "launches": len(ds)}
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     out = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md")
     open(out, "w").write("\n".join(lines) + "\n")
