@@ -206,6 +206,12 @@ typedef struct {
     uint64_t bytes;              /* algorithmic bytes moved by those launches */
 } plex_kernel_stats;
 
+typedef struct {
+    int32_t which;               /* PLEX_STAT_*                              */
+    float ms;                    /* CUDA-event duration of the launch/copy   */
+    uint64_t bytes;              /* algorithmic bytes                        */
+} plex_launch_record;
+
 #define PLEX_STAT_PACK    0      /* K1 gather-pack (+checksum)  */
 #define PLEX_STAT_UNPACK  1      /* K2 scatter-unpack (+verify) */
 #define PLEX_STAT_PUSH    2      /* K3+K4 fused cast/reshard push over NVLink */
@@ -252,6 +258,9 @@ PLEX_API plex_status plex_ctx_create(int32_t device, void* staging, uint64_t sta
 PLEX_API plex_status plex_ctx_destroy(plex_ctx_t ctx);
 PLEX_API plex_status plex_ctx_stats(plex_ctx_t ctx, int32_t which, plex_kernel_stats* out);
 PLEX_API plex_status plex_ctx_reset_stats(plex_ctx_t ctx);
+/* Per-launch records behind plex_ctx_stats (PLEX_CTX_TIMING), oldest first,
+ * since the last reset; *n = how many exist (copies min(cap, *n)). */
+PLEX_API plex_status plex_ctx_trace(plex_ctx_t ctx, plex_launch_record* out, int32_t cap, int32_t* n);
 
 /* Pinned host slab for `rank`'s state under `plan` (exact size; PAPER.md:574
  * "the host tier uses pinned memory").  Initial residency: DEVICE.

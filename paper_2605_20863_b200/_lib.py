@@ -33,6 +33,7 @@ EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
+    "plex_ctx_trace",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_slab_spill", "plex_slab_fill",
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
@@ -85,6 +86,10 @@ class DstDesc(C.Structure):
                 ("rows", C.c_int64), ("cols", C.c_int64)]
 
 
+class LaunchRecord(C.Structure):
+    _fields_ = [("which", C.c_int32), ("ms", C.c_float), ("bytes", C.c_uint64)]
+
+
 class KernelStats(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64)]
 
@@ -110,6 +115,7 @@ def _load() -> C.CDLL:
         "plex_ctx_destroy": (C.c_int, [VP]),
         "plex_ctx_stats": (C.c_int, [VP, I32, P(KernelStats)]),
         "plex_ctx_reset_stats": (C.c_int, [VP]),
+        "plex_ctx_trace": (C.c_int, [VP, P(LaunchRecord), I32, P(I32)]),
         "plex_slab_create": (C.c_int, [VP, I32, U32, P(VP)]),
         "plex_slab_destroy": (C.c_int, [VP]),
         "plex_slab_info": (C.c_int, [VP, P(VP), P(U64), P(I32)]),

@@ -114,6 +114,7 @@ struct plex_ctx_s {
     size_t pool_used = 0;
     std::vector<Timed> pending;
     plex_kernel_stats stats[PLEX_NUM_STATS] = {};
+    std::vector<plex_launch_record> trace;   // every timed launch since the last reset
     // pointer tables (pinned host mirror -> device)
     uint64_t* h_ptrs = nullptr;
     uint64_t* d_ptrs = nullptr;
@@ -269,6 +270,7 @@ static plex_status timed_collect(plex_ctx_s* c) {
         c->stats[t.which].launches += 1;
         c->stats[t.which].total_ms += ms;
         c->stats[t.which].bytes += t.bytes;
+        if (c->trace.size() < (1u << 20)) c->trace.push_back(plex_launch_record{t.which, ms, t.bytes});
     }
     c->pending.clear();
     c->pool_used = 0;
@@ -641,6 +643,14 @@ plex_status plex_ctx_stats(plex_ctx_t c, int32_t which, plex_kernel_stats* out) 
 plex_status plex_ctx_reset_stats(plex_ctx_t c) {
     if (!c) { set_error("NULL ctx"); return PLEX_E_INVAL; }
     for (auto& s : c->stats) s = plex_kernel_stats{};
+    c->trace.clear();
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_trace(plex_ctx_t c, plex_launch_record* out, int32_t cap, int32_t* n) {
+    if (!c || !n) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    *n = (int32_t)c->trace.size();
+    if (out) std::memcpy(out, c->trace.data(), sizeof(plex_launch_record) * std::min<size_t>(cap, c->trace.size()));
     return PLEX_OK;
 }
 

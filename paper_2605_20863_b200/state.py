@@ -392,6 +392,14 @@ class StateManager:
             out[nm] = {"launches": s.launches, "ms": s.total_ms, "bytes": s.bytes}
         return out
 
+    def trace(self) -> List[Tuple[str, float, int]]:
+        """Every timed launch since the last reset: (kind, ms, algorithmic bytes)."""
+        n = C.c_int32()
+        check(lib.plex_ctx_trace(self.h, None, 0, C.byref(n)))
+        buf = (L.LaunchRecord * max(1, n.value))()
+        check(lib.plex_ctx_trace(self.h, buf, n.value, C.byref(n)))
+        return [(L.STAT_NAMES[r.which], float(r.ms), int(r.bytes)) for r in buf[:n.value]]
+
     def reset_stats(self) -> None:
         check(lib.plex_ctx_reset_stats(self.h))
 

@@ -24,9 +24,11 @@ def main():
     ap.add_argument("--model", default="qwen2.5-0.5b")
     ap.add_argument("--buckets", default="256,1024")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--ballast-gb", type=int, default=0, help="occupy this much HBM first (experiment)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
-    out = {"variant": os.environ.get("PLEX_PACK_VARIANT", "0"), "model": a.model}
+    ballast = torch.empty(a.ballast_gb << 30, dtype=torch.uint8, device="cuda") if a.ballast_gb else None
+    out = {"ballast_gb": a.ballast_gb, "variant": os.environ.get("PLEX_PACK_VARIANT", "0"), "model": a.model}
     for bmb in [int(x) for x in a.buckets.split(",")]:
         mgr = P.StateManager(device=0, bucket_bytes=bmb << 20, n_slots=2, timing=True, duplex=False,
                              bootstrap=False)
@@ -49,6 +51,9 @@ def main():
                 res[k] = {"GBs": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1),
                           "us_per_launch": round(1e3 * v["ms"] / v["launches"], 2),
                           "MB_per_launch": round(v["bytes"] / v["launches"] / 1e6, 2)}
+        tr = [(k, round(ms * 1e3, 1), round(b / (ms * 1e-3) / 1e9)) for k, ms, b in mgr.trace()
+              if k in ("pack", "unpack")]
+        res["per_launch_us_GBs"] = tr[:64]
         out[f"bucket_{bmb}MiB"] = res
         del job, arena, plan
         mgr.close()
