@@ -105,7 +105,8 @@ def scen_duplex(a, c: Ctx):
     shape = MODELS[a.model]
     tp = a.tp or min(2, c.world)
     mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
-    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp) for _ in range(2)]
+    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO)
+             for _ in range(2)]
     jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic() for pl, s in zip(plans, (1, 2))]
     arena = mgr.arena(plans[0])
     jobs[1].suspend()
@@ -203,10 +204,14 @@ def scen_moe(a, c: Ctx):
     shape = MODELS[model]
     tp = min(2, c.world)
     mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
-    plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, ep=c.world)
+    plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, ep=c.world,
+                    rank_map=L.RANKMAP_AUTO)
     job = P.Job(mgr, plan, seed=3, slab=False).alloc(kinds=(1,)).init_synthetic()
     arena = mgr.arena(plan)
+    mgr.reset_stats()
     ms_sync, clk = timed(c, lambda: job.sync(arena), a.steps, a.warmup)
+    st = mgr.stats()
+    push_ms = c.allmax(st["push"]["ms"] / max(1, st["push"]["launches"]))
     info = plan.rank_info(c.rank)
     nv = c.allmax(float(max(info.send_bytes, info.recv_bytes)))
     # per-expert units: KEY_MAJOR slab of the first --units (layer, expert) units
@@ -224,8 +229,9 @@ def scen_moe(a, c: Ctx):
     ms_unit, _ = timed(c, lambda: (ujob.suspend(release=False), ujob.resume()), a.steps, a.warmup)
     ub = uplan.rank_info(c.rank).payload_bytes
     c.emit({"scenario": "moe", "model": model, "n_gpus": c.world, "layout": f"attn TP-{tp}xDP-{c.world // tp}, EP-{c.world}",
-            "sync_ms": round(ms_sync, 3), "nvlink_bytes_max_rank": nv,
-            "nvlink_GBs": round(nv / (ms_sync * 1e-3) / 1e9, 1) if c.world > 1 else None,
+            "sync_ms": round(ms_sync, 3), "push_kernel_ms": round(push_ms, 3), "nvlink_bytes_max_rank": nv,
+            "nvlink_GBs_push_kernel": round(nv / (push_ms * 1e-3) / 1e9, 1) if c.world > 1 else None,
+            "rank_map": plan.stats().rank_map,
             "units": a.units, "unit_bytes_per_gpu": ub // max(1, a.units),
             "unit_offload_onload_ms": round(ms_unit, 3), "clocks": clk}, a.out)
 
