@@ -159,6 +159,13 @@ class Plan:
         shape = self.manifest[t][1]
         return (b - a,) + tuple(shape[1:])
 
+    def shard_numels(self, rank: int) -> List[int]:
+        """numel of every tensor's FSDP shard on `rank` (cached)."""
+        cache = self.__dict__.setdefault("_numels", {})
+        if rank not in cache:
+            cache[rank] = [int(np.prod(self.shard_shape(rank, t))) for t in range(len(self.manifest))]
+        return cache[rank]
+
     def dst_tensors(self, rank: int) -> List[Tuple[str, int, Tuple[int, ...]]]:
         """(rollout name, arena byte offset, shape) of rank's destination tensors."""
         n = self.rank_info(rank).n_dst_tensors
@@ -326,37 +333,70 @@ class StateManager:
 
     # ---- the four hot-path calls --------------------------------------------------
     @staticmethod
-    def _state_ptrs(plan: Plan, shards: Dict[Tuple[str, int], torch.Tensor]):
+    def _state_ptrs(plan: Plan, shards: Dict[Tuple[str, int], torch.Tensor], rank: int):
+        """Pointer table [kind * n_tensors + t]; every shard is checked against the
+        plan (device, contiguity, dtype width, FSDP shard numel) before the
+        library touches it, so a mis-sized tensor never reaches a kernel."""
         nt = len(plan.manifest)
         ptrs = [0] * (L.NUM_KINDS * nt)
+        numels = plan.shard_numels(rank)
         for (key, kind), t in shards.items():
+            ti = plan.index[key]
+            if not t.is_cuda:
+                raise ValueError(f"shard {key}/{kind} must be a CUDA tensor")
             if not t.is_contiguous():
                 raise ValueError(f"shard {key}/{kind} must be contiguous")
-            ptrs[kind * nt + plan.index[key]] = t.data_ptr() if t.numel() else 0
+            if t.element_size() != (2 if kind == L.KIND_PARAM else 4):
+                raise ValueError(f"shard {key}/{kind}: element size {t.element_size()} does not match the kind")
+            want = numels[ti]
+            if t.numel() != want:
+                raise ValueError(f"shard {key}/{kind}: {t.numel()} elements, plan expects {want} on rank {rank}")
+            ptrs[kind * nt + ti] = t.data_ptr() if t.numel() else 0
         return ptr_array(ptrs), len(ptrs)
 
     def offload(self, plan: Plan, shards, slab: Slab, stream=None) -> None:
-        arr, n = self._state_ptrs(plan, shards)
+        arr, n = self._state_ptrs(plan, shards, slab.rank)
         check(lib.plex_state_offload(self.h, plan.h, arr, n, slab.h, _stream_ptr(stream)))
 
     def onload(self, plan: Plan, slab: Slab, shards, stream=None) -> None:
-        arr, n = self._state_ptrs(plan, shards)
+        arr, n = self._state_ptrs(plan, shards, slab.rank)
         check(lib.plex_state_onload(self.h, plan.h, slab.h, arr, n, _stream_ptr(stream)))
 
     def switch(self, plan_out: Plan, shards_out, slab_out: Slab, plan_in: Plan, slab_in: Slab, shards_in,
                stream=None) -> None:
         """Duplex context switch: offload one job while onloading another (NEXT-1)."""
-        a, na = self._state_ptrs(plan_out, shards_out)
-        b, nb = self._state_ptrs(plan_in, shards_in)
+        a, na = self._state_ptrs(plan_out, shards_out, slab_out.rank)
+        b, nb = self._state_ptrs(plan_in, shards_in, slab_in.rank)
         check(lib.plex_state_switch(self.h, plan_out.h, a, na, slab_out.h, plan_in.h, slab_in.h, b, nb,
                                     _stream_ptr(stream)))
 
+    @staticmethod
+    def _check_masters(plan: Plan, masters: Sequence[torch.Tensor], rank: int) -> None:
+        if len(masters) != len(plan.manifest):
+            raise ValueError(f"{len(masters)} master shards, plan has {len(plan.manifest)} tensors")
+        numels = plan.shard_numels(rank)
+        for t, m in enumerate(masters):
+            want = numels[t]
+            if not m.is_contiguous() or m.element_size() != 4 or m.numel() != want:
+                raise ValueError(f"master shard {plan.manifest[t][0]}: need {want} contiguous fp32 elements")
+
+    @staticmethod
+    def _check_arena(plan: Plan, arena: torch.Tensor, rank: int) -> None:
+        need = plan.rank_info(rank).dst_arena_bytes
+        if not arena.is_cuda or arena.numel() * arena.element_size() < need:
+            raise ValueError(f"rollout arena of rank {rank} needs {need} device bytes")
+
     def sync(self, plan: Plan, masters: Sequence[torch.Tensor], arena: torch.Tensor, stream=None) -> None:
+        self._check_masters(plan, masters, self.rank)
+        self._check_arena(plan, arena, self.rank)
         arr = ptr_array([m.data_ptr() if m.numel() else 0 for m in masters])
         check(lib.plex_weight_sync(self.h, plan.h, arr, len(masters), arena.data_ptr(), _stream_ptr(stream)))
 
     def sync_rank(self, plan: Plan, rank: int, masters: Sequence[torch.Tensor], arenas: Sequence[torch.Tensor],
                   stream=None) -> None:
+        self._check_masters(plan, masters, rank)
+        for g, a in enumerate(arenas):
+            self._check_arena(plan, a, g)
         arr = ptr_array([m.data_ptr() if m.numel() else 0 for m in masters])
         ar = ptr_array([a.data_ptr() for a in arenas])
         check(lib.plex_weight_sync_rank(self.h, plan.h, rank, arr, len(masters), ar, len(arenas),
@@ -364,10 +404,13 @@ class StateManager:
 
     def sync_from_slab(self, plan: Plan, slab: Slab, arena: torch.Tensor, stream=None) -> None:
         """NEXT-3: sync a suspended job straight from its pinned slab."""
+        self._check_arena(plan, arena, self.rank)
         check(lib.plex_weight_sync_from_slab(self.h, plan.h, slab.h, arena.data_ptr(), _stream_ptr(stream)))
 
     def sync_rank_from_slab(self, plan: Plan, rank: int, slab: Slab, arenas: Sequence[torch.Tensor],
                             stream=None) -> None:
+        for g, a in enumerate(arenas):
+            self._check_arena(plan, a, g)
         ar = ptr_array([a.data_ptr() for a in arenas])
         check(lib.plex_weight_sync_rank_from_slab(self.h, plan.h, rank, slab.h, ar, len(arenas), _stream_ptr(stream)))
 
