@@ -416,3 +416,28 @@ def test_slab_nvme_tier(tmp_path):
         job.resume()
     assert e.value.code == L.E_CHECKSUM
     m.close()
+
+
+def test_binding_rejects_mis_sized_tensors():
+    """A wrong-size / wrong-dtype / non-contiguous shard or arena is refused by
+    the binding before any kernel could write out of bounds."""
+    man = manifest("mid")
+    plan = P.Plan(man, head_dim=32, world=2, tp=2, dp=1, bucket_bytes=1 << 16)
+    m = mgr(2, 0, bucket=1 << 16)
+    sh = rank_shards(plan, 0, seed=1)
+    slab = P.Slab(plan, 0)
+    key = man[3][0]
+    bad = dict(sh)
+    bad[(key, 1)] = torch.empty(sh[(key, 1)].numel() + 1, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        m.offload(plan, bad, slab)
+    bad[(key, 1)] = sh[(key, 1)].to(torch.float16) if sh[(key, 1)].numel() else sh[(key, 1)]
+    with pytest.raises(ValueError):
+        m.offload(plan, bad, slab)
+    assert slab.residency == L.RES_DEVICE                      # nothing happened
+    masters = [sh[(k, 1)] for k, _ in man]
+    small = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        m.sync_rank(plan, 0, masters, [small, small])
+    with pytest.raises(ValueError):
+        m.sync_rank(plan, 0, masters[:-1], [m.arena(plan, 0), m.arena(plan, 1)])
