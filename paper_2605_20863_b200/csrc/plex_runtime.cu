@@ -18,11 +18,14 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <set>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "plex_internal.h"
 
@@ -288,6 +291,13 @@ struct DeviceGuard {
         cudaGetDevice(&cur);
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
     }
+};
+
+// NVTX range around every exported transfer so nsys timelines show the
+// a3-a12 phases next to the copy-engine rows and kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
@@ -824,6 +834,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
     if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_offload");
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
     Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
@@ -854,6 +865,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     }
     if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier: plex_slab_fill first"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_onload");
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst)) ||
         (st = get_devplan(c, plan->p, &h.d)))
@@ -900,6 +912,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         return PLEX_E_INVAL;
     }
     DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_switch");
     const bool do_off = slab_out->residency == PLEX_RES_DEVICE;
     const bool do_on = slab_in->residency == PLEX_RES_HOST;
     Half ho{&plan_out->p, &plan_out->p.ranks[c->rank], nullptr, slab_out, 0, {}, false, 0, nullptr, nullptr, nullptr};
@@ -924,8 +937,10 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     // Each half has its own kernel stream: on one shared stream a pack waiting
     // for its D2H slot would hold back the other direction's unpack (and with
     // it the H2D ring), lock-stepping the two directions of the host link.
+    static int serial = -1;    // experiment knob: both halves' kernels on one stream
+    if (serial < 0) { const char* v = getenv("PLEX_DUPLEX_SERIAL"); serial = v ? atoi(v) : 0; }
     Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
-            c->ev_copy2.data(), c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1};
+            c->ev_copy2.data(), serial ? c->pack : c->pack2, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->pack2, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
@@ -1075,6 +1090,7 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
     if (!dst_arena && p.ranks[c->rank].arena_bytes) { set_error("NULL arena"); return PLEX_E_INVAL; }
     if (c->world > 1 && !c->comm) { set_error("world > 1 needs a ctx created with an NCCL id"); return PLEX_E_INVAL; }
     DeviceGuard g(c->device);
+    NvtxRange nv("plex_weight_sync");
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     if (c->flags & PLEX_CTX_SYNC_NCCL) return nccl_sync(c, p, src_master, dst_arena, caller);
     DevPlan* d;
