@@ -171,6 +171,82 @@ def scen_elide(a, c: Ctx):
            a.out)
 
 
+def scen_hrrs(a, c: Ctx):
+    """NEXT-4: drain one queue of RLVR requests from 4 jobs time-slicing the
+    GPU group, FCFS vs HRRS (Alg. 1 / Eq. 3-4) ordering.  Context switches and
+    weight syncs are real (this library); a request's compute phase is modeled
+    as a host-side wait of its Table-2 duration scaled by
+    --time-scale.  HRRS gets C_setup = T_offload + T_load as measured by the
+    library on the first switches (Setup.from_stats)."""
+    import random
+
+    from paper_2605_20863_b200.scheduler import Req, Setup, priority
+    models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    plans, jobs, arenas = [], [], []
+    for j, mo in enumerate(models):
+        tp = 1 if mo == "qwen2.5-0.5b" or c.world == 1 else 2
+        pl = mgr.plan(manifest(mo), head_dim=MODELS[mo].head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO)
+        plans.append(pl)
+        jb = P.Job(mgr, pl, seed=j).alloc().init_synthetic()
+        jb.suspend()
+        jobs.append(jb)
+        arenas.append(mgr.arena(pl))
+    # Table 2 phases (s): compute_log_prob, update_actor, sync_weight of the 7B job;
+    # smaller jobs scale with parameter count
+    base = {"log_prob": 9.66, "update": 38.08, "sync": 9.76}
+    psize = [plans[j].stats().total_params / plans[3].stats().total_params for j in range(4)]
+    rng = random.Random(0)
+    reqs = []
+    for j in range(4):
+        for cyc in range(a.rounds):
+            for k, (kind, sec) in enumerate(base.items()):
+                reqs.append(Req(j, rng.uniform(0, 1.0) + cyc + 0.01 * k, sec * psize[j] * a.time_scale, name=kind))
+    reqs.sort(key=lambda r: r.arrival)
+
+    def run(policy: str, setup: Setup):
+        resident = None
+        t0 = time.perf_counter()
+        pending = list(reqs)
+        switches = 0
+        waits = []
+        while pending:
+            now = time.perf_counter() - t0 + 1.0          # every request has arrived by t = 1
+            if policy == "fcfs":
+                r = pending[0]
+            else:
+                cur = Req(resident, 0.0, 1e-9, remaining=1e-9) if resident is not None else None
+                r = max(pending, key=lambda q: priority(q, now, cur, setup))
+            pending.remove(r)
+            waits.append(now - r.arrival)
+            if r.job != resident:
+                if resident is None:
+                    jobs[r.job].resume()
+                else:
+                    jobs[resident].switch_to(jobs[r.job])
+                resident = r.job
+                switches += 1
+            if r.name == "sync":
+                jobs[r.job].sync(arenas[r.job])
+            torch.cuda.synchronize()
+            time.sleep(r.exec_time)                       # the request's own compute phase (modeled)
+        jobs[resident].suspend()
+        return time.perf_counter() - t0, switches, sum(waits) / len(waits)
+
+    mgr.reset_stats()
+    t_fcfs, n_fcfs, w_fcfs = run("fcfs", Setup(0.0, 0.0))
+    st = mgr.stats()
+    setup = Setup.from_stats(st, n_fcfs, n_fcfs, duplex=True,
+                             job_bytes={j: plans[j].rank_info(c.rank).payload_bytes for j in range(4)})
+    t_hrrs, n_hrrs, w_hrrs = run("hrrs", setup)
+    c.emit({"scenario": "hrrs", "jobs": models, "n_gpus": c.world, "requests": len(reqs),
+            "time_scale": a.time_scale,
+            "measured_host_link_GBs": {"d2h": round(setup.bw_out / 1e9, 2), "h2d": round(setup.bw_in / 1e9, 2)},
+            "fcfs": {"makespan_s": round(c.allmax(t_fcfs), 3), "switches": n_fcfs, "mean_wait_s": round(w_fcfs, 3)},
+            "hrrs": {"makespan_s": round(c.allmax(t_hrrs), 3), "switches": n_hrrs, "mean_wait_s": round(w_hrrs, 3)}},
+           a.out)
+
+
 def scen_optim(a, c: Ctx):
     # each process = rank c.rank of an FSDP-8 plan; k = world processes copy at once
     W = 8
@@ -285,7 +361,8 @@ def scen_multiplex(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs"])
+    ap.add_argument("--time-scale", type=float, default=0.005)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
@@ -301,7 +378,7 @@ def main():
     if not a.model:
         a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
-     "multiplex": scen_multiplex}[a.scenario](a, c)
+     "multiplex": scen_multiplex, "hrrs": scen_hrrs}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
