@@ -304,6 +304,30 @@ PLEX_API plex_status plex_state_offload(plex_ctx_t ctx, plex_plan_t plan, const 
 PLEX_API plex_status plex_state_onload(plex_ctx_t ctx, plex_plan_t plan, plex_slab_t slab, void* const* dst,
                               int32_t n_dst, void* caller_stream);
 
+/* ---- NEXT-1: scheduler-directed prefetch and asynchronous drain ------------ */
+/* PAPER.md:506 ("when an upcoming context switch is predicted, StateManager
+ * can proactively move state upward in the hierarchy") and :513 ("state can be
+ * prefetched or drained across the memory hierarchy asynchronously", keeping
+ * only operations on the active deployment on the critical path).
+ * plex_state_drain = plex_state_offload and plex_state_prefetch =
+ * plex_state_onload, except that they return as soon as the transfer is
+ * enqueued on library-owned side streams (ordered after prior work on
+ * caller_stream) so the caller keeps computing; the source (drain) / the
+ * destination (prefetch) must not be touched until plex_state_wait.  One drain
+ * and one prefetch may be in flight per ctx (they use the two staging halves:
+ * staging >= 2 x n_slots x bucket); blocking state transfers on the ctx return
+ * E_STATE meanwhile, plex_weight_sync does not.  plex_state_wait(op =
+ * PLEX_OP_OFFLOAD | PLEX_OP_ONLOAD) host-blocks until that transfer is done,
+ * makes caller_stream wait on it, and flips residency (prefetch: verifies the
+ * R14 checksums first, E_CHECKSUM leaves the slab HOST); a no-op if nothing is
+ * in flight.  plex_state_poll sets *done without blocking. */
+PLEX_API plex_status plex_state_drain(plex_ctx_t ctx, plex_plan_t plan, const void* const* src, int32_t n_src,
+                                      plex_slab_t slab, void* caller_stream);
+PLEX_API plex_status plex_state_prefetch(plex_ctx_t ctx, plex_plan_t plan, plex_slab_t slab, void* const* dst,
+                                         int32_t n_dst, void* caller_stream);
+PLEX_API plex_status plex_state_wait(plex_ctx_t ctx, int32_t op, void* caller_stream);
+PLEX_API plex_status plex_state_poll(plex_ctx_t ctx, int32_t op, int32_t* done);
+
 /* ---- NEXT-1: duplex switch (offload A || onload B) ------------------------ */
 /* The context switch of PAPER.md:555 (OFFLOAD resident A, ONLOAD incoming B)
  * as one call whose two halves run concurrently: A's buckets go D2H on

@@ -36,7 +36,8 @@ EXPORTS = [
     "plex_ctx_trace",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_slab_spill", "plex_slab_fill",
-    "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync", "plex_weight_sync_rank",
+    "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync",
+    "plex_state_drain", "plex_state_prefetch", "plex_state_wait", "plex_state_poll", "plex_weight_sync_rank",
     "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
@@ -126,6 +127,10 @@ def _load() -> C.CDLL:
         "plex_state_offload": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_state_onload": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),
         "plex_state_switch": (C.c_int, [VP, VP, P(VP), I32, VP, VP, VP, P(VP), I32, VP]),
+        "plex_state_drain": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
+        "plex_state_prefetch": (C.c_int, [VP, VP, VP, P(VP), I32, VP]),
+        "plex_state_wait": (C.c_int, [VP, I32, VP]),
+        "plex_state_poll": (C.c_int, [VP, I32, P(I32)]),
         "plex_weight_sync": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_weight_sync_rank": (C.c_int, [VP, VP, I32, P(VP), I32, P(VP), I32, VP]),
         "plex_weight_sync_from_slab": (C.c_int, [VP, VP, VP, VP, VP]),

@@ -97,6 +97,8 @@ struct Timed {
     cudaEvent_t a, b;
 };
 
+struct AsyncState;   // an in-flight plex_state_drain / plex_state_prefetch
+
 }  // namespace plex
 
 using namespace plex;
@@ -127,6 +129,13 @@ struct plex_ctx_s {
     uint64_t* d_ptrs2 = nullptr;
     size_t ptr_cap2 = 0;
     cudaStream_t copy2 = nullptr;       // library-owned H2D stream of a duplex switch, created lazily
+    // NEXT-1 async prefetch / drain: own kernel stream, D2H stream, ring events, pointer table
+    cudaStream_t kasync = nullptr, copy3 = nullptr;
+    std::vector<cudaEvent_t> ev_pack3, ev_copy3;
+    uint64_t* h_ptrs3 = nullptr;
+    uint64_t* d_ptrs3 = nullptr;
+    size_t ptr_cap3 = 0;
+    AsyncState* async[2] = {nullptr, nullptr};   // [0] drain (offload), [1] prefetch (onload)
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
@@ -154,6 +163,7 @@ struct plex_slab_s {
     int residency = PLEX_RES_DEVICE;
     bool written = false;
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
+    bool busy = false;                  // an async drain / prefetch of this slab is in flight
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
 };
 
@@ -330,10 +340,11 @@ static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* con
         set_error("expected %zu pointers (4 kinds x %zu tensors), got %d", PLEX_NUM_KINDS * nt, nt, n);
         return PLEX_E_INVAL;
     }
-    plex_status s = table == 0 ? ensure_ptrs(c, PLEX_NUM_KINDS * nt)
-                               : ensure_table(&c->h_ptrs2, &c->d_ptrs2, &c->ptr_cap2, PLEX_NUM_KINDS * nt);
+    plex_status s = table == 0   ? ensure_ptrs(c, PLEX_NUM_KINDS * nt)
+                    : table == 1 ? ensure_table(&c->h_ptrs2, &c->d_ptrs2, &c->ptr_cap2, PLEX_NUM_KINDS * nt)
+                                 : ensure_table(&c->h_ptrs3, &c->d_ptrs3, &c->ptr_cap3, PLEX_NUM_KINDS * nt);
     if (s) return s;
-    uint64_t* h = table == 0 ? c->h_ptrs : c->h_ptrs2;
+    uint64_t* h = table == 0 ? c->h_ptrs : table == 1 ? c->h_ptrs2 : c->h_ptrs3;
     const RankPlan& R = p.ranks[c->rank];
     for (size_t i = 0; i < PLEX_NUM_KINDS * nt; ++i) h[i] = reinterpret_cast<uint64_t>(ptrs[i]);
     for (const SegDev& sg : R.segs) {
@@ -358,7 +369,17 @@ struct Pipe {
     uint64_t* h_ptrs;
     uint64_t* d_ptrs;
     unsigned int* ctr;      // per-launch work counter of the pack/unpack kernel
+    int* d_flag;            // elision check / checksum verify result (device)
+    int* h_flag;            // ... and its pinned host mirror
+    bool untimed = false;   // async ops do not record per-launch events
 };
+
+static plex_status tbeg(plex_ctx_s* c, const Pipe& pp, cudaStream_t s, cudaEvent_t* a) {
+    return pp.untimed ? PLEX_OK : timed_begin(c, s, a);
+}
+static plex_status tend(plex_ctx_s* c, const Pipe& pp, cudaStream_t s, cudaEvent_t a, int which, uint64_t bytes) {
+    return pp.untimed ? PLEX_OK : timed_end(c, s, a, which, bytes);
+}
 
 struct Half {           // one offload or onload in flight
     const Plan* p;
@@ -402,16 +423,16 @@ static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     use_grid(h, false);
     if (h.R->elide_start) {
         // NEXT-2: does every bf16 param equal RNE(master)?  (checksums the params)
-        CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
+        CK(cudaMemsetAsync(pp.d_flag, 0, sizeof(int), pp.kern));
         cudaEvent_t ta = nullptr;
         plex_status st;
-        if ((st = timed_begin(c, pp.kern, &ta))) return st;
+        if ((st = tbeg(c, pp, pp.kern, &ta))) return st;
         CK(launch_derive(true, h.d->items, (uint32_t)h.R->n_param_items, h.d->segs, pp.d_ptrs,
-                         (uint32_t)h.p->tensors.size(), h.d->cks, c->d_flag, pp.kern));
-        if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
-        CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
+                         (uint32_t)h.p->tensors.size(), h.d->cks, pp.d_flag, pp.kern));
+        if ((st = tend(c, pp, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
+        CK(cudaMemcpyAsync(pp.h_flag, pp.d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
         CK(cudaStreamSynchronize(pp.kern));
-        if (*c->h_flag == 0) use_grid(h, true);
+        if (*pp.h_flag == 0) use_grid(h, true);
         else CK(cudaMemsetAsync(h.d->cks, 0, ckb, pp.kern));    // full offload after all
     }
     return PLEX_OK;
@@ -428,15 +449,15 @@ static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     const uint64_t i0 = h.bstart[b], i1 = h.bstart[b + 1];
     cudaEvent_t ta = nullptr;
     plex_status st;
-    if ((st = timed_begin(c, pp.kern, &ta))) return st;
+    if ((st = tbeg(c, pp, pp.kern, &ta))) return st;
     CK(launch_pack(true, h.grid_items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks, pp.ctr,
                    pp.kern));
-    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_PACK, 2 * h.payload[b]))) return st;
+    if ((st = tend(c, pp, pp.kern, ta, PLEX_STAT_PACK, 2 * h.payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
-    if ((st = timed_begin(c, pp.copy, &ta))) return st;
+    if ((st = tbeg(c, pp, pp.copy, &ta))) return st;
     CK(cudaMemcpyAsync(h.slab->host + lo, stg, len, cudaMemcpyDeviceToHost, pp.copy));
-    if ((st = timed_end(c, pp.copy, ta, PLEX_STAT_D2H, len))) return st;
+    if ((st = tend(c, pp, pp.copy, ta, PLEX_STAT_D2H, len))) return st;
     CK(cudaEventRecord(pp.ev_c[slot], pp.copy));
     return PLEX_OK;
 }
@@ -453,7 +474,7 @@ static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
     CK(cudaMemsetAsync(h.d->cks_in, 0, 8 * std::max<size_t>(2, nck), pp.kern));
     if (nck) CK(cudaMemcpyAsync(h.d->cks_want, h.slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, pp.kern));
-    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), pp.kern));
+    CK(cudaMemsetAsync(pp.d_flag, 0, sizeof(int), pp.kern));
     use_grid(h, h.slab->elided);
     return PLEX_OK;
 }
@@ -468,16 +489,16 @@ static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     if (b >= pp.n_slots) CK(cudaStreamWaitEvent(pp.copy, pp.ev_k[slot], 0));
     cudaEvent_t ta = nullptr;
     plex_status st;
-    if ((st = timed_begin(c, pp.copy, &ta))) return st;
+    if ((st = tbeg(c, pp, pp.copy, &ta))) return st;
     CK(cudaMemcpyAsync(stg, h.slab->host + lo, len, cudaMemcpyHostToDevice, pp.copy));
-    if ((st = timed_end(c, pp.copy, ta, PLEX_STAT_H2D, len))) return st;
+    if ((st = tend(c, pp, pp.copy, ta, PLEX_STAT_H2D, len))) return st;
     CK(cudaEventRecord(pp.ev_c[slot], pp.copy));
     CK(cudaStreamWaitEvent(pp.kern, pp.ev_c[slot], 0));
     const uint64_t i0 = h.bstart[b], i1 = h.bstart[b + 1];
-    if ((st = timed_begin(c, pp.kern, &ta))) return st;
+    if ((st = tbeg(c, pp, pp.kern, &ta))) return st;
     CK(launch_pack(false, h.grid_items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, stg, lo, h.d->cks_in, pp.ctr,
                    pp.kern));
-    if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.payload[b]))) return st;
+    if ((st = tend(c, pp, pp.kern, ta, PLEX_STAT_UNPACK, 2 * h.payload[b]))) return st;
     CK(cudaEventRecord(pp.ev_k[slot], pp.kern));
     return PLEX_OK;
 }
@@ -486,13 +507,13 @@ static plex_status on_end(plex_ctx_s* c, Pipe& pp, Half& h) {
     if (h.elide) {   // NEXT-2: re-derive the elided params from the restored master
         cudaEvent_t ta = nullptr;
         plex_status st;
-        if ((st = timed_begin(c, pp.kern, &ta))) return st;
+        if ((st = tbeg(c, pp, pp.kern, &ta))) return st;
         CK(launch_derive(false, h.d->items, (uint32_t)h.R->n_param_items, h.d->segs, pp.d_ptrs,
-                         (uint32_t)h.p->tensors.size(), h.d->cks_in, c->d_flag, pp.kern));
-        if ((st = timed_end(c, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
+                         (uint32_t)h.p->tensors.size(), h.d->cks_in, pp.d_flag, pp.kern));
+        if ((st = tend(c, pp, pp.kern, ta, PLEX_STAT_DERIVE, 3 * h.d->elide_payload))) return st;
     }
-    CK(launch_verify(h.d->cks_in, h.d->cks_want, (uint32_t)h.R->segs.size(), c->d_flag, pp.kern));
-    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
+    CK(launch_verify(h.d->cks_in, h.d->cks_want, (uint32_t)h.R->segs.size(), pp.d_flag, pp.kern));
+    CK(cudaMemcpyAsync(pp.h_flag, pp.d_flag, sizeof(int), cudaMemcpyDeviceToHost, pp.kern));
     return PLEX_OK;
 }
 
@@ -500,6 +521,30 @@ static plex_status check_slab(plex_ctx_s* c, plex_plan_t plan, plex_slab_t slab)
     if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) {
         set_error("slab does not belong to this plan/rank");
         return PLEX_E_INVAL;
+    }
+    if (slab->busy) { set_error("an async transfer of this slab is in flight: plex_state_wait first"); return PLEX_E_STATE; }
+    return PLEX_OK;
+}
+
+struct AsyncState {
+    Half h;
+    Pipe pp;
+    plex_slab_s* slab = nullptr;
+    cudaEvent_t done_k = nullptr, done_c = nullptr;
+};
+
+static void async_free(AsyncState* a) {
+    if (!a) return;
+    if (a->done_k) cudaEventDestroy(a->done_k);
+    if (a->done_c) cudaEventDestroy(a->done_c);
+    delete a;
+}
+
+// Blocking state transfers use the rings the async ones run on.
+static plex_status check_no_async(plex_ctx_s* c) {
+    if (c->async[0] || c->async[1]) {
+        set_error("async drain/prefetch in flight on this ctx: plex_state_wait first");
+        return PLEX_E_STATE;
     }
     return PLEX_OK;
 }
@@ -597,6 +642,11 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     if (c->pack) cudaStreamSynchronize(c->pack);
     if (c->copy) cudaStreamSynchronize(c->copy);
     if (c->copy2) cudaStreamSynchronize(c->copy2);
+    if (c->kasync) cudaStreamSynchronize(c->kasync);
+    if (c->copy3) cudaStreamSynchronize(c->copy3);
+    for (auto& a : c->async) {
+        if (a) { a->slab->busy = false; async_free(a); a = nullptr; }
+    }
     for (auto& kv : c->dev) free_devplan(kv.second);
     for (auto& kv : c->peers)
         if (kv.second.second) cudaIpcCloseMemHandle(kv.second.second);
@@ -615,6 +665,12 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     for (cudaEvent_t e : c->ev_pack2) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy2) cudaEventDestroy(e);
     if (c->copy2) cudaStreamDestroy(c->copy2);
+    if (c->kasync) cudaStreamDestroy(c->kasync);
+    if (c->copy3) cudaStreamDestroy(c->copy3);
+    for (cudaEvent_t e : c->ev_pack3) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_copy3) cudaEventDestroy(e);
+    cudaFreeHost(c->h_ptrs3);
+    cudaFree(c->d_ptrs3);
     cudaFreeHost(c->h_flag);
     cudaFree(c->d_flag);
     cudaFree(c->d_ctr);
@@ -774,7 +830,7 @@ static plex_status pio(bool write, int fd, uint8_t* buf, size_t n, int threads) 
 
 plex_status plex_slab_spill(plex_slab_t s, const char* path, int32_t threads) {
     if (!s || !path) { set_error("NULL slab/path"); return PLEX_E_INVAL; }
-    if (s->residency != PLEX_RES_HOST || !s->host) { set_error("spill needs a HOST-resident slab"); return PLEX_E_STATE; }
+    if (s->residency != PLEX_RES_HOST || !s->host || s->busy) { set_error("spill needs a HOST-resident, idle slab"); return PLEX_E_STATE; }
     const size_t n = align_up(std::max<uint64_t>(s->bytes, 1), 4096);
     int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | O_DIRECT, 0600);
     if (fd < 0) { set_error("open(%s, O_DIRECT): %s", path, strerror(errno)); return PLEX_E_INVAL; }
@@ -828,7 +884,7 @@ plex_status plex_slab_checksums(plex_slab_t s, uint64_t* out, int32_t n) {
 plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
                                void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st || (st = check_slab(c, plan, slab))) return st;
+    if (st || (st = check_slab(c, plan, slab)) || (st = check_no_async(c))) return st;
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
     if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
@@ -836,7 +892,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     Half h{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
     if ((st = fill_state_ptrs(c, plan->p, src, n_src)) || (st = get_devplan(c, plan->p, &h.d))) return st;
     Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
-            c->d_ctr};
+            c->d_ctr, c->d_flag, c->h_flag};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
@@ -856,7 +912,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
 plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, void* const* dst, int32_t n_dst,
                               void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st || (st = check_slab(c, plan, slab))) return st;
+    if (st || (st = check_slab(c, plan, slab)) || (st = check_no_async(c))) return st;
     if (slab->residency == PLEX_RES_DEVICE) {
         if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
         return PLEX_OK;                                     // idempotent
@@ -869,7 +925,7 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
         (st = get_devplan(c, plan->p, &h.d)))
         return st;
     Pipe pp{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
-            c->d_ctr};
+            c->d_ctr, c->d_flag, c->h_flag};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
@@ -878,8 +934,8 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     for (int32_t b = 0; b < h.nb; ++b)
         if ((st = on_bucket(c, pp, h, b))) return st;
     if ((st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
-    if (*c->h_flag) {
-        set_error("onload: %d segment checksum(s) differ from offload", *c->h_flag);
+    if (*pp.h_flag) {
+        set_error("onload: %d segment checksum(s) differ from offload", *pp.h_flag);
         return PLEX_E_CHECKSUM;
     }
     slab->residency = PLEX_RES_DEVICE;
@@ -897,7 +953,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
                               int32_t n_dst, void* caller_stream) {
     plex_status st = check_common(c, plan_out);
     if (st || (st = check_common(c, plan_in)) || (st = check_slab(c, plan_out, slab_out)) ||
-        (st = check_slab(c, plan_in, slab_in)))
+        (st = check_slab(c, plan_in, slab_in)) || (st = check_no_async(c)))
         return st;
     if (slab_out == slab_in) { set_error("switch needs two different slabs"); return PLEX_E_INVAL; }
     if (slab_in->residency == PLEX_RES_DEVICE && !slab_in->written) {
@@ -930,7 +986,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         }
     }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
-            c->d_ctr};
+            c->d_ctr, c->d_flag + 2, c->h_flag + 2};
     // Both halves' kernels share the pack stream.  The two rings run at the
     // host link's pace and would otherwise launch their pack/unpack kernels at
     // the same moments (phase-locked), halving each kernel's SMs; serialised,
@@ -938,7 +994,8 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     // copy time the coupling costs nothing (measured: 1545-1574 vs 1584-1612 ms
     // per 7B N=2 step, kernels at 0.94-0.96 vs 0.87-0.89 of HBM).
     Pipe pi{c->staging + (uint64_t)c->n_slots * plan_out->p.bucket, c->n_slots, c->ev_pack2.data(),
-            c->ev_copy2.data(), c->pack, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1};
+            c->ev_copy2.data(), c->pack, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1, c->d_flag + 1,
+            c->h_flag + 1};
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
@@ -962,13 +1019,196 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
         slab_out->elided = ho.elide;
     }
     if (do_on) {
-        if (*c->h_flag) {
-            set_error("switch onload: %d segment checksum(s) differ from offload", *c->h_flag);
+        if (*pi.h_flag) {
+            set_error("switch onload: %d segment checksum(s) differ from offload", *pi.h_flag);
             return PLEX_E_CHECKSUM;
         }
         slab_in->residency = PLEX_RES_DEVICE;
     }
     return PLEX_OK;
+}
+
+// ---- NEXT-1: scheduler-directed prefetch and asynchronous drain -----------------------
+// PAPER.md:506 "when an upcoming context switch is predicted, StateManager can
+// proactively move state upward in the hierarchy before the corresponding
+// deployment becomes active"; :513 "state can be prefetched or drained across
+// the memory hierarchy asynchronously", keeping "only operations that directly
+// access or mutate the active GPU-resident deployment" on the critical path.
+// A drain (offload) / prefetch (onload) is enqueued on library-owned side
+// streams and returns at once; the caller keeps computing; plex_state_wait
+// completes it (verify, residency flip, caller-stream ordering).
+}  // extern "C"
+
+namespace plex {
+static plex_status async_resources(plex_ctx_s* c) {
+    if (!c->kasync) CK(cudaStreamCreateWithFlags(&c->kasync, cudaStreamNonBlocking));
+    if (!c->copy2) CK(cudaStreamCreateWithFlags(&c->copy2, cudaStreamNonBlocking));
+    if (!c->copy3) CK(cudaStreamCreateWithFlags(&c->copy3, cudaStreamNonBlocking));
+    auto mk = [&](std::vector<cudaEvent_t>& v) -> plex_status {
+        if (!v.empty()) return PLEX_OK;
+        v.resize(c->n_slots);
+        for (auto& e : v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return PLEX_OK;
+    };
+    plex_status st;
+    if ((st = mk(c->ev_pack2)) || (st = mk(c->ev_copy2)) || (st = mk(c->ev_pack3)) || (st = mk(c->ev_copy3))) return st;
+    return PLEX_OK;
+}
+
+}  // namespace plex
+
+extern "C" {
+
+plex_status plex_state_drain(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
+                             void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st || (st = check_slab(c, plan, slab))) return st;
+    if (c->async[0]) { set_error("a drain is already in flight"); return PLEX_E_STATE; }
+    if (slab->residency != PLEX_RES_DEVICE) return PLEX_OK;      // already offloaded: nothing to drain
+    if ((uint64_t)c->n_slots * plan->p.bucket > c->staging_bytes / 2) {
+        set_error("async transfers need staging >= 2 x n_slots x bucket");
+        return PLEX_E_INVAL;
+    }
+    DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_drain");
+    if ((st = async_resources(c)) || (st = fill_state_ptrs(c, plan->p, src, n_src, 2))) return st;
+    auto* a = new AsyncState();
+    a->h = Half{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
+    a->pp = Pipe{c->staging, c->n_slots, c->ev_pack3.data(), c->ev_copy3.data(), c->kasync, c->copy3, c->h_ptrs3,
+                 c->d_ptrs3, c->d_ctr + 2, c->d_flag + 3, c->h_flag + 3, true};
+    a->slab = slab;
+    auto fail = [&](plex_status e) { async_free(a); return e; };
+    if ((st = get_devplan(c, plan->p, &a->h.d))) return fail(st);
+    if (cudaEventCreateWithFlags(&a->done_k, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a->done_c, cudaEventDisableTiming) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("cudaEventCreate failed");
+        return fail(PLEX_E_CUDA);
+    }
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    if (cudaEventRecord(c->ev_caller, caller) != cudaSuccess ||
+        cudaStreamWaitEvent(c->kasync, c->ev_caller, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(c->copy3, c->ev_caller, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("drain: stream ordering failed");
+        return fail(PLEX_E_CUDA);
+    }
+    if ((st = off_begin(c, a->pp, a->h))) return fail(st);
+    for (int32_t b = 0; b < a->h.nb; ++b)
+        if ((st = off_bucket(c, a->pp, a->h, b))) return fail(st);
+    if ((st = off_end(c, a->pp, a->h))) return fail(st);
+    if (cudaEventRecord(a->done_k, c->kasync) != cudaSuccess || cudaEventRecord(a->done_c, c->copy3) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("drain: event record failed");
+        return fail(PLEX_E_CUDA);
+    }
+    slab->busy = true;
+    c->async[0] = a;
+    return PLEX_OK;
+}
+
+plex_status plex_state_prefetch(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, void* const* dst, int32_t n_dst,
+                                void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st || (st = check_slab(c, plan, slab))) return st;
+    if (c->async[1]) { set_error("a prefetch is already in flight"); return PLEX_E_STATE; }
+    if (slab->residency == PLEX_RES_DEVICE) {
+        if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
+        return PLEX_OK;
+    }
+    if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier: plex_slab_fill first"); return PLEX_E_STATE; }
+    if ((uint64_t)c->n_slots * plan->p.bucket > c->staging_bytes / 2) {
+        set_error("async transfers need staging >= 2 x n_slots x bucket");
+        return PLEX_E_INVAL;
+    }
+    DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_prefetch");
+    if ((st = async_resources(c)) ||
+        (st = fill_state_ptrs(c, plan->p, reinterpret_cast<const void* const*>(dst), n_dst, 1)))
+        return st;
+    auto* a = new AsyncState();
+    a->h = Half{&plan->p, &plan->p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
+    a->pp = Pipe{c->staging + ((c->staging_bytes / 2) & ~255ull), c->n_slots, c->ev_pack2.data(), c->ev_copy2.data(),
+                 c->kasync, c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1, c->d_flag + 1, c->h_flag + 1, true};
+    a->slab = slab;
+    auto fail = [&](plex_status e) { async_free(a); return e; };
+    if ((st = get_devplan(c, plan->p, &a->h.d))) return fail(st);
+    if (cudaEventCreateWithFlags(&a->done_k, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&a->done_c, cudaEventDisableTiming) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("cudaEventCreate failed");
+        return fail(PLEX_E_CUDA);
+    }
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    if (cudaEventRecord(c->ev_caller, caller) != cudaSuccess ||
+        cudaStreamWaitEvent(c->kasync, c->ev_caller, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(c->copy2, c->ev_caller, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("prefetch: stream ordering failed");
+        return fail(PLEX_E_CUDA);
+    }
+    if ((st = on_begin(c, a->pp, a->h))) return fail(st);
+    for (int32_t b = 0; b < a->h.nb; ++b)
+        if ((st = on_bucket(c, a->pp, a->h, b))) return fail(st);
+    if ((st = on_end(c, a->pp, a->h))) return fail(st);
+    if (cudaEventRecord(a->done_k, c->kasync) != cudaSuccess || cudaEventRecord(a->done_c, c->copy2) != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("prefetch: event record failed");
+        return fail(PLEX_E_CUDA);
+    }
+    slab->busy = true;
+    c->async[1] = a;
+    return PLEX_OK;
+}
+
+plex_status plex_state_poll(plex_ctx_t c, int32_t op, int32_t* done) {
+    if (!c || !done || (op != PLEX_OP_OFFLOAD && op != PLEX_OP_ONLOAD)) { set_error("bad poll"); return PLEX_E_INVAL; }
+    AsyncState* a = c->async[op == PLEX_OP_OFFLOAD ? 0 : 1];
+    if (!a) { *done = 1; return PLEX_OK; }
+    DeviceGuard g(c->device);
+    const cudaError_t ek = cudaEventQuery(a->done_k), ec = cudaEventQuery(a->done_c);
+    if ((ek != cudaSuccess && ek != cudaErrorNotReady) || (ec != cudaSuccess && ec != cudaErrorNotReady)) {
+        (void)cudaGetLastError();
+        set_error("async transfer failed: %s", cudaGetErrorString(ek != cudaSuccess ? ek : ec));
+        return PLEX_E_CUDA;
+    }
+    *done = (ek == cudaSuccess && ec == cudaSuccess) ? 1 : 0;
+    return PLEX_OK;
+}
+
+plex_status plex_state_wait(plex_ctx_t c, int32_t op, void* caller_stream) {
+    if (!c || (op != PLEX_OP_OFFLOAD && op != PLEX_OP_ONLOAD)) { set_error("bad wait"); return PLEX_E_INVAL; }
+    const int k = op == PLEX_OP_OFFLOAD ? 0 : 1;
+    AsyncState* a = c->async[k];
+    if (!a) return PLEX_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    c->async[k] = nullptr;
+    a->slab->busy = false;
+    cudaError_t e = cudaEventSynchronize(a->done_k);
+    if (e == cudaSuccess) e = cudaEventSynchronize(a->done_c);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, a->done_k, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, a->done_c, 0);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        set_error("async transfer failed: %s", cudaGetErrorString(e));
+        async_free(a);
+        return PLEX_E_CUDA;
+    }
+    plex_status st = PLEX_OK;
+    if (k == 0) {
+        a->slab->cks.swap(a->h.cks);
+        a->slab->residency = PLEX_RES_HOST;
+        a->slab->written = true;
+        a->slab->elided = a->h.elide;
+    } else if (*a->pp.h_flag) {
+        set_error("prefetch: %d segment checksum(s) differ from offload", *a->pp.h_flag);
+        st = PLEX_E_CHECKSUM;                     // residency stays HOST
+    } else {
+        a->slab->residency = PLEX_RES_DEVICE;
+    }
+    async_free(a);
+    return st;
 }
 
 // ---- a8 - a11: weight sync -------------------------------------------------------------
@@ -1114,8 +1354,8 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
 // plex_weight_sync.
 static plex_status slab_master_ptrs(const Plan& p, plex_slab_t slab, std::vector<const void*>& src) {
     if (!slab || slab->plan_id != p.id) { set_error("slab does not belong to this plan"); return PLEX_E_INVAL; }
-    if (slab->residency != PLEX_RES_HOST || !slab->written) {
-        set_error("sync from slab needs HOST-resident offloaded state");
+    if (slab->residency != PLEX_RES_HOST || !slab->written || slab->busy) {
+        set_error("sync from slab needs HOST-resident offloaded state (and no transfer in flight)");
         return PLEX_E_STATE;
     }
     void* dev = nullptr;

@@ -386,6 +386,29 @@ class StateManager:
         if not arena.is_cuda or arena.numel() * arena.element_size() < need:
             raise ValueError(f"rollout arena of rank {rank} needs {need} device bytes")
 
+    # ---- NEXT-1 async prefetch / drain --------------------------------------------
+    def drain(self, plan: Plan, shards, slab: Slab, stream=None) -> None:
+        """Start an offload and return; complete it with wait(OP_OFFLOAD)."""
+        arr, n = self._state_ptrs(plan, shards, slab.rank)
+        self._keep = getattr(self, "_keep", {})
+        self._keep[L.OP_OFFLOAD] = arr
+        check(lib.plex_state_drain(self.h, plan.h, arr, n, slab.h, _stream_ptr(stream)))
+
+    def prefetch(self, plan: Plan, slab: Slab, shards, stream=None) -> None:
+        """Start an onload into (already allocated) shards and return."""
+        arr, n = self._state_ptrs(plan, shards, slab.rank)
+        self._keep = getattr(self, "_keep", {})
+        self._keep[L.OP_ONLOAD] = arr
+        check(lib.plex_state_prefetch(self.h, plan.h, slab.h, arr, n, _stream_ptr(stream)))
+
+    def wait(self, op: int, stream=None) -> None:
+        check(lib.plex_state_wait(self.h, op, _stream_ptr(stream)))
+
+    def poll(self, op: int) -> bool:
+        d = C.c_int32()
+        check(lib.plex_state_poll(self.h, op, C.byref(d)))
+        return bool(d.value)
+
     def sync(self, plan: Plan, masters: Sequence[torch.Tensor], arena: torch.Tensor, stream=None) -> None:
         self._check_masters(plan, masters, self.rank)
         self._check_arena(plan, arena, self.rank)
@@ -539,6 +562,23 @@ class Job:
     def resume(self, stream=None) -> None:
         self.acquire()
         self.mgr.onload(self.plan, self.slab, self.slab_shards(), stream)
+
+    def prefetch(self, stream=None) -> None:
+        """NEXT-1: start bringing this (HOST-resident) job back; returns at once."""
+        self.acquire()
+        self.mgr.prefetch(self.plan, self.slab, self.slab_shards(), stream)
+
+    def drain(self, stream=None) -> None:
+        """NEXT-1: start offloading this job; returns at once (finish with wait_drain)."""
+        self.mgr.drain(self.plan, self.slab_shards(), self.slab, stream)
+
+    def wait_prefetch(self, stream=None) -> None:
+        self.mgr.wait(L.OP_ONLOAD, stream)
+
+    def wait_drain(self, stream=None, release: bool = True) -> None:
+        self.mgr.wait(L.OP_OFFLOAD, stream)
+        if release:
+            self.release()
 
     def switch_to(self, other: "Job", stream=None, release: bool = True) -> None:
         """PAPER.md:555 context switch self -> other with both host-link

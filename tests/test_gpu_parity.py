@@ -441,3 +441,64 @@ def test_binding_rejects_mis_sized_tensors():
         m.sync_rank(plan, 0, masters, [small, small])
     with pytest.raises(ValueError):
         m.sync_rank(plan, 0, masters[:-1], [m.arena(plan, 0), m.arena(plan, 1)])
+
+
+# ---- NEXT-1 async prefetch / drain ---------------------------------------------------------------
+@pytest.mark.parametrize("elide", [False, True])
+def test_async_prefetch_and_drain(elide):
+    """B is prefetched while A keeps computing, then A is drained while B
+    computes and syncs; both end bit-identical to the oracle's replay."""
+    W, r = 2, 1
+    models = ("mid", "mid-moe")
+    plans = [P.Plan(manifest(mo), head_dim=MODELS[mo].head_dim, world=W, tp=2, dp=1, ep=2 if "moe" in mo else 1,
+                    bucket_bytes=1 << 14, tile_bytes=1024, elide_param=elide) for mo in models]
+    m = mgr(W, r, bucket=1 << 14)
+    a = P.Job(m, plans[0], seed=70, rank=r).alloc().init_synthetic(special_bits=3, derived_param=elide)
+    b = P.Job(m, plans[1], seed=71, rank=r).alloc().init_synthetic(special_bits=3, derived_param=elide)
+    b.suspend()
+    # while B's state comes back, A "trains": one mutation step on every shard
+    b.prefetch()
+    with pytest.raises(P.PlexError) as e:              # blocking transfers must wait for the async one
+        a.suspend()
+    assert e.value.code == L.E_STATE
+    for t, (key, shape) in enumerate(plans[0].manifest):
+        a0, _ = plans[0].shard_rows(r, t)
+        re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        for kd in range(4):
+            if not elide or kd != 0:
+                P.synth_mutate(a.shards[(key, kd)], kd, 70, 0, key, a0 * re_)
+    if elide:                                           # keep params == RNE(master)
+        for key, _ in plans[0].manifest:
+            if a.shards[(key, 0)].numel():
+                P.cast_rne(a.shards[(key, 1)], a.shards[(key, 0)])
+    b.wait_prefetch()
+    assert b.slab.residency == L.RES_DEVICE
+    a.drain()
+    arena = torch.zeros(plans[1].rank_info(r).dst_arena_bytes + 256, dtype=torch.uint8, device="cuda")
+    arenas = [torch.zeros_like(arena) for _ in range(W)]
+    arenas[r] = arena
+    m.sync_rank(plans[1], r, b.masters(), arenas)       # sync of B runs while A drains
+    a.wait_drain()
+    assert a.slab.residency == L.RES_HOST and a.slab.elided == elide
+    # oracle: B unchanged, A mutated once
+    for j, (mo, sd, job) in enumerate(zip(models, (70, 71), (a, b))):
+        full = full_state(mo, seed=sd, kinds=(1, 2, 3), special_bits=3)
+        if not elide:
+            full.update({(k, 0): x for (k, kd), x in full_state(mo, seed=sd, kinds=(0,)).items()})
+        if j == 0:
+            for (key, kd), x in list(full.items()):
+                idx = np.arange(x.size, dtype=np.uint64)
+                full[(key, kd)] = x ^ mutation_bits(70, 0, key, kd, idx).reshape(x.shape)
+        if elide:
+            for (key, kd) in [kk for kk in full if kk[1] == 1]:
+                full[(key, 0)] = O.rne_bf16(full[(key, 1)])
+        osh = fsdp_shards(full, W, r, O.fsdp_rows)
+        if job is a:
+            segs, size = O.slab_layout(manifest(mo), W, r)
+            want = O.pack_slab(segs, size, osh)
+            cut = plans[0].rank_info(r).elide_bytes if elide else 0
+            assert np.array_equal(job.slab.host_bytes()[cut:], want[cut:])
+            job.resume()
+        for kk, x in job.shards.items():
+            assert np.array_equal(bits_np(x), osh[kk]), (j, kk)
+    m.close()
