@@ -247,6 +247,77 @@ def scen_hrrs(a, c: Ctx):
            a.out)
 
 
+def scen_overlap(a, c: Ctx):
+    """NEXT-1 off-critical-path switching: 4 jobs visit the
+    group round-robin; each visit = switch in + weight sync + the job's compute
+    phase (modeled as a host wait of its Table-2 update_actor time x
+    --time-scale).  'blocking': duplex switch at the visit boundary.
+    'overlap': while job j computes, the previous job drains and the next one
+    is prefetched, so the boundary only waits for what is left."""
+    models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    plans, jobs, arenas = [], [], []
+    for j, mo in enumerate(models):
+        tp = 1 if mo == "qwen2.5-0.5b" or c.world == 1 else 2
+        pl = mgr.plan(manifest(mo), head_dim=MODELS[mo].head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO)
+        plans.append(pl)
+        jb = P.Job(mgr, pl, seed=j).alloc().init_synthetic()
+        jb.suspend()
+        jobs.append(jb)
+        arenas.append(mgr.arena(pl))
+    psize = [plans[j].stats().total_params / plans[3].stats().total_params for j in range(4)]
+    compute = [38.08 * psize[j] * a.time_scale for j in range(4)]      # update_actor, PAPER.md:658
+    schedule = list(range(4)) * a.rounds
+
+    def blocking():
+        boundary = 0.0
+        resident = None
+        for j in schedule:
+            t = time.perf_counter()
+            if resident is None:
+                jobs[j].resume()
+            else:
+                jobs[resident].switch_to(jobs[j])
+            jobs[j].sync(arenas[j])
+            torch.cuda.synchronize()
+            boundary += time.perf_counter() - t
+            time.sleep(compute[j])
+            resident = j
+        jobs[resident].suspend()
+        return boundary
+
+    def overlapped():
+        boundary = 0.0
+        jobs[schedule[0]].resume()
+        for v, j in enumerate(schedule):
+            p = schedule[v - 1] if v > 0 else None
+            t = time.perf_counter()
+            if v > 0:
+                jobs[j].wait_prefetch()                   # started during p's compute
+            jobs[j].sync(arenas[j])
+            torch.cuda.synchronize()
+            boundary += time.perf_counter() - t
+            if p is not None:
+                jobs[p].drain()                           # off the critical path, during j's compute
+            if v + 1 < len(schedule):
+                jobs[schedule[v + 1]].prefetch()          # ditto for the next job
+            time.sleep(compute[j])
+            if p is not None:
+                t = time.perf_counter()
+                jobs[p].wait_drain()                      # normally long done
+                boundary += time.perf_counter() - t
+        jobs[schedule[-1]].suspend()
+        return boundary
+
+    t_block = blocking()
+    t_over = overlapped()
+    c.emit({"scenario": "overlap", "jobs": models, "n_gpus": c.world, "visits": len(schedule),
+            "time_scale": a.time_scale, "compute_s_per_visit": [round(x, 3) for x in compute],
+            "blocking_boundary_s_total": round(c.allmax(t_block), 3),
+            "overlapped_boundary_s_total": round(c.allmax(t_over), 3),
+            "note": "boundary = time the group is not running the active job's compute (switch + sync)"}, a.out)
+
+
 def scen_optim(a, c: Ctx):
     # each process = rank c.rank of an FSDP-8 plan; k = world processes copy at once
     W = 8
@@ -361,7 +432,7 @@ def scen_multiplex(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap"])
     ap.add_argument("--time-scale", type=float, default=0.005)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -378,7 +449,7 @@ def main():
     if not a.model:
         a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
-     "multiplex": scen_multiplex, "hrrs": scen_hrrs}[a.scenario](a, c)
+     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
