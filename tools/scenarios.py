@@ -318,6 +318,30 @@ def scen_overlap(a, c: Ctx):
             "note": "boundary = time the group is not running the active job's compute (switch + sync)"}, a.out)
 
 
+def scen_nvme(a, c: Ctx):
+    """NEXT-4 cold tier: spill a suspended job's slab to local storage with
+    O_DIRECT and fill it back; the next resume verifies it."""
+    model = a.model or "qwen2.5-1.5b"
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20)
+    plan = mgr.plan(manifest(model))
+    job = P.Job(mgr, plan, seed=5).alloc().init_synthetic()
+    job.suspend()
+    path = os.path.join(a.spill_dir, f"plex_slab_r{c.rank}.bin")
+    n = plan.rank_info(c.rank).slab_bytes
+    c.barrier()
+    t0 = time.perf_counter()
+    job.slab.spill(path, threads=a.io_threads)
+    t1 = time.perf_counter()
+    job.slab.fill(path, threads=a.io_threads)
+    t2 = time.perf_counter()
+    job.resume()                                   # checksum-verified
+    os.remove(path)
+    c.emit({"scenario": "nvme", "model": model, "n_gpus": c.world, "slab_bytes_per_rank": n,
+            "spill_GBs_per_rank": round(n / (c.allmax(t1 - t0)) / 1e9, 2),
+            "fill_GBs_per_rank": round(n / (c.allmax(t2 - t1)) / 1e9, 2), "io_threads": a.io_threads,
+            "dir": a.spill_dir}, a.out)
+
+
 def scen_optim(a, c: Ctx):
     # each process = rank c.rank of an FSDP-8 plan; k = world processes copy at once
     W = 8
@@ -432,7 +456,9 @@ def scen_multiplex(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme"])
+    ap.add_argument("--spill-dir", default="/tmp")
+    ap.add_argument("--io-threads", type=int, default=8)
     ap.add_argument("--time-scale", type=float, default=0.005)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -449,7 +475,7 @@ def main():
     if not a.model:
         a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
-     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap}[a.scenario](a, c)
+     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
