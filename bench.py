@@ -191,7 +191,10 @@ def run_reference(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32 bits",
             "data": "synthetic (counter-based generator, DESIGN.md §3)",
-            "config": {"workload": f"{a.model} FSDP-{world} -> TP-{tp}xDP-{world // tp} (oracle on a bounded sample)"},
+            "config": {"workload": (f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
+                                    f"rollout TP-{tp}xDP-{world // tp}; step = context switch + weight sync -- the "
+                                    f"CPU oracle runs a bounded sample of it (see cpu_baseline.sample)"),
+                       "model_shape": a.model, "impl_note": "CPU oracle (NumPy), no GPU"},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
