@@ -106,3 +106,39 @@ def test_fullsize_qwen7b_one_gpu():
         pytest.skip("needs a 180 GB B200")
     _fullsize("qwen2.5-7b", 1, ["lm_head.weight", "model.layers.0.self_attn.q_proj.weight",
                                 "model.layers.27.mlp.down_proj.weight", "model.norm.weight"])
+
+
+@pytest.mark.slow
+def test_fullsize_qwen05_every_byte():
+    """configs[0] checked exhaustively: every byte of the
+    0.5B slab and every element of every rollout tensor against the oracle's
+    regeneration, tensor by tensor (no sampling)."""
+    torch.cuda.set_device(0)
+    model, seed = "qwen2.5-0.5b", 0
+    man = manifest(model)
+    mgr = P.StateManager(device=0, bucket_bytes=2 << 30, n_slots=2, bootstrap=False)
+    plan = mgr.plan(man, head_dim=MODELS[model].head_dim, tp=1, dp=1)
+    job = P.Job(mgr, plan, seed=seed).alloc().init_synthetic()
+    job.suspend()
+    slab = job.slab.host_bytes()
+    for s in plan.segments(0):
+        key = man[s.tensor][0]
+        want = gen_range(seed, key, s.kind, s.index_base, s.nbytes // (2 if s.kind == 0 else 4))
+        assert np.array_equal(slab[s.slab_offset:s.slab_offset + s.nbytes].view(want.dtype), want), (key, s.kind)
+    job.resume()
+    arena = mgr.arena(plan)
+    job.sync(arena)
+    views = P.StateManager.rollout_views(plan, 0, arena)
+    shapes = dict(man)
+    full = {}
+    for key, shape in man:
+        full[key] = O.rne_bf16(gen_tensor(seed, key, 1, shape))
+    want = O.rollout_tensors(full, 1, 1, 1, 0)
+    assert list(views) == list(want)
+    for name, x in want.items():
+        assert np.array_equal(bits_np(views[name]), x), name
+    del views, arena, job, plan
+    mgr.close()
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
