@@ -542,12 +542,14 @@ template <bool kPack>
 static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                                  uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
                                  cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};                 // per device: the attribute lives in each context
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, PackCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)PackCfg::kSmem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
