@@ -99,6 +99,24 @@ def main():
             if not np.array_equal(bits_np(views[name]), x):
                 print(f"[rank {rank}] sync mismatch {name}", flush=True)
                 bad += 1
+    # the NCCL-baseline transport must produce the same bytes at full size
+    mgr_nccl = P.StateManager(device=local, rank=rank, world=world, sync_nccl=True, duplex=False)
+    arena.fill_(0x5A)
+    mgr_nccl.sync(plans[0], a.masters(), arena)
+    views = P.StateManager.rollout_views(plans[0], rank, arena)
+    for key in SAMPLE:
+        keys = [key]
+        if ".q_proj." in key:
+            keys += [key.replace(".q_proj.", ".k_proj."), key.replace(".q_proj.", ".v_proj.")]
+        if ".gate_proj." in key:
+            keys += [key.replace(".gate_proj.", ".up_proj.")]
+        cast = {k: O.rne_bf16(gen_tensor(1, k, 1, shapes[k])) for k in keys}
+        want = O.rollout_tensors(cast, tp, dp, 1, rank, O.TP_FAST, shape.head_dim)
+        for name, x in want.items():
+            if not np.array_equal(bits_np(views[name]), x):
+                print(f"[rank {rank}] nccl sync mismatch {name}", flush=True)
+                bad += 1
+    mgr_nccl.close()
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()
