@@ -407,6 +407,36 @@ def scen_moe(a, c: Ctx):
             "unit_offload_onload_ms": round(ms_unit, 3), "clocks": clk}, a.out)
 
 
+def scen_sync(a, c: Ctx):
+    """Weight sync alone for any dense config (e.g. configs[2]: Qwen2.5-32B
+    FSDP-N -> TP-4 x DP; at 4 GPUs FSDP-4 -> TP-4), masters only on the device,
+    both transports."""
+    model = a.model or "qwen2.5-32b"
+    shape = MODELS[model]
+    tp = a.tp or min(4, c.world)
+    out = {}
+    for transport in ("push", "nccl"):
+        mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=256 << 20, timing=True,
+                             sync_nccl=transport == "nccl", duplex=False)
+        plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO)
+        job = P.Job(mgr, plan, seed=2, slab=False).alloc(kinds=(1,)).init_synthetic()
+        arena = mgr.arena(plan)
+        mgr.reset_stats()
+        ms, clk = timed(c, lambda: job.sync(arena), a.steps, a.warmup)
+        st = mgr.stats()
+        info = plan.rank_info(c.rank)
+        nv = c.allmax(float(max(info.send_bytes, info.recv_bytes)))
+        k = "push" if transport == "push" else "nccl"
+        t_x = c.allmax(st[k]["ms"] / max(1, a.steps))
+        out[transport] = {"sync_ms": round(ms, 3), "data_ms": round(t_x, 3),
+                          "nvlink_GBs": round(nv / (t_x * 1e-3) / 1e9, 1) if c.world > 1 and t_x > 0 else None}
+        del job, arena, plan
+        mgr.close()
+        torch.cuda.empty_cache()
+    c.emit({"scenario": "sync", "model": model, "n_gpus": c.world, "layout": f"FSDP-{c.world}->TP-{tp}xDP-{c.world // tp}",
+            "nvlink_bytes_max_rank": nv, **out, "clocks": clk}, a.out)
+
+
 def scen_multiplex(a, c: Ctx):
     models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
     mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
@@ -456,7 +486,7 @@ def scen_multiplex(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync"])
     ap.add_argument("--spill-dir", default="/tmp")
     ap.add_argument("--io-threads", type=int, default=8)
     ap.add_argument("--time-scale", type=float, default=0.005)
@@ -475,7 +505,8 @@ def main():
     if not a.model:
         a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
-     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme}[a.scenario](a, c)
+     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme,
+     "sync": scen_sync}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
