@@ -213,10 +213,15 @@ def scen_hrrs(a, c: Ctx):
         while pending:
             now = time.perf_counter() - t0 + 1.0          # every request has arrived by t = 1
             if policy == "fcfs":
-                r = pending[0]
+                pick = 0
             else:
                 cur = Req(resident, 0.0, 1e-9, remaining=1e-9) if resident is not None else None
-                r = max(pending, key=lambda q: priority(q, now, cur, setup))
+                pick = max(range(len(pending)), key=lambda i: priority(pending[i], now, cur, setup))
+            if c.world > 1:                               # every rank must run the same request
+                obj = [pick]
+                dist.broadcast_object_list(obj, src=0)
+                pick = obj[0]
+            r = pending[pick]
             pending.remove(r)
             waits.append(now - r.arrival)
             if r.job != resident:
@@ -427,7 +432,8 @@ def scen_sync(a, c: Ctx):
         info = plan.rank_info(c.rank)
         nv = c.allmax(float(max(info.send_bytes, info.recv_bytes)))
         k = "push" if transport == "push" else "nccl"
-        t_x = c.allmax(st[k]["ms"] / max(1, a.steps))
+        per_sync = 1 if transport == "push" else max(1, st["nccl"]["launches"] // (a.steps + a.warmup))
+        t_x = c.allmax(st[k]["ms"] / max(1, st[k]["launches"]) * per_sync)
         out[transport] = {"sync_ms": round(ms, 3), "data_ms": round(t_x, 3),
                           "nvlink_GBs": round(nv / (t_x * 1e-3) / 1e9, 1) if c.world > 1 and t_x > 0 else None}
         del job, arena, plan
