@@ -431,9 +431,9 @@ def scen_sync(a, c: Ctx):
         st = mgr.stats()
         info = plan.rank_info(c.rank)
         nv = c.allmax(float(max(info.send_bytes, info.recv_bytes)))
-        k = "push" if transport == "push" else "nccl"
-        per_sync = 1 if transport == "push" else max(1, st["nccl"]["launches"] // (a.steps + a.warmup))
-        t_x = c.allmax(st[k]["ms"] / max(1, st[k]["launches"]) * per_sync)
+        # data-moving time: the push kernel, or (NCCL) the whole call -- the
+        # per-round exchange events include waiting for peers' K4 rounds
+        t_x = c.allmax(st["push"]["ms"] / max(1, st["push"]["launches"])) if transport == "push" else ms
         out[transport] = {"sync_ms": round(ms, 3), "data_ms": round(t_x, 3),
                           "nvlink_GBs": round(nv / (t_x * 1e-3) / 1e9, 1) if c.world > 1 and t_x > 0 else None}
         del job, arena, plan
