@@ -189,7 +189,7 @@ def run_reference(a):
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 2),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32 bits",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (counter-based generator, DESIGN.md §3)",
             "config": {"workload": (f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
                                     f"rollout TP-{tp}xDP-{world // tp}; step = context switch + weight sync -- the "
@@ -433,7 +433,7 @@ def run_plex(a):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16/fp32 bits (byte copy; fp32->bf16 RNE integer cast)",
+            "vs_baseline": None, "dtype": "u32", "dtype_note": "state moved as raw bits (bf16 + fp32); the only arithmetic is the fp32->bf16 RNE cast in 32-bit integer ops",
             "data": "synthetic (counter-based generator, DESIGN.md §3); random-init Qwen2.5-7B-shaped state",
             "config": {"workload": (f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
                                     f"rollout TP-{tp}xDP-{dp}; step = context switch A->B (full suspend of A + full "
