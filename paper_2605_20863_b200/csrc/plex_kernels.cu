@@ -6,11 +6,13 @@
 // K6 synthetic init / mutation, K7 checksum, plain cast: infrastructure.
 //
 // Everything here is HBM- (or NVLink-) bound data movement with a few integer
-// ops per element: no tensor cores (nothing is a contraction).  Access is
-// 16-B vectorised (ld.global.nc.L1::no_allocate / st.global.v4), one 256-
-// thread CTA per 64 KiB work item with 4 independent 16-B loads in flight per
-// thread, work items precomputed by the planner so index math stays cheap
-// (DESIGN.md §5).
+// ops per element: no tensor cores (nothing is a contraction).
+//  * K1/K2: persistent TMA bulk-copy pipeline (cp.async.bulk global<->shared,
+//    mbarrier complete_tx), 2 CTAs/SM, dynamic work claiming spread across the
+//    bucket; the checksum is folded from shared memory.
+//  * push / cast / derive: one 256-thread CTA per planner work item, 16-B
+//    vectorised streaming loads (ld.global.nc.L1::no_allocate) and stores;
+//    the push kernel's stores go to peer-mapped arenas over NVLink.
 #include <cuda_runtime.h>
 
 #include <cstdint>
