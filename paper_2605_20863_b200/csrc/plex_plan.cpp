@@ -265,9 +265,12 @@ static plex_status build_sync(Plan& p) {
     }
     std::vector<std::vector<std::vector<PushItem>>> per(p.world, std::vector<std::vector<PushItem>>(p.world));
     for (int32_t g = 0; g < p.world; ++g) emit_push(p, per, g);
-    // Interleave each source's items round-robin over destinations starting
-    // at r+1 so that, at any moment, every sender spreads its NVLink stores
-    // over all peers instead of all senders converging on one receiver.
+    // Interleave each source's items over its destinations in proportion to
+    // their sizes (always take the destination least far along its list, ties
+    // broken starting at r+1): every sender then spreads its NVLink stores
+    // over all peers for the whole kernel -- senders never converge on one
+    // receiver, and local (HBM-only) items never bunch up into a tail while
+    // the links sit idle.
     for (int32_t r = 0; r < p.world; ++r) {
         RankPlan& R = p.ranks[r];
         std::vector<size_t> pos(p.world, 0);
@@ -275,10 +278,17 @@ static plex_status build_sync(Plan& p) {
         for (int32_t g = 0; g < p.world; ++g) left += per[r][g].size();
         R.push.reserve(left);
         while (left) {
+            int32_t best = -1;
+            double best_f = 2.0;
             for (int32_t k = 1; k <= p.world; ++k) {
                 const int32_t g = (r + k) % p.world;
-                if (pos[g] < per[r][g].size()) { R.push.push_back(per[r][g][pos[g]++]); --left; }
+                const size_t n = per[r][g].size();
+                if (pos[g] >= n) continue;
+                const double f = (pos[g] + 0.5) / (double)n;
+                if (f < best_f) { best_f = f; best = g; }
             }
+            R.push.push_back(per[r][best][pos[best]++]);
+            --left;
         }
         for (const PushItem& it : R.push) R.src_read_bytes += (uint64_t)it.rows * it.cols * 4;
     }
