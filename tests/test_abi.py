@@ -34,3 +34,16 @@ def test_version_and_error_string():
     h = C.c_void_p()
     assert _lib.lib.plex_transition_plan(None, C.byref(h)) == _lib.E_INVAL
     assert b"manifest" in _lib.lib.plex_last_error()
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libplex.so the package refuses to import."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_2605_20863_b200"
+    shutil.copytree(os.path.join(ROOT, "paper_2605_20863_b200"), pkg,
+                    ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2605_20863_b200"], cwd=tmp_path,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "libplex.so" in r.stderr and "ImportError" in r.stderr
