@@ -422,8 +422,7 @@ def run_plex(a):
                         "over": "NCCL exchange rounds" if st["nccl"]["launches"] else
                                 "fused cast+push kernel (local casts included)",
                         "peak_kind": "nominal 900 GB/s/dir; measured peer copy 770 (B200_PROFILING.md)"}
-        if st["barrier"]["launches"]:
-            rl["sync_entry_barrier_ms"] = round(allmax(st["barrier"]["ms"] / a.steps), 3)
+
         if st["nccl"]["launches"]:
             rl["nccl_exchange"] = {"ms_per_step": round(st["nccl"]["ms"] / a.steps, 3),
                                    "rounds_per_step": st["nccl"]["launches"] / a.steps}
