@@ -53,6 +53,7 @@ def parse():
                     help="pin slabs with cudaHostAlloc instead of mmap(MADV_HUGEPAGE) + cudaHostRegister")
     ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")
     ap.add_argument("--single-job", action="store_true", help="step = suspend + resume + sync of one job")
+    ap.add_argument("--no-balance", action="store_true", help="no NVLink-carried buckets (host-link balancing)")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=2)
@@ -253,10 +254,43 @@ def run_plex(a):
     t_setup = time.perf_counter()
     mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=a.slots, timing=True,
                          sync_nccl=a.sync_nccl)
+    # host-link roofline BW_host(k = world): pinned copy of 4 GiB, all ranks at once
+    probe = 4 << 30
+    h = torch.empty(probe, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(probe, dtype=torch.uint8, device=f"cuda:{local}")
+    bw = {}
+    for direction in ("d2h", "h2d"):
+        best = 0.0
+        for _ in range(3):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            (h.copy_(dbuf, non_blocking=True) if direction == "d2h" else dbuf.copy_(h, non_blocking=True))
+            e1.record()
+            e1.synchronize()
+            best = max(best, probe / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        bw[direction] = best
+    del h, dbuf
+    torch.cuda.empty_cache()
+
+    # NEXT-1 host-link balancing: every rank's rate for one offload + one onload
+    # byte, all-gathered; the planner hands whole buckets from slow-link ranks
+    # to fast-link ranks over NVLink when that shortens the slowest rank
+    weights = None
+    if world > 1 and not a.no_balance:
+        w_local = 1.0 / (1.0 / bw["d2h"] + 1.0 / bw["h2d"])
+        wt = torch.tensor([w_local], dtype=torch.float64, device=f"cuda:{local}")
+        allw = [torch.zeros_like(wt) for _ in range(world)]
+        dist.all_gather(allw, wt)
+        weights = [float(x.item()) for x in allw]
+
     t0 = time.perf_counter()
     rank_map = {"tp": 0, "dp": 1, "auto": 2}[a.rank_map]
-    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map)
-             for _ in range(2)]
+    plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map,
+                      link_weights=weights) for _ in range(2)]
+    for pl in plans:
+        mgr.enable_carry(pl)
+    n_carried = len(plans[0].carry())
     plan_s = (time.perf_counter() - t0) / 2
     plan = plans[0]
     info = plan.rank_info(rank)
@@ -290,25 +324,6 @@ def run_plex(a):
     free, total = torch.cuda.mem_get_info(local)
     duplex = two_jobs and (not a.no_duplex) and (info.payload_bytes + (4 << 30) < free)
     duplex = allmin(1.0 if duplex else 0.0) > 0.5
-
-    # host-link roofline BW_host(k = world): pinned copy of 4 GiB, all ranks at once
-    probe = 4 << 30
-    h = torch.empty(probe, dtype=torch.uint8).pin_memory()
-    dbuf = torch.empty(probe, dtype=torch.uint8, device=f"cuda:{local}")
-    bw = {}
-    for direction in ("d2h", "h2d"):
-        best = 0.0
-        for _ in range(3):
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            (h.copy_(dbuf, non_blocking=True) if direction == "d2h" else dbuf.copy_(h, non_blocking=True))
-            e1.record()
-            e1.synchronize()
-            best = max(best, probe / (e0.elapsed_time(e1) * 1e-3) / 1e9)
-        bw[direction] = best
-    del h, dbuf
-    torch.cuda.empty_cache()
 
     phase_ev = []
     cur = {"i": 0}
@@ -442,6 +457,8 @@ def run_plex(a):
                                     f"TP-{tp}xDP-{dp}; step = full suspend + full resume + weight sync (two jobs' "
                                     f"slabs exceed the host's pinnable memory)"),
                        "jobs": 2 if two_jobs else 1,
+                       "host_link_weights_GBs": [round(x, 2) for x in weights] if weights else None,
+                       "carried_buckets_per_job": n_carried,
                        "model_shape": a.model, "state_bytes_per_rank_per_job": info.payload_bytes,
                        "bytes_switched_per_step": int(S_total), "duplex": duplex,
                        "bucket_bytes": bucket, "staging_slots": a.slots,

@@ -144,6 +144,11 @@ typedef struct {
     int64_t incoming_job;
     int32_t op;
     uint32_t flags;              /* PLEX_PLAN_* */
+    /* NEXT-1 host-link balancing: relative host-link rate of every rank
+     * (world entries, > 0; NULL = no carrying).  Ranks whose slab would take
+     * longer than the group average hand whole buckets over NVLink to ranks
+     * with spare host bandwidth, which keep them in a pinned carry region. */
+    const float* link_weights;
 } plex_plan_req;
 
 /* Plan flags. */
@@ -182,7 +187,17 @@ typedef struct {
     uint64_t src_read_bytes;     /* fp32 bytes read by this rank's push     */
     int32_t elide_buckets;       /* PLEX_PLAN_ELIDE_PARAM: buckets still moved when eliding */
     uint64_t elide_bytes;        /* ... and the PARAM prefix derived instead (0 = none) */
+    int32_t carried_out;         /* own buckets carried by other ranks      */
+    int32_t carried_in;          /* other ranks' buckets this rank carries  */
+    uint64_t carry_bytes;        /* pinned carry region this rank hosts     */
 } plex_rank_info;
+
+typedef struct {                 /* one carried bucket (global plan order)  */
+    int32_t owner, bucket, carrier;
+    uint64_t slab_offset;        /* in the owner's canonical slab           */
+    uint64_t bytes;
+    uint64_t carry_offset;       /* in the carrier's carry region           */
+} plex_carry_desc;
 
 typedef struct {
     int32_t tensor;              /* manifest index                          */
@@ -239,6 +254,9 @@ PLEX_API plex_status plex_plan_segment(plex_plan_t plan, int32_t rank, int32_t i
 PLEX_API plex_status plex_plan_dst_tensor(plex_plan_t plan, int32_t rank, int32_t i, plex_dst_desc* out);
 /* FSDP rows [row0, row1) of tensor t held by `rank` (R2; empty when row0 == row1). */
 PLEX_API plex_status plex_plan_shard_rows(plex_plan_t plan, int32_t rank, int32_t t, int64_t* row0, int64_t* row1);
+/* i-th carried bucket of the plan (0 <= i < plex_plan_n_carry). */
+PLEX_API plex_status plex_plan_n_carry(plex_plan_t plan, int32_t* n);
+PLEX_API plex_status plex_plan_carry(plex_plan_t plan, int32_t i, plex_carry_desc* out);
 /* bytes[r * world + g]: bf16 bytes source rank r contributes to rollout rank g
  * (diagonal = local).  The zero-redundancy ledger of PAPER.md:576. */
 PLEX_API plex_status plex_plan_ledger(plex_plan_t plan, uint64_t* bytes, int32_t n);
@@ -256,6 +274,12 @@ PLEX_API plex_status plex_ctx_create(int32_t device, void* staging, uint64_t sta
                             void* pack_stream, void* copy_stream, const void* nccl_id,
                             int32_t rank, int32_t world, uint32_t flags, plex_ctx_t* out);
 PLEX_API plex_status plex_ctx_destroy(plex_ctx_t ctx);
+/* NEXT-1 host-link balancing: caller-owned device buffer of >= 4 x bucket
+ * bytes (256-B aligned) used to stage carried buckets (plans built with
+ * link_weights).  With carried buckets, offload / onload / switch become
+ * collective over the ctx's NCCL world (every rank calls them with the same
+ * plan). */
+PLEX_API plex_status plex_ctx_set_carry_staging(plex_ctx_t ctx, void* staging, uint64_t bytes);
 PLEX_API plex_status plex_ctx_stats(plex_ctx_t ctx, int32_t which, plex_kernel_stats* out);
 PLEX_API plex_status plex_ctx_reset_stats(plex_ctx_t ctx);
 /* Per-launch records behind plex_ctx_stats (PLEX_CTX_TIMING), oldest first,
@@ -278,6 +302,9 @@ PLEX_API plex_status plex_slab_info(plex_slab_t slab, void** host_ptr, uint64_t*
  * O_DIRECT, E_TIER_FULL on I/O or pinning failure (state unchanged). */
 PLEX_API plex_status plex_slab_spill(plex_slab_t slab, const char* path, int32_t threads);
 PLEX_API plex_status plex_slab_fill(plex_slab_t slab, const char* path, int32_t threads);
+/* The pinned carry region holding other ranks' carried buckets (carry_offset
+ * of plex_carry_desc), NULL / 0 if this rank carries none. */
+PLEX_API plex_status plex_slab_carry(plex_slab_t slab, void** host_ptr, uint64_t* bytes);
 /* *elided = 1 if the last offload elided the derived PARAM buckets. */
 PLEX_API plex_status plex_slab_elided(plex_slab_t slab, int32_t* elided);
 /* out[2*i], out[2*i+1] = (S1, S2) of segment i recorded at offload (R14). */

@@ -32,6 +32,7 @@ PLAN_ELIDE_PARAM = 0x1
 EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
+    "plex_plan_n_carry", "plex_plan_carry", "plex_ctx_set_carry_staging", "plex_slab_carry",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
     "plex_ctx_trace",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
@@ -60,7 +61,8 @@ class PlanReq(C.Structure):
                 ("tp", C.c_int32), ("dp", C.c_int32), ("ep", C.c_int32), ("rank_map", C.c_int32),
                 ("slab_layout", C.c_int32), ("kind_mask", C.c_uint32), ("n_subset", C.c_int32),
                 ("subset", C.POINTER(C.c_int32)), ("bucket_bytes", C.c_uint64), ("tile_bytes", C.c_uint64),
-                ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32), ("flags", C.c_uint32)]
+                ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32), ("flags", C.c_uint32),
+                ("link_weights", C.POINTER(C.c_float))]
 
 
 class PlanStats(C.Structure):
@@ -74,7 +76,13 @@ class RankInfo(C.Structure):
                 ("n_buckets", C.c_int32), ("n_pack_items", C.c_uint64), ("dst_arena_bytes", C.c_uint64),
                 ("n_dst_tensors", C.c_int32), ("n_push_items", C.c_uint64), ("send_bytes", C.c_uint64),
                 ("recv_bytes", C.c_uint64), ("local_bytes", C.c_uint64), ("src_read_bytes", C.c_uint64),
-                ("elide_buckets", C.c_int32), ("elide_bytes", C.c_uint64)]
+                ("elide_buckets", C.c_int32), ("elide_bytes", C.c_uint64), ("carried_out", C.c_int32),
+                ("carried_in", C.c_int32), ("carry_bytes", C.c_uint64)]
+
+
+class CarryDesc(C.Structure):
+    _fields_ = [("owner", C.c_int32), ("bucket", C.c_int32), ("carrier", C.c_int32), ("slab_offset", C.c_uint64),
+                ("bytes", C.c_uint64), ("carry_offset", C.c_uint64)]
 
 
 class SegDesc(C.Structure):
@@ -111,6 +119,10 @@ def _load() -> C.CDLL:
         "plex_plan_dst_tensor": (C.c_int, [VP, I32, I32, P(DstDesc)]),
         "plex_plan_shard_rows": (C.c_int, [VP, I32, I32, P(I64), P(I64)]),
         "plex_plan_ledger": (C.c_int, [VP, P(U64), I32]),
+        "plex_plan_n_carry": (C.c_int, [VP, P(I32)]),
+        "plex_plan_carry": (C.c_int, [VP, I32, P(CarryDesc)]),
+        "plex_ctx_set_carry_staging": (C.c_int, [VP, VP, U64]),
+        "plex_slab_carry": (C.c_int, [VP, P(VP), P(U64)]),
         "plex_nccl_unique_id": (C.c_int, [VP]),
         "plex_ctx_create": (C.c_int, [I32, VP, U64, I32, VP, VP, VP, I32, I32, U32, P(VP)]),
         "plex_ctx_destroy": (C.c_int, [VP]),

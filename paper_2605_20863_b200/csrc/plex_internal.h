@@ -92,11 +92,21 @@ struct RankPlan {
     std::vector<DstTensor> dst;
     uint64_t arena_bytes = 0;
     std::vector<PushItem> push;                 // items whose source is this rank
+    std::vector<char> carried;                  // per own bucket: moved by another rank's host link
+    int32_t carried_out = 0, carried_in = 0;
+    uint64_t carry_bytes = 0;
     uint64_t send_bytes = 0, recv_bytes = 0, local_bytes = 0, src_read_bytes = 0;
+};
+
+struct CarryXfer {       // a whole bucket of `owner`'s slab moved through `carrier`'s host link
+    int32_t owner, bucket, carrier;
+    uint64_t lo, len;    // owner slab byte range
+    uint64_t coff;       // offset in the carrier's carry region
 };
 
 struct Plan {
     std::vector<Tensor> tensors;
+    std::vector<CarryXfer> carry;               // global, sorted by (owner, bucket)
     int32_t world = 1, tp = 0, dp = 0, ep = 1, rank_map = 0, layout = 0;
     uint32_t kind_mask = PLEX_KINDMASK_ALL;
     uint64_t bucket = kDefaultBucket, tile = kDefaultTile;

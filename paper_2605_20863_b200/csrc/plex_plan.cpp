@@ -309,6 +309,67 @@ static uint64_t max_link_bytes(const Plan& p) {
     return m;
 }
 
+// NEXT-1 host-link balancing: with per-rank host-link weights w_r, the group
+// needs T = sum_r S_r / sum_r w_r; ranks above T hand their last whole buckets
+// to the ranks with the most spare capacity (deterministic greedy).
+static plex_status build_carry(Plan& p, const float* w) {
+    const int32_t W = p.world;
+    double sw = 0, ss = 0;
+    for (int32_t r = 0; r < W; ++r) {
+        if (!(w[r] > 0)) { set_error("link weight of rank %d must be > 0", r); return PLEX_E_INVAL; }
+        sw += w[r];
+        ss += (double)p.ranks[r].slab_bytes;
+        p.ranks[r].carried.assign(n_buckets(p, p.ranks[r]), 0);
+    }
+    const double T = ss / sw;
+    std::vector<double> load(W);
+    for (int32_t r = 0; r < W; ++r) load[r] = (double)p.ranks[r].slab_bytes;
+    std::vector<char> giver(W, 0);
+    std::vector<int32_t> next_b(W, 0);                       // next bucket a giver would hand off
+    for (int32_t r = 0; r < W; ++r) {
+        if (load[r] / w[r] > T * 1.02) giver[r] = 1;
+        next_b[r] = n_buckets(p, p.ranks[r]) - 1;
+    }
+    for (;;) {
+        // the most loaded giver hands its last remaining bucket (never bucket 0)
+        // to the carrier with the most spare capacity, one bucket at a time
+        int32_t r = -1;
+        for (int32_t g = 0; g < W; ++g)
+            if (giver[g] && next_b[g] >= 1 && load[g] / w[g] > T && (r < 0 || load[g] / w[g] > load[r] / w[r]))
+                r = g;
+        if (r < 0) break;
+        const RankPlan& R = p.ranks[r];
+        const int32_t b = next_b[r];
+        const uint64_t lo = (uint64_t)b * p.bucket;
+        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+        int32_t best = -1;
+        double spare = 0;
+        for (int32_t c = 0; c < W; ++c) {
+            if (giver[c]) continue;
+            const double sp = T * w[c] - load[c];
+            if (sp > spare) { spare = sp; best = c; }
+        }
+        // only if it lowers the group's maximum
+        if (best < 0 || (load[best] + (double)len) / w[best] >= load[r] / w[r]) { next_b[r] = 0; continue; }
+        p.carry.push_back(CarryXfer{r, b, best, lo, len, 0});
+        p.ranks[r].carried[b] = 1;
+        load[r] -= (double)len;
+        load[best] += (double)len;
+        next_b[r] = b - 1;
+    }
+    std::sort(p.carry.begin(), p.carry.end(), [](const CarryXfer& a, const CarryXfer& b) {
+        return a.owner != b.owner ? a.owner < b.owner : a.bucket < b.bucket;
+    });
+    for (CarryXfer& x : p.carry) {
+        RankPlan& C = p.ranks[x.carrier];
+        x.coff = C.carry_bytes;
+        C.carry_bytes += align_up(x.len, kSegAlign);
+        C.carried_in += 1;
+        p.ranks[x.owner].carried_out += 1;
+    }
+    return PLEX_OK;
+}
+
 static plex_status build(const plex_plan_req* q, Plan& p) {
     if (!q || q->n_tensors <= 0 || !q->tensors) { set_error("empty manifest"); return PLEX_E_INVAL; }
     if (q->world < 1) { set_error("world must be >= 1"); return PLEX_E_INVAL; }
@@ -376,6 +437,12 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
         if (s) return s;
     }
     p.ledger.assign((size_t)p.world * p.world, 0);
+    for (RankPlan& R : p.ranks) R.carried.assign(n_buckets(p, R), 0);
+    if (q->link_weights && p.world > 1) {
+        if (p.flags & PLEX_PLAN_ELIDE_PARAM) { set_error("link balancing and param elision are exclusive"); return PLEX_E_INVAL; }
+        plex_status s2 = build_carry(p, q->link_weights);
+        if (s2) return s2;
+    }
     if (sync) {
         if (q->rank_map == PLEX_RANKMAP_AUTO) {
             int32_t best = PLEX_RANKMAP_TP_FAST;
@@ -454,6 +521,9 @@ plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* 
     o.src_read_bytes = R.src_read_bytes;
     o.elide_buckets = R.elide_start ? (int32_t)R.bstart_el.size() - 1 : 0;
     o.elide_bytes = R.elide_start;
+    o.carried_out = R.carried_out;
+    o.carried_in = R.carried_in;
+    o.carry_bytes = R.carry_bytes;
     *out = o;
     return PLEX_OK;
 }
@@ -486,6 +556,19 @@ plex_status plex_plan_shard_rows(plex_plan_t plan, int32_t rank, int32_t t, int6
         return PLEX_E_INVAL;
     }
     fsdp_rows(plan->p.tensors[t].d0, plan->p.world, rank, row0, row1);
+    return PLEX_OK;
+}
+
+plex_status plex_plan_n_carry(plex_plan_t plan, int32_t* n) {
+    if (!plan || !n) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    *n = (int32_t)plan->p.carry.size();
+    return PLEX_OK;
+}
+
+plex_status plex_plan_carry(plex_plan_t plan, int32_t i, plex_carry_desc* out) {
+    if (!plan || !out || i < 0 || i >= (int32_t)plan->p.carry.size()) { set_error("bad carry index"); return PLEX_E_INVAL; }
+    const CarryXfer& x = plan->p.carry[i];
+    *out = plex_carry_desc{x.owner, x.bucket, x.carrier, x.lo, x.len, x.coff};
     return PLEX_OK;
 }
 

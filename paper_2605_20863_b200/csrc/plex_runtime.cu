@@ -136,6 +136,14 @@ struct plex_ctx_s {
     uint64_t* d_ptrs3 = nullptr;
     size_t ptr_cap3 = 0;
     AsyncState* async[2] = {nullptr, nullptr};   // [0] drain (offload), [1] prefetch (onload)
+    // NEXT-1 host-link balancing (carried buckets): caller-provided carry staging
+    // (4 bucket slots: 0-1 offload direction, 2-3 onload direction), a kernel
+    // stream, one NCCL stream for every carry send/recv, a carrier copy stream
+    uint8_t* cstaging = nullptr;
+    uint64_t cstaging_bytes = 0;
+    cudaStream_t ckern = nullptr, cstream = nullptr, ccopy = nullptr;
+    cudaEvent_t ev_cs[4] = {}, ev_cc[4] = {}, ev_cbeg = nullptr, ev_cend = nullptr;
+    bool carry_used = false;            // the current blocking op enqueued carry work
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
@@ -164,6 +172,8 @@ struct plex_slab_s {
     bool written = false;
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
     bool busy = false;                  // an async drain / prefetch of this slab is in flight
+    uint8_t* carry_host = nullptr;      // other ranks' carried buckets (pinned)
+    uint64_t carry_bytes = 0;
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
 };
 
@@ -315,6 +325,14 @@ static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
     CK(cudaEventRecord(c->ev_copy_done, c->copy));
     CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
     CK(cudaStreamWaitEvent(caller, c->ev_copy_done, 0));
+    if (c->carry_used) {
+        for (cudaStream_t s2 : {c->ckern, c->cstream, c->ccopy}) {
+            CK(cudaEventRecord(c->ev_cend, s2));
+            CK(cudaStreamWaitEvent(caller, c->ev_cend, 0));
+            CK(cudaStreamSynchronize(s2));
+        }
+        c->carry_used = false;
+    }
     CK(cudaStreamSynchronize(c->pack));
     CK(cudaStreamSynchronize(c->copy));
     return timed_collect(c);
@@ -414,6 +432,132 @@ static void use_grid(Half& h, bool elide) {
     }
 }
 
+// ---- NEXT-1 host-link balancing: carried buckets -----------------------------------
+// Every rank walks the plan's global carry list in order and issues only the
+// NCCL sends/receives it takes part in, on its one carry stream: both ends of
+// every pair see their common transfers in the same order, and the global
+// order rules out cycles.  Offload: the owner packs a carried bucket into a
+// carry slot (ckern) and sends it; the carrier receives it into its slot and
+// D2H-copies it into its pinned carry region (ccopy).  Onload mirrors it.
+static plex_status carry_ready(plex_ctx_s* c, const Plan& p) {
+    if (p.carry.empty()) return PLEX_OK;
+    if (!c->comm) { set_error("carried buckets need a ctx with an NCCL communicator"); return PLEX_E_INVAL; }
+    if (!c->cstaging || c->cstaging_bytes < 4 * p.bucket) {
+        set_error("carried buckets need carry staging >= 4 x bucket (plex_ctx_set_carry_staging)");
+        return PLEX_E_INVAL;
+    }
+    if (!c->ckern) {
+        CK(cudaStreamCreateWithFlags(&c->ckern, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->ccopy, cudaStreamNonBlocking));
+        for (int i = 0; i < 4; ++i) {
+            CK(cudaEventCreateWithFlags(&c->ev_cs[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_cc[i], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&c->ev_cbeg, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_cend, cudaEventDisableTiming));
+    }
+    return PLEX_OK;
+}
+
+// offload direction (slots 0-1): call after off_begin, before the own buckets
+static plex_status carry_out(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const Plan& p = *h.p;
+    if (p.carry.empty() || h.elide) return PLEX_OK;
+    plex_status st;
+    if ((st = carry_ready(c, p))) return st;
+    c->carry_used = true;
+    CK(cudaEventRecord(c->ev_cbeg, pp.kern));                 // pointer table + zeroed checksums
+    CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_cbeg, 0));
+    CK(cudaStreamWaitEvent(c->ccopy, c->ev_cbeg, 0));
+    const RankPlan& R = *h.R;
+    int k = 0;
+    for (const CarryXfer& x : p.carry) {
+        if (x.owner != c->rank && x.carrier != c->rank) continue;
+        const int sl = k % 2;
+        uint8_t* slot = c->cstaging + (uint64_t)sl * p.bucket;
+        cudaEvent_t ta = nullptr;
+        if (x.owner == c->rank) {
+            if (k >= 2) CK(cudaStreamWaitEvent(c->ckern, c->ev_cs[sl], 0));      // slot's last send done
+            const uint64_t i0 = R.bucket_item_start[x.bucket], i1 = R.bucket_item_start[x.bucket + 1];
+            if ((st = tbeg(c, pp, c->ckern, &ta))) return st;
+            CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, slot, x.lo, h.d->cks,
+                           c->d_ctr + 4, c->ckern));
+            if ((st = tend(c, pp, c->ckern, ta, PLEX_STAT_PACK, 2 * h.d->bucket_payload[x.bucket]))) return st;
+            CK(cudaEventRecord(c->ev_cc[sl], c->ckern));
+            CK(cudaStreamWaitEvent(c->cstream, c->ev_cc[sl], 0));
+            NK(ncclSend(slot, x.len, ncclUint8, x.carrier, c->comm, c->cstream));
+            CK(cudaEventRecord(c->ev_cs[sl], c->cstream));
+        } else {
+            if (k >= 2) CK(cudaStreamWaitEvent(c->cstream, c->ev_cc[sl], 0));    // slot's last D2H done
+            NK(ncclRecv(slot, x.len, ncclUint8, x.owner, c->comm, c->cstream));
+            CK(cudaEventRecord(c->ev_cs[sl], c->cstream));
+            CK(cudaStreamWaitEvent(c->ccopy, c->ev_cs[sl], 0));
+            if ((st = tbeg(c, pp, c->ccopy, &ta))) return st;
+            CK(cudaMemcpyAsync(h.slab->carry_host + x.coff, slot, x.len, cudaMemcpyDeviceToHost, c->ccopy));
+            if ((st = tend(c, pp, c->ccopy, ta, PLEX_STAT_D2H, x.len))) return st;
+            CK(cudaEventRecord(c->ev_cc[sl], c->ccopy));
+        }
+        ++k;
+    }
+    return PLEX_OK;
+}
+
+// onload direction (slots 2-3): call after on_begin, before the own buckets
+static plex_status carry_in(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const Plan& p = *h.p;
+    if (p.carry.empty() || h.elide) return PLEX_OK;
+    plex_status st;
+    if ((st = carry_ready(c, p))) return st;
+    c->carry_used = true;
+    CK(cudaEventRecord(c->ev_cbeg, pp.kern));
+    CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_cbeg, 0));
+    CK(cudaStreamWaitEvent(c->ccopy, c->ev_cbeg, 0));
+    const RankPlan& R = *h.R;
+    int k = 0;
+    for (const CarryXfer& x : p.carry) {
+        if (x.owner != c->rank && x.carrier != c->rank) continue;
+        const int sl = 2 + k % 2;
+        uint8_t* slot = c->cstaging + (uint64_t)sl * p.bucket;
+        cudaEvent_t ta = nullptr;
+        if (x.carrier == c->rank) {
+            if (k >= 2) CK(cudaStreamWaitEvent(c->ccopy, c->ev_cs[sl], 0));      // slot's last send done
+            if ((st = tbeg(c, pp, c->ccopy, &ta))) return st;
+            CK(cudaMemcpyAsync(slot, h.slab->carry_host + x.coff, x.len, cudaMemcpyHostToDevice, c->ccopy));
+            if ((st = tend(c, pp, c->ccopy, ta, PLEX_STAT_H2D, x.len))) return st;
+            CK(cudaEventRecord(c->ev_cc[sl], c->ccopy));
+            CK(cudaStreamWaitEvent(c->cstream, c->ev_cc[sl], 0));
+            NK(ncclSend(slot, x.len, ncclUint8, x.owner, c->comm, c->cstream));
+            CK(cudaEventRecord(c->ev_cs[sl], c->cstream));
+        } else {
+            if (k >= 2) CK(cudaStreamWaitEvent(c->cstream, c->ev_cc[sl], 0));    // slot's last unpack done
+            NK(ncclRecv(slot, x.len, ncclUint8, x.carrier, c->comm, c->cstream));
+            CK(cudaEventRecord(c->ev_cs[sl], c->cstream));
+            CK(cudaStreamWaitEvent(c->ckern, c->ev_cs[sl], 0));
+            const uint64_t i0 = R.bucket_item_start[x.bucket], i1 = R.bucket_item_start[x.bucket + 1];
+            if ((st = tbeg(c, pp, c->ckern, &ta))) return st;
+            CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, slot, x.lo,
+                           h.d->cks_in, c->d_ctr + 5, c->ckern));
+            if ((st = tend(c, pp, c->ckern, ta, PLEX_STAT_UNPACK, 2 * h.d->bucket_payload[x.bucket]))) return st;
+            CK(cudaEventRecord(c->ev_cc[sl], c->ckern));
+        }
+        ++k;
+    }
+    return PLEX_OK;
+}
+
+// Before the checksum read-back (offload) / verify (onload): the half's kernel
+// stream waits for the carried buckets' pack / unpack kernels.  Enqueued after
+// the own buckets so the own pipeline never queues behind carried transfers.
+static plex_status carry_join(plex_ctx_s* c, Pipe& pp, Half& h) {
+    if (h.p->carry.empty() || h.elide || !c->ckern) return PLEX_OK;
+    CK(cudaEventRecord(c->ev_cend, c->ckern));
+    CK(cudaStreamWaitEvent(pp.kern, c->ev_cend, 0));
+    return PLEX_OK;
+}
+
 static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     const size_t np = PLEX_NUM_KINDS * h.p->tensors.size();
     const size_t ckb = 16 * std::max<size_t>(1, h.R->segs.size());
@@ -441,6 +585,7 @@ static plex_status off_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
 static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     const Plan& p = *h.p;
     const RankPlan& R = *h.R;
+    if (!h.elide && R.carried[b]) return PLEX_OK;            // moved through another rank's host link
     const int slot = b % pp.n_slots;
     uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
     const uint64_t lo = h.base + (uint64_t)b * p.bucket;
@@ -482,6 +627,7 @@ static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
 static plex_status on_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
     const Plan& p = *h.p;
     const RankPlan& R = *h.R;
+    if (!h.elide && R.carried[b]) return PLEX_OK;            // comes back through another rank
     const int slot = b % pp.n_slots;
     uint8_t* stg = pp.staging + (uint64_t)slot * p.bucket;
     const uint64_t lo = h.base + (uint64_t)b * p.bucket;
@@ -643,6 +789,8 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     if (c->copy) cudaStreamSynchronize(c->copy);
     if (c->copy2) cudaStreamSynchronize(c->copy2);
     if (c->kasync) cudaStreamSynchronize(c->kasync);
+    for (cudaStream_t s2 : {c->ckern, c->cstream, c->ccopy})
+        if (s2) cudaStreamSynchronize(s2);
     if (c->copy3) cudaStreamSynchronize(c->copy3);
     for (auto& a : c->async) {
         if (a) { a->slab->busy = false; async_free(a); a = nullptr; }
@@ -666,6 +814,14 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     for (cudaEvent_t e : c->ev_copy2) cudaEventDestroy(e);
     if (c->copy2) cudaStreamDestroy(c->copy2);
     if (c->kasync) cudaStreamDestroy(c->kasync);
+    for (cudaStream_t s2 : {c->ckern, c->cstream, c->ccopy})
+        if (s2) cudaStreamDestroy(s2);
+    for (int i = 0; i < 4; ++i) {
+        if (c->ev_cs[i]) cudaEventDestroy(c->ev_cs[i]);
+        if (c->ev_cc[i]) cudaEventDestroy(c->ev_cc[i]);
+    }
+    if (c->ev_cbeg) cudaEventDestroy(c->ev_cbeg);
+    if (c->ev_cend) cudaEventDestroy(c->ev_cend);
     if (c->copy3) cudaStreamDestroy(c->copy3);
     for (cudaEvent_t e : c->ev_pack3) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy3) cudaEventDestroy(e);
@@ -698,6 +854,16 @@ plex_status plex_plan_destroy(plex_plan_t plan) {
     return PLEX_OK;
 }
 
+plex_status plex_ctx_set_carry_staging(plex_ctx_t c, void* staging, uint64_t bytes) {
+    if (!c || (bytes && !staging) || (reinterpret_cast<uintptr_t>(staging) % 256)) {
+        set_error("bad carry staging");
+        return PLEX_E_INVAL;
+    }
+    c->cstaging = reinterpret_cast<uint8_t*>(staging);
+    c->cstaging_bytes = bytes;
+    return PLEX_OK;
+}
+
 plex_status plex_ctx_stats(plex_ctx_t c, int32_t which, plex_kernel_stats* out) {
     if (!c || !out || which < 0 || which >= PLEX_NUM_STATS) { set_error("bad stats query"); return PLEX_E_INVAL; }
     *out = c->stats[which];
@@ -719,6 +885,8 @@ plex_status plex_ctx_trace(plex_ctx_t c, plex_launch_record* out, int32_t cap, i
 }
 
 // ---- slabs ("the host tier uses pinned memory") ---------------
+static void slab_unpin(plex_slab_s* s);
+
 static plex_status slab_pin(plex_slab_s* s) {
     const size_t want = std::max<uint64_t>(s->bytes, 4096);
     if (s->flags & PLEX_SLAB_HUGEPAGE) {
@@ -752,10 +920,25 @@ static plex_status slab_pin(plex_slab_s* s) {
         s->map_bytes = n;
         s->registered = false;
     }
+    if (s->carry_bytes) {                       // other ranks' carried buckets (NEXT-1 balancing)
+        cudaError_t e = cudaHostAlloc(&s->carry_host, s->carry_bytes, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            s->carry_host = nullptr;
+            slab_unpin(s);
+            set_error("cudaHostAlloc(%llu B carry region): %s", (unsigned long long)s->carry_bytes,
+                      cudaGetErrorString(e));
+            return PLEX_E_TIER_FULL;
+        }
+    }
     return PLEX_OK;
 }
 
 static void slab_unpin(plex_slab_s* s) {
+    if (s->carry_host) {
+        cudaFreeHost(s->carry_host);
+        s->carry_host = nullptr;
+    }
     if (!s->host) return;
     if (s->registered) {
         cudaHostUnregister(s->host);
@@ -775,6 +958,7 @@ plex_status plex_slab_create(plex_plan_t plan, int32_t rank, uint32_t flags, ple
     s->rank = rank;
     s->bytes = R.slab_bytes;
     s->flags = flags;
+    s->carry_bytes = R.carry_bytes;
     s->cks.assign(2 * R.segs.size(), 0);
     plex_status st = slab_pin(s);
     if (st) {
@@ -831,6 +1015,7 @@ static plex_status pio(bool write, int fd, uint8_t* buf, size_t n, int threads) 
 plex_status plex_slab_spill(plex_slab_t s, const char* path, int32_t threads) {
     if (!s || !path) { set_error("NULL slab/path"); return PLEX_E_INVAL; }
     if (s->residency != PLEX_RES_HOST || !s->host || s->busy) { set_error("spill needs a HOST-resident, idle slab"); return PLEX_E_STATE; }
+    if (s->carry_bytes) { set_error("spill of a slab with a carry region is not supported"); return PLEX_E_INVAL; }
     const size_t n = align_up(std::max<uint64_t>(s->bytes, 1), 4096);
     int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | O_DIRECT, 0600);
     if (fd < 0) { set_error("open(%s, O_DIRECT): %s", path, strerror(errno)); return PLEX_E_INVAL; }
@@ -868,6 +1053,13 @@ plex_status plex_slab_info(plex_slab_t s, void** host_ptr, uint64_t* bytes, int3
     return PLEX_OK;
 }
 
+plex_status plex_slab_carry(plex_slab_t s, void** host_ptr, uint64_t* bytes) {
+    if (!s) { set_error("NULL slab"); return PLEX_E_INVAL; }
+    if (host_ptr) *host_ptr = s->carry_host;
+    if (bytes) *bytes = s->carry_bytes;
+    return PLEX_OK;
+}
+
 plex_status plex_slab_elided(plex_slab_t s, int32_t* elided) {
     if (!s || !elided) { set_error("NULL argument"); return PLEX_E_INVAL; }
     *elided = s->elided ? 1 : 0;
@@ -897,10 +1089,10 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
-    if ((st = off_begin(c, pp, h))) return st;
+    if ((st = off_begin(c, pp, h)) || (st = carry_out(c, pp, h))) return st;
     for (int32_t b = 0; b < h.nb; ++b)
         if ((st = off_bucket(c, pp, h, b))) return st;
-    if ((st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
+    if ((st = carry_join(c, pp, h)) || (st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
     slab->cks.swap(h.cks);
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
@@ -930,10 +1122,10 @@ plex_status plex_state_onload(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab, 
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     CK(cudaStreamWaitEvent(c->copy, c->ev_caller, 0));
-    if ((st = on_begin(c, pp, h))) return st;
+    if ((st = on_begin(c, pp, h)) || (st = carry_in(c, pp, h))) return st;
     for (int32_t b = 0; b < h.nb; ++b)
         if ((st = on_bucket(c, pp, h, b))) return st;
-    if ((st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
+    if ((st = carry_join(c, pp, h)) || (st = on_end(c, pp, h)) || (st = finish(c, caller))) return st;
     if (*pp.h_flag) {
         set_error("onload: %d segment checksum(s) differ from offload", *pp.h_flag);
         return PLEX_E_CHECKSUM;
@@ -999,15 +1191,15 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
-    if (do_off && (st = off_begin(c, po, ho))) return st;
-    if (do_on && (st = on_begin(c, pi, hi))) return st;
+    if (do_off && ((st = off_begin(c, po, ho)) || (st = carry_out(c, po, ho)))) return st;
+    if (do_on && ((st = on_begin(c, pi, hi)) || (st = carry_in(c, pi, hi)))) return st;
     const int32_t no = do_off ? ho.nb : 0, ni = do_on ? hi.nb : 0;
     for (int32_t k = 0; k < std::max(no, ni); ++k) {   // interleave so both directions start at once
         if (k < no && (st = off_bucket(c, po, ho, k))) return st;
         if (k < ni && (st = on_bucket(c, pi, hi, k))) return st;
     }
-    if (do_off && (st = off_end(c, po, ho))) return st;
-    if (do_on && (st = on_end(c, pi, hi))) return st;
+    if (do_off && ((st = carry_join(c, po, ho)) || (st = off_end(c, po, ho)))) return st;
+    if (do_on && ((st = carry_join(c, pi, hi)) || (st = on_end(c, pi, hi)))) return st;
     CK(cudaEventRecord(c->ev_pack_done, c->copy2));
     CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
     CK(cudaStreamSynchronize(c->copy2));
@@ -1064,6 +1256,7 @@ plex_status plex_state_drain(plex_ctx_t c, plex_plan_t plan, const void* const* 
     plex_status st = check_common(c, plan);
     if (st || (st = check_slab(c, plan, slab))) return st;
     if (c->async[0]) { set_error("a drain is already in flight"); return PLEX_E_STATE; }
+    if (!plan->p.carry.empty()) { set_error("async drain does not support carried buckets"); return PLEX_E_INVAL; }
     if (slab->residency != PLEX_RES_DEVICE) return PLEX_OK;      // already offloaded: nothing to drain
     if ((uint64_t)c->n_slots * plan->p.bucket > c->staging_bytes / 2) {
         set_error("async transfers need staging >= 2 x n_slots x bucket");
@@ -1112,6 +1305,7 @@ plex_status plex_state_prefetch(plex_ctx_t c, plex_plan_t plan, plex_slab_t slab
     plex_status st = check_common(c, plan);
     if (st || (st = check_slab(c, plan, slab))) return st;
     if (c->async[1]) { set_error("a prefetch is already in flight"); return PLEX_E_STATE; }
+    if (!plan->p.carry.empty()) { set_error("async prefetch does not support carried buckets"); return PLEX_E_INVAL; }
     if (slab->residency == PLEX_RES_DEVICE) {
         if (!slab->written) { set_error("slab holds no offloaded state"); return PLEX_E_STATE; }
         return PLEX_OK;

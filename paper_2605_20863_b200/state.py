@@ -90,7 +90,8 @@ class Plan:
                  rank_map: int = L.RANKMAP_TP_FAST, slab_layout: int = L.SLAB_KIND_MAJOR,
                  kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
                  bucket_bytes: int = 2 << 30, tile_bytes: int = 64 << 10,
-                 resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE, elide_param: bool = False):
+                 resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE, elide_param: bool = False,
+                 link_weights: Optional[Sequence[float]] = None):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
         descs, self.group_names = describe(self.manifest, head_dim)
@@ -108,9 +109,12 @@ class Plan:
             sub = (C.c_int32 * max(1, len(idx)))(*idx)
             n_sub = len(idx)
         self._sub = sub
+        self._lw = None
+        if link_weights is not None:
+            self._lw = (C.c_float * world)(*[float(x) for x in link_weights])
         req = L.PlanReq(len(descs), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
                         bucket_bytes, tile_bytes, resident_job, incoming_job, op,
-                        L.PLAN_ELIDE_PARAM if elide_param else 0)
+                        L.PLAN_ELIDE_PARAM if elide_param else 0, self._lw)
         h = C.c_void_p()
         check(lib.plex_transition_plan(C.byref(req), C.byref(h)))
         self.h = h
@@ -188,6 +192,17 @@ class Plan:
         return sum(1 for d in self.descs if d["key"].startswith(pre + "mlp.experts.")
                    and d["key"].endswith("down_proj.weight"))
 
+    def carry(self) -> List[L.CarryDesc]:
+        """Carried buckets (NEXT-1 host-link balancing), in the plan's global order."""
+        n = C.c_int32()
+        check(lib.plex_plan_n_carry(self.h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            d = L.CarryDesc()
+            check(lib.plex_plan_carry(self.h, i, C.byref(d)))
+            out.append(d)
+        return out
+
     def ledger(self) -> np.ndarray:
         n = self.world * self.world
         buf = (C.c_uint64 * n)()
@@ -241,6 +256,14 @@ class Slab:
     def fill(self, path: str, threads: int = 8) -> None:
         """NEXT-4: bring a spilled slab back into pinned host memory."""
         check(lib.plex_slab_fill(self.h, path.encode(), threads))
+
+    def carry_bytes(self) -> np.ndarray:
+        """Pinned carry region (other ranks' carried buckets) as a NumPy view."""
+        p, n = C.c_void_p(), C.c_uint64()
+        check(lib.plex_slab_carry(self.h, C.byref(p), C.byref(n)))
+        if not p.value or not n.value:
+            return np.zeros(0, dtype=np.uint8)
+        return np.ctypeslib.as_array((C.c_uint8 * n.value).from_address(p.value))
 
     def checksums(self) -> np.ndarray:
         n = 2 * self.plan.rank_info(self.rank).n_segments
@@ -449,6 +472,15 @@ class StateManager:
             n = int(np.prod(shape))
             out[name] = arena[off:off + 2 * n].view(torch.bfloat16).view(shape)
         return out
+
+    def enable_carry(self, plan: Plan) -> None:
+        """Give the ctx carry staging (4 bucket slots) if `plan` carries buckets."""
+        if not plan.carry():
+            return
+        need = 4 * plan.bucket_bytes
+        if getattr(self, "carry_staging", None) is None or self.carry_staging.numel() < need:
+            self.carry_staging = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+            check(lib.plex_ctx_set_carry_staging(self.h, self.carry_staging.data_ptr(), self.carry_staging.numel()))
 
     def stats(self) -> Dict[str, dict]:
         out = {}

@@ -43,3 +43,15 @@ def test_fullsize_7b_multi_gpu(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_carried_buckets_multi_gpu(n):
+    """NEXT-1 host-link balancing: buckets carried over NVLink, bit-exact."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mp_carry_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
