@@ -161,6 +161,19 @@ typedef struct {
  * derivation is still caught (E_CHECKSUM).  Falls back to a full offload when
  * any element differs. */
 #define PLEX_PLAN_ELIDE_PARAM 0x1u
+/* NEXT-2 canonical dedup of replicated state ("deduplicating
+ * replicated state"; ZeRO-2 training): the bf16 PARAM tensors
+ * are replicated on every rank of the world (master / m / v stay FSDP-N dim-0
+ * chunks).  Each rank's slab still holds only its own FSDP rows of every
+ * param, so the slab bytes are those of the sharded plan and a replica is
+ * moved over the host link exactly once per group (1/world of it per rank).
+ * State pointers of kind PARAM are then the FULL replicated tensors (row 0);
+ * offload/onload read/write this rank's rows of them, and
+ * plex_param_allgather restores the other ranks' rows over NVLink.  The
+ * replicated params live in one per-rank bf16 "param arena" whose layout is
+ * given by plex_plan_param_arena (every tensor at a 256-B-aligned offset, in
+ * manifest order). */
+#define PLEX_PLAN_REPLICA_PARAM 0x2u
 
 typedef struct {
     int32_t n_ops;               /* transition op list       */
@@ -190,6 +203,9 @@ typedef struct {
     int32_t carried_out;         /* own buckets carried by other ranks      */
     int32_t carried_in;          /* other ranks' buckets this rank carries  */
     uint64_t carry_bytes;        /* pinned carry region this rank hosts     */
+    uint64_t n_gather_items;     /* PLEX_PLAN_REPLICA_PARAM: all-gather push items */
+    uint64_t gather_send_bytes;  /* ... bf16 bytes this rank stores into peers */
+    uint64_t gather_recv_bytes;  /* ... bf16 bytes peers store into this rank  */
 } plex_rank_info;
 
 typedef struct {                 /* one carried bucket (global plan order)  */
@@ -237,7 +253,8 @@ typedef struct {
 #define PLEX_STAT_RUNPACK 7      /* K5 reshard-unpack (NCCL path) */
 #define PLEX_STAT_DERIVE  8      /* NEXT-2 param check / re-derivation */
 #define PLEX_STAT_BARRIER 9      /* sync entry barrier (time spent waiting for the slowest rank) */
-#define PLEX_NUM_STATS    10
+#define PLEX_STAT_GATHER  10     /* NEXT-2 replicated-param all-gather push */
+#define PLEX_NUM_STATS    11
 
 /* ---- errors / version ---------------------------------------------------- */
 PLEX_API const char* plex_last_error(void);
@@ -260,6 +277,10 @@ PLEX_API plex_status plex_plan_carry(plex_plan_t plan, int32_t i, plex_carry_des
 /* bytes[r * world + g]: bf16 bytes source rank r contributes to rollout rank g
  * (diagonal = local).  The zero-redundancy ledger of PAPER.md:576. */
 PLEX_API plex_status plex_plan_ledger(plex_plan_t plan, uint64_t* bytes, int32_t n);
+/* PLEX_PLAN_REPLICA_PARAM: byte offset of tensor t's bf16 replica in the param
+ * arena (t < 0: only *arena_bytes), and the arena size.  E_INVAL for plans
+ * without the flag. */
+PLEX_API plex_status plex_plan_param_arena(plex_plan_t plan, int32_t t, uint64_t* offset, uint64_t* arena_bytes);
 
 /* ---- lifecycle ------------------------------------------------------------ */
 /* 128-byte NCCL unique id for bootstrapping (rank 0 calls it and broadcasts). */
@@ -385,6 +406,20 @@ PLEX_API plex_status plex_weight_sync(plex_ctx_t ctx, plex_plan_t plan, const vo
  * and by plex_weight_sync itself.  Ordered on stream, blocking. */
 PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, const void* const* src_master,
                                   int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream);
+
+/* ---- NEXT-2: replicated-param restore (PLEX_PLAN_REPLICA_PARAM) ----------- */
+/* Collective over the ctx's world.  param_arena = this rank's bf16 param
+ * arena (plex_plan_param_arena layout) whose own FSDP rows of every tensor
+ * in the plan's key subset are valid (e.g. just onloaded).  Every rank stores
+ * its own rows straight into every peer's arena over NVLink (peer-mapped),
+ * so on return every arena holds the full replicated params; each row is
+ * sent once to each peer (the all-gather of PAPER.md:508's deduplicated
+ * state).  Ordered after prior work on caller_stream; blocking. */
+PLEX_API plex_status plex_param_allgather(plex_ctx_t ctx, plex_plan_t plan, void* param_arena, void* caller_stream);
+/* One rank's share into explicitly given arenas (arenas[g], g < world, on
+ * ctx's device): single-GPU emulation counterpart, not collective. */
+PLEX_API plex_status plex_param_allgather_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, void* const* arenas,
+                                               int32_t n_arenas, void* stream);
 
 /* ---- NEXT-3: sync from the offloaded canonical state ---------------------- */
 /* The sync of a SUSPENDED job, materialised "directly from managed memory"

@@ -164,6 +164,43 @@ def segment_checksums(segs: Sequence[Segment],
 
 
 # ---------------------------------------------------------------------------
+# NEXT-2 — canonical dedup of replicated state ("deduplicating
+# replicated state"; ZeRO-2 training with DP-replicated weights, PAPER.md:587;
+# reading R18: the replicated bf16 params are stored once per group, rank r
+# keeping its FSDP rows, and restored by gathering every rank's rows)
+# ---------------------------------------------------------------------------
+def dedup_param_shards(replicas: Sequence["OrderedDict[str, np.ndarray]"], rank: int) -> "OrderedDict[str, np.ndarray]":
+    """What rank `rank` stores of the replicated params: its FSDP rows (R2) of
+    its replica.  Replicas must be identical -- the dedup is only defined then."""
+    world = len(replicas)
+    out = OrderedDict()
+    for key, x in replicas[rank].items():
+        for other in replicas:
+            assert np.array_equal(other[key], x), f"replicas of {key} differ"
+        out[key] = shard(x, world, rank)
+    return out
+
+
+def restore_replicas(stored: Sequence["OrderedDict[str, np.ndarray]"]) -> List["OrderedDict[str, np.ndarray]"]:
+    """Inverse of dedup_param_shards: every rank gets the concatenation of all
+    ranks' stored rows (an all-gather along dim 0)."""
+    full = OrderedDict((key, gather([st[key] for st in stored])) for key in stored[0])
+    return [OrderedDict((k, v.copy()) for k, v in full.items()) for _ in stored]
+
+
+def param_arena_layout(manifest: Sequence[Tuple[str, Tuple[int, ...]]]) -> Tuple[List[int], int]:
+    """Byte offset of every manifest tensor's full bf16 replica in a rank's param
+    arena (manifest order, each at the next 256-B boundary, R4's alignment) and
+    the arena size."""
+    offs, cur = [], 0
+    for _, s in manifest:
+        off = _align(cur)
+        offs.append(off)
+        cur = off + int(np.prod(s)) * ELEM_BYTES[KIND_PARAM]
+    return offs, _align(cur)
+
+
+# ---------------------------------------------------------------------------
 # o7 — rollout layout (PAPER.md:576 "each rollout rank fetches only the tensor
 # slices required by its target parallel layout"; PAPER.md:510; layout: R3)
 # ---------------------------------------------------------------------------

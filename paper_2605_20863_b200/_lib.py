@@ -24,10 +24,11 @@ RES_DEVICE, RES_HOST, RES_DISK = 0, 1, 2
 CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
 SLAB_HUGEPAGE = 0x1
 STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE, \
-    STAT_BARRIER = range(10)
-STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive", "barrier")
-NUM_STATS = 10
+    STAT_BARRIER, STAT_GATHER = range(11)
+STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive", "barrier", "gather")
+NUM_STATS = 11
 PLAN_ELIDE_PARAM = 0x1
+PLAN_REPLICA_PARAM = 0x2
 
 EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
@@ -40,6 +41,7 @@ EXPORTS = [
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync",
     "plex_state_drain", "plex_state_prefetch", "plex_state_wait", "plex_state_poll", "plex_weight_sync_rank",
     "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
+    "plex_plan_param_arena", "plex_param_allgather", "plex_param_allgather_rank",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
 
@@ -77,7 +79,8 @@ class RankInfo(C.Structure):
                 ("n_dst_tensors", C.c_int32), ("n_push_items", C.c_uint64), ("send_bytes", C.c_uint64),
                 ("recv_bytes", C.c_uint64), ("local_bytes", C.c_uint64), ("src_read_bytes", C.c_uint64),
                 ("elide_buckets", C.c_int32), ("elide_bytes", C.c_uint64), ("carried_out", C.c_int32),
-                ("carried_in", C.c_int32), ("carry_bytes", C.c_uint64)]
+                ("carried_in", C.c_int32), ("carry_bytes", C.c_uint64), ("n_gather_items", C.c_uint64),
+                ("gather_send_bytes", C.c_uint64), ("gather_recv_bytes", C.c_uint64)]
 
 
 class CarryDesc(C.Structure):
@@ -147,6 +150,9 @@ def _load() -> C.CDLL:
         "plex_weight_sync_rank": (C.c_int, [VP, VP, I32, P(VP), I32, P(VP), I32, VP]),
         "plex_weight_sync_from_slab": (C.c_int, [VP, VP, VP, VP, VP]),
         "plex_weight_sync_rank_from_slab": (C.c_int, [VP, VP, I32, VP, P(VP), I32, VP]),
+        "plex_plan_param_arena": (C.c_int, [VP, I32, P(U64), P(U64)]),
+        "plex_param_allgather": (C.c_int, [VP, VP, VP, VP]),
+        "plex_param_allgather_rank": (C.c_int, [VP, VP, I32, P(VP), I32, VP]),
         "plex_synth_fill": (C.c_int, [VP, I32, U64, C.c_char_p, U64, U64, I32, VP]),
         "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
         "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),

@@ -96,6 +96,9 @@ struct RankPlan {
     int32_t carried_out = 0, carried_in = 0;
     uint64_t carry_bytes = 0;
     uint64_t send_bytes = 0, recv_bytes = 0, local_bytes = 0, src_read_bytes = 0;
+    // NEXT-2 replicated params: this rank's rows of every param pushed to every peer
+    std::vector<PushItem> gather;
+    uint64_t gather_send = 0, gather_recv = 0;
 };
 
 struct CarryXfer {       // a whole bucket of `owner`'s slab moved through `carrier`'s host link
@@ -114,6 +117,8 @@ struct Plan {
     std::vector<int32_t> subset;                // sorted tensor indices in the slab
     std::vector<RankPlan> ranks;
     std::vector<uint64_t> ledger;               // world * world
+    std::vector<uint64_t> param_off;            // PLEX_PLAN_REPLICA_PARAM: param arena offsets
+    uint64_t param_arena_bytes = 0;
     plex_plan_stats stats{};
     uint64_t id = 0;                            // unique per plan (device cache key)
 };

@@ -370,6 +370,42 @@ static plex_status build_carry(Plan& p, const float* w) {
     return PLEX_OK;
 }
 
+// NEXT-2 canonical dedup of the replicated bf16 params (ZeRO-2
+// at :587): the slab keeps each rank's FSDP rows only; after onload every rank
+// stores its rows of every param into every peer's param arena.  Items are
+// contiguous runs of one tile, cycled over the peers so every link is busy for
+// the whole kernel.
+static plex_status build_replica(Plan& p) {
+    if (!(p.kind_mask & (1u << PLEX_KIND_PARAM))) { set_error("REPLICA_PARAM needs the PARAM kind"); return PLEX_E_INVAL; }
+    uint64_t cur = 0;
+    p.param_off.resize(p.tensors.size());
+    for (size_t t = 0; t < p.tensors.size(); ++t) {
+        p.param_off[t] = align_up(cur, kSegAlign);
+        cur = p.param_off[t] + (uint64_t)p.tensors[t].d0 * (uint64_t)p.tensors[t].d1 * 2;
+    }
+    p.param_arena_bytes = align_up(cur, kSegAlign);
+    const uint64_t tile_elems = std::max<uint64_t>(8, p.tile / 2);
+    for (int32_t r = 0; r < p.world; ++r) {
+        RankPlan& R = p.ranks[r];
+        for (int32_t t : p.subset) {
+            const Tensor& T = p.tensors[t];
+            int64_t a, b;
+            fsdp_rows(T.d0, p.world, r, &a, &b);
+            const uint64_t n = (uint64_t)(b - a) * (uint64_t)T.d1;
+            const uint64_t e0 = p.param_off[t] / 2 + (uint64_t)a * (uint64_t)T.d1;
+            for (uint64_t o = 0; o < n; o += tile_elems) {
+                const uint32_t c = (uint32_t)std::min(tile_elems, n - o);
+                for (int32_t k = 1; k < p.world; ++k)
+                    R.gather.push_back(PushItem{e0 + o, e0 + o, 0, (uint32_t)((r + k) % p.world), 1, c, c, c});
+            }
+            R.gather_send += n * 2 * (uint64_t)(p.world - 1);
+            for (int32_t g = 0; g < p.world; ++g)
+                if (g != r) p.ranks[g].gather_recv += n * 2;
+        }
+    }
+    return PLEX_OK;
+}
+
 static plex_status build(const plex_plan_req* q, Plan& p) {
     if (!q || q->n_tensors <= 0 || !q->tensors) { set_error("empty manifest"); return PLEX_E_INVAL; }
     if (q->world < 1) { set_error("world must be >= 1"); return PLEX_E_INVAL; }
@@ -385,6 +421,7 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
         set_error("bucket/tile must be multiples of 256 B (tile < 2 GiB)"); return PLEX_E_INVAL;
     }
     if (p.kind_mask & ~PLEX_KINDMASK_ALL) { set_error("bad kind mask"); return PLEX_E_INVAL; }
+    if (p.flags & ~(PLEX_PLAN_ELIDE_PARAM | PLEX_PLAN_REPLICA_PARAM)) { set_error("bad plan flags"); return PLEX_E_INVAL; }
     if (p.layout != PLEX_SLAB_KIND_MAJOR && p.layout != PLEX_SLAB_KEY_MAJOR) { set_error("bad slab layout"); return PLEX_E_INVAL; }
     if (p.rank_map != PLEX_RANKMAP_TP_FAST && p.rank_map != PLEX_RANKMAP_DP_FAST && p.rank_map != PLEX_RANKMAP_AUTO) {
         set_error("bad rank map");
@@ -438,6 +475,10 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
     }
     p.ledger.assign((size_t)p.world * p.world, 0);
     for (RankPlan& R : p.ranks) R.carried.assign(n_buckets(p, R), 0);
+    if (p.flags & PLEX_PLAN_REPLICA_PARAM) {
+        plex_status s2 = build_replica(p);
+        if (s2) return s2;
+    }
     if (q->link_weights && p.world > 1) {
         if (p.flags & PLEX_PLAN_ELIDE_PARAM) { set_error("link balancing and param elision are exclusive"); return PLEX_E_INVAL; }
         plex_status s2 = build_carry(p, q->link_weights);
@@ -524,6 +565,9 @@ plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* 
     o.carried_out = R.carried_out;
     o.carried_in = R.carried_in;
     o.carry_bytes = R.carry_bytes;
+    o.n_gather_items = R.gather.size();
+    o.gather_send_bytes = R.gather_send;
+    o.gather_recv_bytes = R.gather_recv;
     *out = o;
     return PLEX_OK;
 }
@@ -577,6 +621,16 @@ plex_status plex_plan_ledger(plex_plan_t plan, uint64_t* bytes, int32_t n) {
     const Plan& p = plan->p;
     if (n != p.world * p.world) { set_error("ledger needs world*world = %d entries", p.world * p.world); return PLEX_E_INVAL; }
     std::memcpy(bytes, p.ledger.data(), sizeof(uint64_t) * p.ledger.size());
+    return PLEX_OK;
+}
+
+plex_status plex_plan_param_arena(plex_plan_t plan, int32_t t, uint64_t* offset, uint64_t* arena_bytes) {
+    if (!plan) { set_error("NULL plan"); return PLEX_E_INVAL; }
+    const Plan& p = plan->p;
+    if (!(p.flags & PLEX_PLAN_REPLICA_PARAM)) { set_error("plan has no replicated params"); return PLEX_E_INVAL; }
+    if (t >= (int32_t)p.tensors.size()) { set_error("tensor %d out of range", t); return PLEX_E_INVAL; }
+    if (offset) *offset = t >= 0 ? p.param_off[t] : 0;
+    if (arena_bytes) *arena_bytes = p.param_arena_bytes;
     return PLEX_OK;
 }
 

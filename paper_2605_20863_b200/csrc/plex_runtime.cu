@@ -72,6 +72,7 @@ struct DevPlan {
     SegDev* segs = nullptr;
     PackItem* items = nullptr;
     PushItem* push = nullptr;
+    PushItem* gather = nullptr;               // NEXT-2 replicated-param all-gather items
     unsigned long long* cks = nullptr;        // computed (S1,S2) per segment
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
     unsigned long long* cks_in = nullptr;     // recomputed at onload
@@ -153,9 +154,10 @@ struct plex_ctx_s {
     uint8_t* h_scratch = nullptr;
     size_t scratch_bytes = 0;
     // peer arenas opened over CUDA IPC: rank -> (peer's buffer id, mapped base)
+    // peer mappings per (arena role, rank): role 0 = rollout arena, 1 = param arena
     std::map<int, std::pair<uint64_t, void*>> peers;
-    uint64_t my_buffer_id = 0;          // arena last exported (and its cached handle)
-    cudaIpcMemHandle_t my_handle{};
+    uint64_t my_buffer_id[2] = {0, 0};  // arena last exported per role (and its cached handle)
+    cudaIpcMemHandle_t my_handle[2]{};
     std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
     cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
 };
@@ -186,6 +188,7 @@ static void free_devplan(DevPlan& d) {
     cudaFree(d.segs);
     cudaFree(d.items);
     cudaFree(d.push);
+    cudaFree(d.gather);
     cudaFree(d.cks);
     cudaFree(d.cks_want);
     cudaFree(d.cks_in);
@@ -212,7 +215,7 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     DevPlan d;
     plex_status s;
     if ((s = upload(&d.segs, R.segs)) || (s = upload(&d.items, R.items)) || (s = upload(&d.push, R.push)) ||
-        (s = upload(&d.items_el, R.items_el))) {
+        (s = upload(&d.items_el, R.items_el)) || (s = upload(&d.gather, R.gather))) {
         free_devplan(d);
         return s;
     }
@@ -370,6 +373,10 @@ static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* con
             set_error("NULL pointer for tensor %u kind %u", sg.ptr_slot % (uint32_t)nt, sg.ptr_slot / (uint32_t)nt);
             return PLEX_E_INVAL;
         }
+        // NEXT-2 replicated params: the PARAM pointer is the full tensor; this
+        // rank's segment starts at its first FSDP row
+        if ((p.flags & PLEX_PLAN_REPLICA_PARAM) && sg.ptr_slot < nt && h[sg.ptr_slot])
+            h[sg.ptr_slot] += sg.index_base * sg.esize;
     }
     return PLEX_OK;
 }
@@ -1454,10 +1461,9 @@ static constexpr int kAttrBufferId = 7;      // CU_POINTER_ATTRIBUTE_BUFFER_ID
 static constexpr int kAttrRangeStart = 11;   // CU_POINTER_ATTRIBUTE_RANGE_START_ADDR
 
 // Every rank publishes (CUDA-IPC handle, process-unique buffer id, offset) of
-// its rollout arena; peers open a handle only when that (rank, buffer id) is
-// new, so steady-state syncs reuse their NVLink mappings.
-static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, std::vector<void*>& arenas) {
-    (void)p;
+// its arena of the given role; peers open a handle only when that (role, rank,
+// buffer id) is new, so steady-state calls reuse their NVLink mappings.
+static plex_status exchange_arenas(plex_ctx_s* c, int role, void* arena, std::vector<void*>& arenas) {
     static cuPointerGetAttribute_t getattr = nullptr;
     if (!getattr) {
         cudaDriverEntryPointQueryResult q;
@@ -1478,11 +1484,11 @@ static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, st
     };
     static_assert(sizeof(Pub) <= 256, "Pub");
     Pub me{};
-    if (c->my_buffer_id != bid) {
-        CK(cudaIpcGetMemHandle(&c->my_handle, reinterpret_cast<void*>(base)));
-        c->my_buffer_id = bid;
+    if (c->my_buffer_id[role] != bid) {
+        CK(cudaIpcGetMemHandle(&c->my_handle[role], reinterpret_cast<void*>(base)));
+        c->my_buffer_id[role] = bid;
     }
-    me.h = c->my_handle;
+    me.h = c->my_handle[role];
     me.offset = a - base;
     me.buffer_id = bid;
     std::memcpy(c->h_scratch, &me, sizeof(me));
@@ -1497,15 +1503,16 @@ static plex_status exchange_arenas(plex_ctx_s* c, const Plan& p, void* arena, st
         if (g == c->rank) { arenas[g] = arena; continue; }
         Pub pub;
         std::memcpy(&pub, c->h_scratch + 256 + 256 * (size_t)g, sizeof(pub));
-        auto it = c->peers.find(g);
+        const int pk = role * 4096 + g;
+        auto it = c->peers.find(pk);
         if (it == c->peers.end() || it->second.first != pub.buffer_id) {
             if (it != c->peers.end() && it->second.second) cudaIpcCloseMemHandle(it->second.second);
-            c->peers.erase(g);
+            c->peers.erase(pk);
             void* mapped = nullptr;
             CK(cudaIpcOpenMemHandle(&mapped, pub.h, cudaIpcMemLazyEnablePeerAccess));
-            c->peers[g] = {pub.buffer_id, mapped};
+            c->peers[pk] = {pub.buffer_id, mapped};
         }
-        arenas[g] = reinterpret_cast<uint8_t*>(c->peers[g].second) + pub.offset;
+        arenas[g] = reinterpret_cast<uint8_t*>(c->peers[pk].second) + pub.offset;
     }
     return PLEX_OK;
 }
@@ -1525,7 +1532,7 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
     DevPlan* d;
     if ((st = get_devplan(c, p, &d))) return st;
     std::vector<void*> arenas(1, dst_arena);
-    if (c->world > 1 && (st = exchange_arenas(c, p, dst_arena, arenas))) return st;
+    if (c->world > 1 && (st = exchange_arenas(c, 0, dst_arena, arenas))) return st;
     CK(cudaEventRecord(c->ev_caller, caller));
     CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
     int* d_bar = reinterpret_cast<int*>(c->d_scratch + 256 + 256 * (size_t)c->world);
@@ -1537,6 +1544,75 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
     }
     if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push))) return st;
     if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all pushes landed
+    return finish(c, caller);
+}
+
+// ---- NEXT-2: replicated-param restore -------------------------------------------------
+static plex_status gather_rank(plex_ctx_s* c, const Plan& p, int32_t rank, void* const* arenas, cudaStream_t s,
+                               const PushItem* d_items) {
+    const RankPlan& R = p.ranks[rank];
+    plex_status st = ensure_ptrs(c, 1 + p.world);
+    if (st) return st;
+    for (int32_t g = 0; g < p.world; ++g) {
+        if (!arenas[g]) { set_error("NULL param arena for rank %d", g); return PLEX_E_INVAL; }
+        c->h_ptrs[1 + g] = reinterpret_cast<uint64_t>(arenas[g]);
+    }
+    c->h_ptrs[0] = c->h_ptrs[1 + rank];
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, (1 + p.world) * 8, cudaMemcpyHostToDevice, s));
+    cudaEvent_t ta = nullptr;
+    if ((st = timed_begin(c, s, &ta))) return st;
+    CK(launch_push(false, d_items, R.gather.size(), c->d_ptrs, c->d_ptrs + 1, s));
+    return timed_end(c, s, ta, PLEX_STAT_GATHER, 2 * R.gather_send);
+}
+
+static plex_status check_replica(plex_ctx_s* c, plex_plan_t plan) {
+    if (!c || !plan) { set_error("NULL ctx/plan"); return PLEX_E_INVAL; }
+    if (!(plan->p.flags & PLEX_PLAN_REPLICA_PARAM)) { set_error("plan has no replicated params"); return PLEX_E_INVAL; }
+    if (plan->p.world != c->world) { set_error("plan world %d != ctx world %d", plan->p.world, c->world); return PLEX_E_INVAL; }
+    return PLEX_OK;
+}
+
+plex_status plex_param_allgather_rank(plex_ctx_t c, plex_plan_t plan, int32_t rank, void* const* arenas,
+                                      int32_t n_arenas, void* stream) {
+    plex_status st = check_replica(c, plan);
+    if (st) return st;
+    const Plan& p = plan->p;
+    if (rank < 0 || rank >= p.world || n_arenas != p.world || !arenas) { set_error("bad rank/arenas"); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    const uint64_t key = p.id ^ (0xC2B2AE3D27D4EB4Full * (uint64_t)(rank + 1));
+    auto it = c->dev.find(key);
+    if (it == c->dev.end()) {
+        DevPlan d;
+        if ((st = upload(&d.gather, p.ranks[rank].gather))) return st;
+        it = c->dev.emplace(key, d).first;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if ((st = gather_rank(c, p, rank, arenas, s, it->second.gather))) return st;
+    CK(cudaStreamSynchronize(s));
+    return timed_collect(c);
+}
+
+plex_status plex_param_allgather(plex_ctx_t c, plex_plan_t plan, void* param_arena, void* caller_stream) {
+    plex_status st = check_replica(c, plan);
+    if (st) return st;
+    const Plan& p = plan->p;
+    if (!param_arena) { set_error("NULL param arena"); return PLEX_E_INVAL; }
+    if (c->world > 1 && !c->comm) { set_error("world > 1 needs a ctx created with an NCCL id"); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    NvtxRange nv("plex_param_allgather");
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    if (c->world == 1) return PLEX_OK;
+    DevPlan* d;
+    if ((st = get_devplan(c, p, &d))) return st;
+    std::vector<void*> arenas(1, param_arena);
+    if ((st = exchange_arenas(c, 1, param_arena, arenas))) return st;
+    CK(cudaEventRecord(c->ev_caller, caller));
+    CK(cudaStreamWaitEvent(c->pack, c->ev_caller, 0));
+    int* d_bar = reinterpret_cast<int*>(c->d_scratch + 256 + 256 * (size_t)c->world);
+    // every rank's own rows are in place (each rank orders this after its onload)
+    NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));
+    if ((st = gather_rank(c, p, c->rank, arenas.data(), c->pack, d->gather))) return st;
+    NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // every store landed
     return finish(c, caller);
 }
 

@@ -91,7 +91,7 @@ class Plan:
                  kind_mask: int = L.KINDMASK_ALL, subset: Optional[Sequence[str]] = None,
                  bucket_bytes: int = 2 << 30, tile_bytes: int = 64 << 10,
                  resident_job: int = -1, incoming_job: int = -1, op: int = L.OP_NONE, elide_param: bool = False,
-                 link_weights: Optional[Sequence[float]] = None):
+                 link_weights: Optional[Sequence[float]] = None, replica_param: bool = False):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
         descs, self.group_names = describe(self.manifest, head_dim)
@@ -114,7 +114,8 @@ class Plan:
             self._lw = (C.c_float * world)(*[float(x) for x in link_weights])
         req = L.PlanReq(len(descs), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
                         bucket_bytes, tile_bytes, resident_job, incoming_job, op,
-                        L.PLAN_ELIDE_PARAM if elide_param else 0, self._lw)
+                        (L.PLAN_ELIDE_PARAM if elide_param else 0) | (L.PLAN_REPLICA_PARAM if replica_param else 0),
+                        self._lw)
         h = C.c_void_p()
         check(lib.plex_transition_plan(C.byref(req), C.byref(h)))
         self.h = h
@@ -122,6 +123,7 @@ class Plan:
         self.kind_mask = kind_mask
         self.bucket_bytes = bucket_bytes
         self.subset = None if subset is None else frozenset(subset)
+        self.replica_param = replica_param
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -201,6 +203,30 @@ class Plan:
             d = L.CarryDesc()
             check(lib.plex_plan_carry(self.h, i, C.byref(d)))
             out.append(d)
+        return out
+
+    # ---- NEXT-2 replicated params (ZeRO-2) ------------------------------------------
+    @property
+    def param_arena_bytes(self) -> int:
+        n = C.c_uint64()
+        check(lib.plex_plan_param_arena(self.h, -1, None, C.byref(n)))
+        return n.value
+
+    def param_offsets(self) -> List[int]:
+        cache = self.__dict__.setdefault("_param_off", [])
+        if not cache:
+            for t in range(len(self.manifest)):
+                o = C.c_uint64()
+                check(lib.plex_plan_param_arena(self.h, t, C.byref(o), None))
+                cache.append(o.value)
+        return cache
+
+    def param_views(self, arena: torch.Tensor) -> "OrderedDict[str, torch.Tensor]":
+        """Full replicated bf16 param of every manifest tensor, viewed in a param arena."""
+        out = OrderedDict()
+        for (key, shape), off in zip(self.manifest, self.param_offsets()):
+            n = int(np.prod(shape))
+            out[key] = arena[off:off + 2 * n].view(torch.bfloat16).view(shape)
         return out
 
     def ledger(self) -> np.ndarray:
@@ -372,6 +398,8 @@ class StateManager:
             if t.element_size() != (2 if kind == L.KIND_PARAM else 4):
                 raise ValueError(f"shard {key}/{kind}: element size {t.element_size()} does not match the kind")
             want = numels[ti]
+            if kind == L.KIND_PARAM and plan.replica_param:    # the full replicated tensor
+                want = int(np.prod(plan.manifest[ti][1]))
             if t.numel() != want:
                 raise ValueError(f"shard {key}/{kind}: {t.numel()} elements, plan expects {want} on rank {rank}")
             ptrs[kind * nt + ti] = t.data_ptr() if t.numel() else 0
@@ -460,6 +488,28 @@ class StateManager:
         ar = ptr_array([a.data_ptr() for a in arenas])
         check(lib.plex_weight_sync_rank_from_slab(self.h, plan.h, rank, slab.h, ar, len(arenas), _stream_ptr(stream)))
 
+    # ---- NEXT-2 replicated-param restore ------------------------------------------------
+    def param_arena(self, plan: Plan) -> torch.Tensor:
+        return torch.empty(max(plan.param_arena_bytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    @staticmethod
+    def _check_param_arena(plan: Plan, arena: torch.Tensor) -> None:
+        if not plan.replica_param:
+            raise ValueError("plan was not built with replica_param=True")
+        if not arena.is_cuda or arena.numel() * arena.element_size() < plan.param_arena_bytes:
+            raise ValueError(f"param arena needs {plan.param_arena_bytes} device bytes")
+
+    def param_allgather(self, plan: Plan, arena: torch.Tensor, stream=None) -> None:
+        """Collective: every rank's own param rows -> every peer's param arena (NVLink)."""
+        self._check_param_arena(plan, arena)
+        check(lib.plex_param_allgather(self.h, plan.h, arena.data_ptr(), _stream_ptr(stream)))
+
+    def param_allgather_rank(self, plan: Plan, rank: int, arenas: Sequence[torch.Tensor], stream=None) -> None:
+        for a in arenas:
+            self._check_param_arena(plan, a)
+        ar = ptr_array([a.data_ptr() for a in arenas])
+        check(lib.plex_param_allgather_rank(self.h, plan.h, rank, ar, len(arenas), _stream_ptr(stream)))
+
     # ---- helpers ---------------------------------------------------------------------
     def arena(self, plan: Plan, rank: Optional[int] = None) -> torch.Tensor:
         n = plan.rank_info(self.rank if rank is None else rank).dst_arena_bytes
@@ -541,12 +591,20 @@ class Job:
         self.slab = Slab(plan, self.rank, hugepage) if slab else None
         self.shards: "OrderedDict[Tuple[str, int], torch.Tensor]" = OrderedDict()
         self.dev = f"cuda:{mgr.device}"
+        self.param_arena: Optional[torch.Tensor] = None     # replica_param plans: full bf16 params
 
     def alloc(self, kinds=(0, 1, 2, 3)) -> "Job":
+        replica = self.plan.replica_param and L.KIND_PARAM in kinds
+        if replica:
+            self.param_arena = self.mgr.param_arena(self.plan)
+            views = self.plan.param_views(self.param_arena)
         for t, (key, _) in enumerate(self.plan.manifest):
             shp = self.plan.shard_shape(self.rank, t)
             for kd in kinds:
-                self.shards[(key, kd)] = torch.empty(shp, dtype=KIND_TORCH[kd], device=self.dev)
+                if replica and kd == L.KIND_PARAM:
+                    self.shards[(key, kd)] = views[key]
+                else:
+                    self.shards[(key, kd)] = torch.empty(shp, dtype=KIND_TORCH[kd], device=self.dev)
         return self
 
     def init_synthetic(self, special_bits: int = 0, derived_param: bool = False) -> "Job":
@@ -558,9 +616,12 @@ class Job:
             re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
             for (k2, kd), x in self.shards.items():
                 if k2 == key and not (derived_param and kd == 0):
-                    synth_fill(x, kd, self.seed, key, r0 * re_, special_bits)
+                    full = kd == L.KIND_PARAM and self.param_arena is not None
+                    synth_fill(x, kd, self.seed, key, 0 if full else r0 * re_, special_bits)
             if derived_param and (key, 0) in self.shards and (key, 1) in self.shards:
                 p, m = self.shards[(key, 0)], self.shards[(key, 1)]
+                if self.param_arena is not None:            # this rank's rows of the replica
+                    p = p.reshape(-1)[r0 * re_:r0 * re_ + m.numel()]
                 if p.numel():
                     cast_rne(m, p)
         return self
@@ -586,14 +647,26 @@ class Job:
 
     def acquire(self) -> None:
         """a5: re-allocate the slab-carried shards' device storage."""
-        for v in self.slab_shards().values():
+        if self.param_arena is not None:
+            st = self.param_arena.untyped_storage()
+            if st.nbytes() != self.param_arena.numel():
+                st.resize_(self.param_arena.numel())
+        for (key, kd), v in self.slab_shards().items():
+            if kd == L.KIND_PARAM and self.param_arena is not None:
+                continue
             need = v.numel() * v.element_size()
             if v.untyped_storage().nbytes() != need:
                 v.untyped_storage().resize_(need)
 
+    def restore_replicas(self, stream=None) -> None:
+        """NEXT-2: after an onload, fill the other ranks' rows of the replicated params."""
+        if self.param_arena is not None and self.plan.kind_mask & (1 << L.KIND_PARAM):
+            self.mgr.param_allgather(self.plan, self.param_arena, stream)
+
     def resume(self, stream=None) -> None:
         self.acquire()
         self.mgr.onload(self.plan, self.slab, self.slab_shards(), stream)
+        self.restore_replicas(stream)
 
     def prefetch(self, stream=None) -> None:
         """NEXT-1: start bringing this (HOST-resident) job back; returns at once."""
@@ -606,6 +679,7 @@ class Job:
 
     def wait_prefetch(self, stream=None) -> None:
         self.mgr.wait(L.OP_ONLOAD, stream)
+        self.restore_replicas(stream)
 
     def wait_drain(self, stream=None, release: bool = True) -> None:
         self.mgr.wait(L.OP_OFFLOAD, stream)
@@ -620,6 +694,7 @@ class Job:
                         stream)
         if release:
             self.release()
+        other.restore_replicas(stream)
 
     def sync(self, arena: torch.Tensor, stream=None) -> None:
         self.mgr.sync(self.plan, self.masters(), arena, stream)

@@ -76,6 +76,35 @@ def main():
                     print(f"[rank {rank}] restore mismatch {model} {k}", flush=True)
                     bad += 1
             del arena
+    # NEXT-2 replicated (ZeRO-2) params: dedup slab + collective NVLink all-gather,
+    # interleaved with a rollout sync so both peer-mapped arena roles stay live
+    for model in ("mid", "toy-odd"):
+        man = manifest(model)
+        hd = MODELS[model].head_dim
+        plan = mgr.plan(man, head_dim=hd, tp=1, dp=world, replica_param=True, tile_bytes=2048)
+        job = P.Job(mgr, plan, seed=33).alloc().init_synthetic(special_bits=3)
+        arena = mgr.arena(plan)
+        full = full_state(model, seed=33, special_bits=3)
+        want_sync = O.weight_sync(master_shards(full, world, O.fsdp_rows), 1, world, 1, 0, hd)[rank]
+        osh = fsdp_shards(full, world, rank, O.fsdp_rows)
+        segs, size = O.slab_layout(man, world, rank)
+        for it in range(2):
+            job.sync(arena)
+            for name, v in P.StateManager.rollout_views(plan, rank, arena).items():
+                if not np.array_equal(bits_np(v), want_sync[name]):
+                    print(f"[rank {rank}] replica-plan sync mismatch {model} {name}", flush=True)
+                    bad += 1
+            job.suspend()
+            if not np.array_equal(job.slab.host_bytes(), O.pack_slab(segs, size, osh)):
+                print(f"[rank {rank}] dedup slab mismatch {model}", flush=True)
+                bad += 1
+            job.resume()                                    # onload own rows + all-gather
+            for (k, kd), v in job.shards.items():
+                want = full[(k, kd)] if kd == 0 else osh[(k, kd)]
+                if not np.array_equal(bits_np(v), want):
+                    print(f"[rank {rank}] replica restore mismatch {model} {k}/{kd} iter {it}", flush=True)
+                    bad += 1
+        del arena, job
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()

@@ -4,6 +4,8 @@ Multi-rank layouts are emulated on one GPU (every rank's buffers on cuda:0,
 one ctx per rank; the sync's per-rank push kernels write into all ranks'
 arenas), so the full W-rank data path is covered without W GPUs.
 """
+from collections import OrderedDict
+
 import numpy as np
 import pytest
 import torch
@@ -347,6 +349,97 @@ def test_param_elision(model, W, bucket):
         for kk, x in job.shards.items():
             assert np.array_equal(bits_np(x), state[kk]), kk
         m.close()
+
+
+# ---- NEXT-2 canonical dedup of replicated (ZeRO-2) params -------------------------------------------
+@pytest.mark.parametrize("model,W,layout,elide", [("mid", 3, L.SLAB_KIND_MAJOR, False),
+                                                  ("toy-moe", 4, L.SLAB_KEY_MAJOR, False),
+                                                  ("toy-odd", 5, L.SLAB_KIND_MAJOR, True),
+                                                  ("toy", 13, L.SLAB_KIND_MAJOR, False),
+                                                  ("mid", 2, L.SLAB_KIND_MAJOR, True)])
+def test_replica_param_dedup(model, W, layout, elide):
+    """Each rank offloads only its FSDP rows of the replicated bf16 params; onload
+    + the NVLink all-gather (emulated: every rank's push into all W arenas)
+    restores every replica bit for bit (oracle dedup_param_shards / restore_replicas)."""
+    man = manifest(model)
+    plan = P.Plan(man, world=W, slab_layout=layout, bucket_bytes=1 << 14, tile_bytes=512, replica_param=True,
+                  elide_param=elide)
+    full = full_state(model, seed=21, special_bits=0 if elide else 3)
+    if elide:                                   # params == RNE(master): the derivable case
+        for (k, kd) in list(full):
+            if kd == 1:
+                full[(k, 0)] = O.rne_bf16(full[(k, 1)])
+    reps = [OrderedDict((k, full[(k, 0)]) for k, _ in man) for _ in range(W)]
+    stored = [O.dedup_param_shards(reps, r) for r in range(W)]
+    want_rep = O.restore_replicas(stored)
+    mgrs = [mgr(W, r, bucket=1 << 14) for r in range(W)]
+    slabs = []
+    for r in range(W):
+        arena = mgrs[r].param_arena(plan)
+        views = plan.param_views(arena)
+        osh = fsdp_shards(full, W, r, O.fsdp_rows)
+        sh = OrderedDict()
+        for k, _ in man:
+            for kd in range(4):
+                if kd == 0:
+                    views[k].copy_(to_dev(full[(k, 0)], 0))
+                    sh[(k, 0)] = views[k]
+                else:
+                    sh[(k, kd)] = to_dev(osh[(k, kd)], kd)
+        slab = P.Slab(plan, r)
+        mgrs[r].offload(plan, sh, slab)
+        # the dedup slab == the sharded slab of the oracle (params: own rows only)
+        for k, _ in man:
+            osh[(k, 0)] = stored[r][k]
+        segs, size = O.slab_layout(man, W, r, layout)
+        cut = plan.rank_info(r).elide_bytes if slab.elided else 0
+        assert slab.elided == (elide and layout == L.SLAB_KIND_MAJOR)
+        assert np.array_equal(slab.host_bytes()[cut:], O.pack_slab(segs, size, osh)[cut:])
+        assert np.array_equal(slab.checksums(), np.array(O.segment_checksums(segs, osh), dtype=np.uint64).reshape(-1, 2))
+        slabs.append((slab, osh))
+    # restore into fresh, garbage-filled arenas and optimizer buffers
+    arenas = [torch.full((max(256, plan.param_arena_bytes),), 0xAB, dtype=torch.uint8, device="cuda")
+              for _ in range(W)]
+    opt = []
+    for r in range(W):
+        views = plan.param_views(arenas[r])
+        slab, osh = slabs[r]
+        sh = OrderedDict()
+        for k, _ in man:
+            sh[(k, 0)] = views[k]
+            for kd in (1, 2, 3):
+                sh[(k, kd)] = torch.full_like(to_dev(osh[(k, kd)], kd), 3) if osh[(k, kd)].size \
+                    else to_dev(osh[(k, kd)], kd)
+        mgrs[r].onload(plan, slab, sh)
+        opt.append(sh)
+    for r in range(W):
+        mgrs[r].param_allgather_rank(plan, r, arenas)
+    for g in range(W):
+        views = plan.param_views(arenas[g])
+        for k, _ in man:
+            assert np.array_equal(bits_np(views[k]), want_rep[g][k]), (g, k)
+            for kd in (1, 2, 3):
+                assert np.array_equal(bits_np(opt[g][(k, kd)]), slabs[g][1][(k, kd)]), (g, k, kd)
+    for m in mgrs:
+        m.close()
+
+
+def test_replica_job_release_resume_world1():
+    man = manifest("mid")
+    m = mgr(1, 0, bucket=1 << 16)
+    plan = m.plan(man, replica_param=True)
+    job = P.Job(m, plan, seed=6).alloc().init_synthetic(special_bits=3)
+    assert job.param_arena is not None
+    before = {k: bits_np(v) for k, v in job.shards.items()}
+    full = full_state("mid", seed=6, special_bits=3)
+    for kk, x in before.items():
+        assert np.array_equal(x, full[kk]), kk      # world 1: shards are the full tensors
+    job.suspend()
+    assert job.param_arena.untyped_storage().nbytes() == 0
+    job.resume()
+    for kk, v in job.shards.items():
+        assert np.array_equal(bits_np(v), before[kk]), kk
+    m.close()
 
 
 # ---- NEXT-3 sync straight from the offloaded slab ----------------------------------------------------

@@ -490,9 +490,58 @@ def scen_multiplex(a, c: Ctx):
             "ms_per_visit": round(ms / len(schedule), 1), "clocks": clk}, a.out)
 
 
+def scen_zero2(a, c: Ctx):
+    """NEXT-2 canonical dedup under ZeRO-2: the bf16 params are
+    replicated on every rank.  naive = every rank offloads/onloads its full
+    replica plus its optimizer shards; dedup = every rank moves only its FSDP
+    rows of the replica (replica_param plan) and resume restores the rest with
+    the NVLink all-gather (plex_param_allgather).  Step = suspend + resume."""
+    man = manifest(a.model)
+    B = a.bucket_mb << 20
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=B, timing=True, duplex=False)
+    out = {}
+    # dedup
+    plan = mgr.plan(man, replica_param=True)
+    job = P.Job(mgr, plan, seed=5).alloc().init_synthetic()
+    ref = {k: P.checksum(v).cpu() for k, v in job.shards.items() if k[1] == 0}
+    mgr.reset_stats()
+    ms, clk = timed(c, lambda: (job.suspend(), job.resume()), a.steps, a.warmup)
+    st = mgr.stats()
+    ok = all(torch.equal(P.checksum(v).cpu(), ref[k]) for k, v in job.shards.items() if k[1] == 0)
+    info = plan.rank_info(c.rank)
+    n = a.steps + a.warmup
+    out["dedup"] = {"suspend_resume_ms": round(ms, 1), "host_bytes_per_rank_each_way": info.slab_bytes,
+                    "gather_ms_per_step": round(st["gather"]["ms"] / max(1, n), 2),
+                    "gather_send_bytes": info.gather_send_bytes, "replicas_restored_bit_exact": bool(c.allmin(ok))}
+    del job, plan
+    torch.cuda.empty_cache()
+    # naive: full replica through the host link on every rank
+    mgr1 = P.StateManager(device=c.local, rank=0, world=1, bucket_bytes=B, bootstrap=False, duplex=False)
+    plan_p = mgr1.plan(man, kind_mask=1 << L.KIND_PARAM)
+    plan_o = mgr.plan(man, kind_mask=L.KINDMASK_OPTIM)
+    jp = P.Job(mgr1, plan_p, seed=5, rank=0).alloc(kinds=(0,)).init_synthetic()
+    jo = P.Job(mgr, plan_o, seed=5).alloc(kinds=(1, 2, 3)).init_synthetic()
+
+    def naive():
+        jp.suspend()
+        jo.suspend()
+        jp.resume()
+        jo.resume()
+
+    ms2, _ = timed(c, naive, a.steps, a.warmup)
+    out["naive"] = {"suspend_resume_ms": round(ms2, 1),
+                    "host_bytes_per_rank_each_way": plan_p.rank_info(0).slab_bytes + plan_o.rank_info(c.rank).slab_bytes}
+    del jp, jo
+    mgr1.close()
+    c.emit({"scenario": "zero2", "model": a.model, "n_gpus": c.world, **out,
+            "host_bytes_ratio": round(out["naive"]["host_bytes_per_rank_each_way"] /
+                                      out["dedup"]["host_bytes_per_rank_each_way"], 3),
+            "speedup": round(ms2 / ms, 3), "clocks": clk}, a.out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync", "zero2"])
     ap.add_argument("--spill-dir", default="/tmp")
     ap.add_argument("--io-threads", type=int, default=8)
     ap.add_argument("--time-scale", type=float, default=0.005)
@@ -509,10 +558,10 @@ def main():
     a = ap.parse_args()
     c = Ctx(a.gpus)
     if not a.model:
-        a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b"}.get(a.scenario, "")
+        a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b", "zero2": "qwen2.5-7b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
      "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme,
-     "sync": scen_sync}[a.scenario](a, c)
+     "sync": scen_sync, "zero2": scen_zero2}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
