@@ -407,6 +407,29 @@ PLEX_API plex_status plex_weight_sync(plex_ctx_t ctx, plex_plan_t plan, const vo
 PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, const void* const* src_master,
                                   int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream);
 
+/* ---- NEXT-3: checkpoint materialisation from the offloaded state ---------- */
+/* a checkpoint is a materialisation of managed (possibly
+ * offloaded) state, written in the background off the critical path.  Writes
+ * the HOST-resident slab of `plan` (rank = the slab's) to `path` as a standard
+ * safetensors file: one tensor per slab segment in slab order, named by its
+ * logical key (PARAM, BF16) or "optimizer.<master|exp_avg|exp_avg_sq>.<key>"
+ * (F32), shaped as the rank's FSDP shard (R2), no padding; header metadata
+ * "plex.world", "plex.rank", "plex.layout" and "plex.checksums" (the R14
+ * (S1, S2) pairs recorded at offload, 16 hex digits each).  `threads` writers
+ * at disjoint offsets, then fsync.  Host-only (no CUDA call), safe to run on
+ * another thread; the slab is marked busy meanwhile (offload/onload/spill of
+ * it -> E_STATE).  E_STATE if the slab is not HOST-resident or holds elided
+ * params; E_INVAL for plans that carry this rank's buckets; E_TIER_FULL on I/O
+ * errors. */
+PLEX_API plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t slab, const char* path, int32_t threads);
+/* Inverse: fill an idle slab of `plan` from a checkpoint written by
+ * plex_slab_checkpoint for the same plan and rank; residency becomes HOST with
+ * the file's checksums, so the next onload verifies every tensor
+ * (E_CHECKSUM on corrupted data).  E_LAYOUT if the header is not exactly what
+ * this plan/rank writes (other names, shapes, order or sizes) -- the slab is
+ * then untouched; on an I/O error the slab holds no state (onload -> E_STATE). */
+PLEX_API plex_status plex_slab_restore(plex_plan_t plan, plex_slab_t slab, const char* path, int32_t threads);
+
 /* ---- NEXT-2: replicated-param restore (PLEX_PLAN_REPLICA_PARAM) ----------- */
 /* Collective over the ctx's world.  param_arena = this rank's bf16 param
  * arena (plex_plan_param_arena layout) whose own FSDP rows of every tensor

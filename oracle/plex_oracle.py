@@ -201,6 +201,30 @@ def param_arena_layout(manifest: Sequence[Tuple[str, Tuple[int, ...]]]) -> Tuple
 
 
 # ---------------------------------------------------------------------------
+# NEXT-3 — checkpoint materialisation from offloaded state (PAPER.md:510
+# "checkpointing ... materialization", :513 background checkpoint
+# materialization; format reading R19: one safetensors tensor per slab segment)
+# ---------------------------------------------------------------------------
+CKPT_KIND = {KIND_PARAM: "param", KIND_MASTER: "master", KIND_EXP_AVG: "exp_avg", KIND_EXP_AVG_SQ: "exp_avg_sq"}
+
+
+def checkpoint_name(key: str, kind: int) -> str:
+    return key if kind == KIND_PARAM else f"optimizer.{CKPT_KIND[kind]}.{key}"
+
+
+def checkpoint_tensors(segs: Sequence[Segment],
+                       shards: Dict[Tuple[str, int], np.ndarray]) -> "OrderedDict[str, np.ndarray]":
+    """The tensors a rank's checkpoint holds, in slab order: each segment's shard
+    (this rank's FSDP rows, R2) under its checkpoint name."""
+    return OrderedDict((checkpoint_name(sg.key, sg.kind), shards[(sg.key, sg.kind)]) for sg in segs)
+
+
+def checkpoint_metadata(world: int, rank: int, cks: Sequence[Tuple[int, int]]) -> Dict[str, str]:
+    return {"format": "pt", "plex.layout": "fsdp-dim0", "plex.world": str(world), "plex.rank": str(rank),
+            "plex.checksums": ",".join(f"{v:016x}" for pair in cks for v in pair)}
+
+
+# ---------------------------------------------------------------------------
 # o7 — rollout layout (PAPER.md:576 "each rollout rank fetches only the tensor
 # slices required by its target parallel layout"; PAPER.md:510; layout: R3)
 # ---------------------------------------------------------------------------

@@ -173,7 +173,7 @@ struct plex_slab_s {
     int residency = PLEX_RES_DEVICE;
     bool written = false;
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
-    bool busy = false;                  // an async drain / prefetch of this slab is in flight
+    std::atomic<bool> busy{false};      // an async drain / prefetch or a checkpoint of this slab is in flight
     uint8_t* carry_host = nullptr;      // other ranks' carried buckets (pinned)
     uint64_t carry_bytes = 0;
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
@@ -675,7 +675,7 @@ static plex_status check_slab(plex_ctx_s* c, plex_plan_t plan, plex_slab_t slab)
         set_error("slab does not belong to this plan/rank");
         return PLEX_E_INVAL;
     }
-    if (slab->busy) { set_error("an async transfer of this slab is in flight: plex_state_wait first"); return PLEX_E_STATE; }
+    if (slab->busy) { set_error("an async transfer or checkpoint of this slab is in flight"); return PLEX_E_STATE; }
     return PLEX_OK;
 }
 
@@ -1050,6 +1050,168 @@ plex_status plex_slab_fill(plex_slab_t s, const char* path, int32_t threads) {
     }
     s->residency = PLEX_RES_HOST;
     return PLEX_OK;
+}
+
+// ---- NEXT-3 checkpoint materialisation from the offloaded state -----------------------
+// checkpoints are "materialization" of managed (possibly
+// offloaded) state, done in the background off the critical path.  A HOST
+// slab is written as a standard safetensors file (u64 LE header length, JSON
+// header, raw little-endian data): one tensor per slab segment, named by its
+// logical key (PARAM, bf16) or "optimizer.<kind>.<key>" (fp32), shaped as this
+// rank's FSDP shard, data in slab order without the 256-B padding.  The
+// header metadata carries world, rank and the (S1, S2) checksums recorded at
+// offload, so a restored slab is verified by the next onload like any other.
+static const char* kCkptKind[4] = {"param", "master", "exp_avg", "exp_avg_sq"};
+
+static std::string ckpt_header(const Plan& p, int32_t rank, const std::vector<uint64_t>& cks) {
+    const RankPlan& R = p.ranks[rank];
+    std::string h = "{\"__metadata__\":{\"format\":\"pt\",\"plex.layout\":\"fsdp-dim0\",\"plex.world\":\"" +
+                    std::to_string(p.world) + "\",\"plex.rank\":\"" + std::to_string(rank) + "\",\"plex.checksums\":\"";
+    char buf[40];
+    for (size_t i = 0; i < cks.size(); ++i) {
+        snprintf(buf, sizeof(buf), "%s%016llx", i ? "," : "", (unsigned long long)cks[i]);
+        h += buf;
+    }
+    h += "\"}";
+    uint64_t off = 0;
+    for (const plex_seg_desc& d : R.seg_desc) {
+        const Tensor& T = p.tensors[d.tensor];
+        std::string name = d.kind == PLEX_KIND_PARAM ? T.key : std::string("optimizer.") + kCkptKind[d.kind] + "." + T.key;
+        std::string esc;
+        for (char ch : name) {
+            if (ch == '"' || ch == '\\') esc += '\\';
+            esc += ch;
+        }
+        h += ",\"" + esc + "\":{\"dtype\":\"" + (d.kind == PLEX_KIND_PARAM ? "BF16" : "F32") + "\",\"shape\":[" +
+             std::to_string(d.row1 - d.row0) + (T.ndim == 2 ? "," + std::to_string(T.d1) : std::string()) +
+             "],\"data_offsets\":[" + std::to_string(off) + "," + std::to_string(off + d.nbytes) + "]}";
+        off += d.nbytes;
+    }
+    h += "}";
+    while ((8 + h.size()) % 8) h += ' ';
+    return h;
+}
+
+// Segment pieces (file offset, slab offset, bytes) in <= 64 MiB chunks, run by `threads` workers.
+static plex_status ckpt_io(bool write, int fd, const RankPlan& R, uint8_t* host, uint64_t data0, int threads) {
+    struct Piece { uint64_t fo, so, n; };
+    std::vector<Piece> pcs;
+    uint64_t fo = data0;
+    for (const plex_seg_desc& d : R.seg_desc) {
+        for (uint64_t o = 0; o < d.nbytes; o += 64ull << 20)
+            pcs.push_back(Piece{fo + o, d.slab_offset + o, std::min<uint64_t>(64ull << 20, d.nbytes - o)});
+        fo += d.nbytes;
+    }
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{0};
+    auto work = [&]() {
+        for (;;) {
+            const size_t i = next.fetch_add(1);
+            if (i >= pcs.size() || err.load()) return;
+            const Piece& q = pcs[i];
+            size_t done = 0;
+            while (done < q.n) {
+                const ssize_t r = write ? pwrite(fd, host + q.so + done, q.n - done, (off_t)(q.fo + done))
+                                        : pread(fd, host + q.so + done, q.n - done, (off_t)(q.fo + done));
+                if (r <= 0) { err.store(r == 0 ? EIO : errno); return; }
+                done += (size_t)r;
+            }
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int i = 1; i < threads; ++i) ts.emplace_back(work);
+    work();
+    for (auto& t : ts) t.join();
+    if (err.load()) {
+        set_error("checkpoint %s: %s", write ? "pwrite" : "pread", strerror(err.load()));
+        return PLEX_E_TIER_FULL;
+    }
+    return PLEX_OK;
+}
+
+static plex_status ckpt_check(plex_plan_t plan, plex_slab_t s, const char* path) {
+    if (!plan || !s || !path) { set_error("NULL plan/slab/path"); return PLEX_E_INVAL; }
+    if (s->plan_id != plan->p.id) { set_error("slab does not belong to this plan"); return PLEX_E_INVAL; }
+    if (plan->p.ranks[s->rank].carried_out) { set_error("checkpoint of a slab with carried buckets is not supported"); return PLEX_E_INVAL; }
+    return PLEX_OK;
+}
+
+plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
+    plex_status st = ckpt_check(plan, s, path);
+    if (st) return st;
+    if (s->residency != PLEX_RES_HOST || !s->host || !s->written) { set_error("checkpoint needs an offloaded (HOST) slab"); return PLEX_E_STATE; }
+    if (s->elided) { set_error("slab holds derived (elided) params: offload without elision to checkpoint"); return PLEX_E_STATE; }
+    bool idle = false;
+    if (!s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
+    const Plan& p = plan->p;
+    const std::string h = ckpt_header(p, s->rank, s->cks);
+    int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) { s->busy = false; set_error("open(%s): %s", path, strerror(errno)); return PLEX_E_INVAL; }
+    uint8_t len8[8];
+    for (int i = 0; i < 8; ++i) len8[i] = (uint8_t)((uint64_t)h.size() >> (8 * i));
+    if (pwrite(fd, len8, 8, 0) != 8 || pwrite(fd, h.data(), h.size(), 8) != (ssize_t)h.size()) {
+        set_error("checkpoint header write: %s", strerror(errno));
+        st = PLEX_E_TIER_FULL;
+    }
+    if (!st) st = ckpt_io(true, fd, p.ranks[s->rank], s->host, 8 + h.size(), std::max(1, threads));
+    if (!st && fsync(fd) != 0) { set_error("fsync: %s", strerror(errno)); st = PLEX_E_TIER_FULL; }
+    close(fd);
+    s->busy = false;
+    return st;
+}
+
+plex_status plex_slab_restore(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
+    plex_status st = ckpt_check(plan, s, path);
+    if (st) return st;
+    bool idle = false;
+    if (!s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
+    const Plan& p = plan->p;
+    const RankPlan& R = p.ranks[s->rank];
+    int fd = open(path, O_RDONLY);
+    if (fd < 0) { s->busy = false; set_error("open(%s): %s", path, strerror(errno)); return PLEX_E_INVAL; }
+    auto fail = [&](plex_status code) { close(fd); s->busy = false; return code; };
+    uint8_t len8[8];
+    if (pread(fd, len8, 8, 0) != 8) { set_error("checkpoint too short"); return fail(PLEX_E_LAYOUT); }
+    uint64_t hl = 0;
+    for (int i = 0; i < 8; ++i) hl |= (uint64_t)len8[i] << (8 * i);
+    if (hl > (64ull << 20)) { set_error("checkpoint header of %llu B", (unsigned long long)hl); return fail(PLEX_E_LAYOUT); }
+    std::string h(hl, '\0');
+    if (pread(fd, &h[0], hl, 8) != (ssize_t)hl) { set_error("checkpoint header read"); return fail(PLEX_E_LAYOUT); }
+    // checksums from the metadata; the rest must be exactly what this plan/rank writes
+    std::vector<uint64_t> cks(2 * R.segs.size(), 0);
+    const std::string tag = "\"plex.checksums\":\"";
+    const size_t a = h.find(tag);
+    if (a == std::string::npos) { set_error("checkpoint carries no plex checksums"); return fail(PLEX_E_LAYOUT); }
+    size_t q = a + tag.size();
+    for (size_t i = 0; i < cks.size(); ++i) {
+        if (i && (q >= h.size() || h[q++] != ',')) { set_error("checkpoint checksum list too short"); return fail(PLEX_E_LAYOUT); }
+        if (q + 16 > h.size()) { set_error("checkpoint checksum list truncated"); return fail(PLEX_E_LAYOUT); }
+        cks[i] = strtoull(h.substr(q, 16).c_str(), nullptr, 16);
+        q += 16;
+    }
+    if (h != ckpt_header(p, s->rank, cks)) {
+        set_error("checkpoint does not match this plan/rank (tensor names, shapes or order differ)");
+        return fail(PLEX_E_LAYOUT);
+    }
+    const off_t size = lseek(fd, 0, SEEK_END);
+    if (size != (off_t)(8 + hl + R.payload_bytes)) { set_error("checkpoint data size mismatch"); return fail(PLEX_E_LAYOUT); }
+    if (!s->host && (st = slab_pin(s))) return fail(st);
+    if ((st = ckpt_io(false, fd, R, s->host, 8 + hl, std::max(1, threads)))) {
+        s->written = false;                                // the slab now holds no valid state
+        s->residency = PLEX_RES_DEVICE;
+        return fail(st);
+    }
+    uint64_t cur = 0;                                      // zero the padding (R4)
+    for (const plex_seg_desc& d : R.seg_desc) {
+        if (d.slab_offset > cur) std::memset(s->host + cur, 0, d.slab_offset - cur);
+        cur = d.slab_offset + d.nbytes;
+    }
+    if (s->bytes > cur) std::memset(s->host + cur, 0, s->bytes - cur);
+    s->cks = cks;
+    s->written = true;
+    s->elided = false;
+    s->residency = PLEX_RES_HOST;
+    return fail(PLEX_OK);
 }
 
 plex_status plex_slab_info(plex_slab_t s, void** host_ptr, uint64_t* bytes, int32_t* residency) {

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import check, lib, ptr_array
+from ._lib import PlexError, check, lib, ptr_array
 
 KIND_TORCH = {0: torch.bfloat16, 1: torch.float32, 2: torch.float32, 3: torch.float32}
 
@@ -282,6 +282,31 @@ class Slab:
     def fill(self, path: str, threads: int = 8) -> None:
         """NEXT-4: bring a spilled slab back into pinned host memory."""
         check(lib.plex_slab_fill(self.h, path.encode(), threads))
+
+    def checkpoint(self, path: str, threads: int = 8, background: bool = False):
+        """NEXT-3: materialise the offloaded state as a safetensors checkpoint
+        (PAPER.md:510, :513).  background=True runs the host-only write on a
+        thread (the library call releases the GIL) and returns it; the slab is
+        busy until it finishes."""
+        if not background:
+            check(lib.plex_slab_checkpoint(self.plan.h, self.h, path.encode(), threads))
+            return None
+        import threading
+        err = []
+
+        def run():
+            code = lib.plex_slab_checkpoint(self.plan.h, self.h, path.encode(), threads)
+            if code != L.OK:
+                err.append(PlexError(code, lib.plex_last_error().decode(errors="replace")))
+
+        th = threading.Thread(target=run, daemon=True)
+        th.errors = err
+        th.start()
+        return th
+
+    def restore(self, path: str, threads: int = 8) -> None:
+        """Fill this slab from a checkpoint of the same plan/rank (residency HOST)."""
+        check(lib.plex_slab_restore(self.plan.h, self.h, path.encode(), threads))
 
     def carry_bytes(self) -> np.ndarray:
         """Pinned carry region (other ranks' carried buckets) as a NumPy view."""

@@ -442,6 +442,88 @@ def test_replica_job_release_resume_world1():
     m.close()
 
 
+# ---- NEXT-3 checkpoint materialisation from the offloaded slab ------------------------------------
+def _load_ckpt(path):
+    import json
+    import struct
+
+    from safetensors.torch import load_file
+    with open(path, "rb") as f:
+        n = struct.unpack("<Q", f.read(8))[0]
+        hdr = json.loads(f.read(n))
+    meta = hdr.pop("__metadata__")
+    order = sorted(hdr, key=lambda k: hdr[k]["data_offsets"])     # data order in the file
+    return load_file(path), meta, order
+
+
+@pytest.mark.parametrize("model,W,layout", [("mid", 3, L.SLAB_KIND_MAJOR), ("toy-moe", 4, L.SLAB_KEY_MAJOR),
+                                            ("toy", 13, L.SLAB_KIND_MAJOR)])
+def test_slab_checkpoint_and_restore(tmp_path, model, W, layout):
+    man = manifest(model)
+    plan = P.Plan(man, world=W, slab_layout=layout, bucket_bytes=1 << 14, tile_bytes=512)
+    full = full_state(model, seed=17, special_bits=3)
+    for r in (0, W - 1):
+        m = mgr(W, r, bucket=1 << 14)
+        sh = rank_shards(plan, r, seed=17, special_bits=3)
+        slab = P.Slab(plan, r)
+        with pytest.raises(P.PlexError) as e:                  # nothing offloaded yet
+            slab.checkpoint(str(tmp_path / "x.safetensors"))
+        assert e.value.code == L.E_STATE
+        m.offload(plan, sh, slab)
+        path = str(tmp_path / f"{model}-r{r}.safetensors")
+        th = slab.checkpoint(path, threads=4, background=True)
+        th.join()
+        assert not th.errors
+        # a standard safetensors file holding exactly the oracle's tensors, in slab order
+        segs, _ = O.slab_layout(man, W, r, layout)
+        osh = fsdp_shards(full, W, r, O.fsdp_rows)
+        want = O.checkpoint_tensors(segs, osh)
+        got, meta, order = _load_ckpt(path)
+        assert order == list(want) and sorted(got) == sorted(want)
+        for name, x in want.items():
+            assert tuple(got[name].shape) == x.shape, name
+            assert got[name].dtype == (torch.bfloat16 if x.dtype == U16 else torch.float32), name
+            assert np.array_equal(bits_np(got[name]), x), name
+        assert meta == O.checkpoint_metadata(W, r, O.segment_checksums(segs, osh))
+        # restore into a fresh slab, onload into fresh buffers
+        slab2 = P.Slab(plan, r)
+        slab2.restore(path)
+        assert slab2.residency == L.RES_HOST
+        new = {k: torch.full_like(v, 5) if v.numel() else torch.empty_like(v) for k, v in sh.items()}
+        m.onload(plan, slab2, new)
+        for (key, kd), x in new.items():
+            assert np.array_equal(bits_np(x), osh[(key, kd)]), (key, kd)
+        # a flipped data byte is caught by the next onload
+        raw = bytearray(open(path, "rb").read())
+        raw[-3] ^= 0x40
+        bad = str(tmp_path / "bad.safetensors")
+        open(bad, "wb").write(bytes(raw))
+        slab3 = P.Slab(plan, r)
+        slab3.restore(bad)
+        with pytest.raises(P.PlexError) as e:
+            m.onload(plan, slab3, new)
+        assert e.value.code == L.E_CHECKSUM
+        # another plan's checkpoint is refused, the slab untouched
+        other = P.Plan(man, world=W + 1, slab_layout=layout, bucket_bytes=1 << 14)
+        with pytest.raises(P.PlexError) as e:
+            P.Slab(other, 0).restore(path)
+        assert e.value.code == L.E_LAYOUT
+        m.close()
+
+
+def test_checkpoint_refuses_elided_slab(tmp_path):
+    man = manifest("mid")
+    plan = P.Plan(man, world=1, bucket_bytes=4096, tile_bytes=512, elide_param=True)
+    m = mgr(1, 0, bucket=4096)
+    job = P.Job(m, plan, seed=2).alloc().init_synthetic(derived_param=True)
+    job.suspend()
+    assert job.slab.elided
+    with pytest.raises(P.PlexError) as e:
+        job.slab.checkpoint(str(tmp_path / "e.safetensors"))
+    assert e.value.code == L.E_STATE
+    m.close()
+
+
 # ---- NEXT-3 sync straight from the offloaded slab ----------------------------------------------------
 @pytest.mark.parametrize("model,W,tp,dp,ep,elide", [("mid", 4, 2, 2, 1, False), ("mid-moe", 4, 2, 2, 4, True),
                                                      ("toy-odd", 3, 1, 3, 1, False)])
