@@ -417,8 +417,9 @@ PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int
  * "plex.world", "plex.rank", "plex.layout" and "plex.checksums" (the R14
  * (S1, S2) pairs recorded at offload, 16 hex digits each).  `threads` writers
  * at disjoint offsets, then fsync.  Host-only (no CUDA call), safe to run on
- * another thread; the slab is marked busy meanwhile (offload/onload/spill of
- * it -> E_STATE).  E_STATE if the slab is not HOST-resident or holds elided
+ * another thread while the job resumes from the same slab: the slab is
+ * read-only meanwhile (offload into it, spill, restore -> E_STATE; onload and
+ * sync-from-slab proceed).  E_STATE if the slab is not HOST-resident or holds elided
  * params; E_INVAL for plans that carry this rank's buckets; E_TIER_FULL on I/O
  * errors. */
 PLEX_API plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t slab, const char* path, int32_t threads);

@@ -173,7 +173,8 @@ struct plex_slab_s {
     int residency = PLEX_RES_DEVICE;
     bool written = false;
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
-    std::atomic<bool> busy{false};      // an async drain / prefetch or a checkpoint of this slab is in flight
+    std::atomic<bool> busy{false};      // an async drain / prefetch or a restore of this slab is in flight
+    std::atomic<int> ckpt{0};           // checkpoints reading the slab (it is read-only meanwhile)
     uint8_t* carry_host = nullptr;      // other ranks' carried buckets (pinned)
     uint64_t carry_bytes = 0;
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
@@ -670,12 +671,13 @@ static plex_status on_end(plex_ctx_s* c, Pipe& pp, Half& h) {
     return PLEX_OK;
 }
 
-static plex_status check_slab(plex_ctx_s* c, plex_plan_t plan, plex_slab_t slab) {
+static plex_status check_slab(plex_ctx_s* c, plex_plan_t plan, plex_slab_t slab, bool write = false) {
     if (!slab || slab->plan_id != plan->p.id || slab->rank != c->rank) {
         set_error("slab does not belong to this plan/rank");
         return PLEX_E_INVAL;
     }
-    if (slab->busy) { set_error("an async transfer or checkpoint of this slab is in flight"); return PLEX_E_STATE; }
+    if (slab->busy) { set_error("an async transfer of this slab is in flight: plex_state_wait first"); return PLEX_E_STATE; }
+    if (write && slab->ckpt.load()) { set_error("a checkpoint of this slab is being written (slab is read-only)"); return PLEX_E_STATE; }
     return PLEX_OK;
 }
 
@@ -1021,7 +1023,7 @@ static plex_status pio(bool write, int fd, uint8_t* buf, size_t n, int threads) 
 
 plex_status plex_slab_spill(plex_slab_t s, const char* path, int32_t threads) {
     if (!s || !path) { set_error("NULL slab/path"); return PLEX_E_INVAL; }
-    if (s->residency != PLEX_RES_HOST || !s->host || s->busy) { set_error("spill needs a HOST-resident, idle slab"); return PLEX_E_STATE; }
+    if (s->residency != PLEX_RES_HOST || !s->host || s->busy || s->ckpt.load()) { set_error("spill needs a HOST-resident, idle slab"); return PLEX_E_STATE; }
     if (s->carry_bytes) { set_error("spill of a slab with a carry region is not supported"); return PLEX_E_INVAL; }
     const size_t n = align_up(std::max<uint64_t>(s->bytes, 1), 4096);
     int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | O_DIRECT, 0600);
@@ -1141,12 +1143,12 @@ plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* pa
     if (st) return st;
     if (s->residency != PLEX_RES_HOST || !s->host || !s->written) { set_error("checkpoint needs an offloaded (HOST) slab"); return PLEX_E_STATE; }
     if (s->elided) { set_error("slab holds derived (elided) params: offload without elision to checkpoint"); return PLEX_E_STATE; }
-    bool idle = false;
-    if (!s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
+    if (s->busy) { set_error("an async transfer of this slab is in flight"); return PLEX_E_STATE; }
+    s->ckpt.fetch_add(1);
     const Plan& p = plan->p;
     const std::string h = ckpt_header(p, s->rank, s->cks);
     int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
-    if (fd < 0) { s->busy = false; set_error("open(%s): %s", path, strerror(errno)); return PLEX_E_INVAL; }
+    if (fd < 0) { s->ckpt.fetch_sub(1); set_error("open(%s): %s", path, strerror(errno)); return PLEX_E_INVAL; }
     uint8_t len8[8];
     for (int i = 0; i < 8; ++i) len8[i] = (uint8_t)((uint64_t)h.size() >> (8 * i));
     if (pwrite(fd, len8, 8, 0) != 8 || pwrite(fd, h.data(), h.size(), 8) != (ssize_t)h.size()) {
@@ -1156,7 +1158,7 @@ plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* pa
     if (!st) st = ckpt_io(true, fd, p.ranks[s->rank], s->host, 8 + h.size(), std::max(1, threads));
     if (!st && fsync(fd) != 0) { set_error("fsync: %s", strerror(errno)); st = PLEX_E_TIER_FULL; }
     close(fd);
-    s->busy = false;
+    s->ckpt.fetch_sub(1);
     return st;
 }
 
@@ -1164,7 +1166,7 @@ plex_status plex_slab_restore(plex_plan_t plan, plex_slab_t s, const char* path,
     plex_status st = ckpt_check(plan, s, path);
     if (st) return st;
     bool idle = false;
-    if (!s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
+    if (s->ckpt.load() || !s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
     const Plan& p = plan->p;
     const RankPlan& R = p.ranks[s->rank];
     int fd = open(path, O_RDONLY);
@@ -1245,7 +1247,8 @@ plex_status plex_slab_checksums(plex_slab_t s, uint64_t* out, int32_t n) {
 plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
                                void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st || (st = check_slab(c, plan, slab)) || (st = check_no_async(c))) return st;
+    if (st || (st = check_slab(c, plan, slab, slab && slab->residency != PLEX_RES_HOST)) || (st = check_no_async(c)))
+        return st;
     if (slab->residency == PLEX_RES_HOST) return PLEX_OK;     // idempotent
     if (slab->residency == PLEX_RES_DISK) { set_error("slab is on the NVMe tier"); return PLEX_E_STATE; }
     DeviceGuard g(c->device);
@@ -1313,7 +1316,8 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
                               plex_slab_t slab_out, plex_plan_t plan_in, plex_slab_t slab_in, void* const* dst_in,
                               int32_t n_dst, void* caller_stream) {
     plex_status st = check_common(c, plan_out);
-    if (st || (st = check_common(c, plan_in)) || (st = check_slab(c, plan_out, slab_out)) ||
+    if (st || (st = check_common(c, plan_in)) ||
+        (st = check_slab(c, plan_out, slab_out, slab_out && slab_out->residency != PLEX_RES_HOST)) ||
         (st = check_slab(c, plan_in, slab_in)) || (st = check_no_async(c)))
         return st;
     if (slab_out == slab_in) { set_error("switch needs two different slabs"); return PLEX_E_INVAL; }
@@ -1423,7 +1427,7 @@ extern "C" {
 plex_status plex_state_drain(plex_ctx_t c, plex_plan_t plan, const void* const* src, int32_t n_src, plex_slab_t slab,
                              void* caller_stream) {
     plex_status st = check_common(c, plan);
-    if (st || (st = check_slab(c, plan, slab))) return st;
+    if (st || (st = check_slab(c, plan, slab, slab && slab->residency != PLEX_RES_HOST))) return st;
     if (c->async[0]) { set_error("a drain is already in flight"); return PLEX_E_STATE; }
     if (!plan->p.carry.empty()) { set_error("async drain does not support carried buckets"); return PLEX_E_INVAL; }
     if (slab->residency != PLEX_RES_DEVICE) return PLEX_OK;      // already offloaded: nothing to drain

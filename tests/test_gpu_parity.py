@@ -472,6 +472,7 @@ def test_slab_checkpoint_and_restore(tmp_path, model, W, layout):
         m.offload(plan, sh, slab)
         path = str(tmp_path / f"{model}-r{r}.safetensors")
         th = slab.checkpoint(path, threads=4, background=True)
+        m.onload(plan, slab, sh)                # resuming from the slab while it is written out is fine
         th.join()
         assert not th.errors
         # a standard safetensors file holding exactly the oracle's tensors, in slab order

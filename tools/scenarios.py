@@ -341,9 +341,31 @@ def scen_nvme(a, c: Ctx):
     t2 = time.perf_counter()
     job.resume()                                   # checksum-verified
     os.remove(path)
+    # NEXT-3 checkpoint materialisation: written in the background while the
+    # job computes (here: while it is resumed), restored into a fresh slab
+    job.suspend(release=False)
+    ck = os.path.join(a.spill_dir, f"plex_ckpt_r{c.rank}.safetensors")
+    c.barrier()
+    t3 = time.perf_counter()
+    th = job.slab.checkpoint(ck, threads=a.io_threads, background=True)
+    job.resume()
+    t4 = time.perf_counter()
+    th.join()
+    t5 = time.perf_counter()
+    assert not th.errors
+    slab2 = P.Slab(plan, c.rank)
+    t6 = time.perf_counter()
+    slab2.restore(ck, threads=a.io_threads)
+    t7 = time.perf_counter()
+    job.slab = slab2
+    job.resume()                                   # verified against the file's checksums
+    os.remove(ck)
     c.emit({"scenario": "nvme", "model": model, "n_gpus": c.world, "slab_bytes_per_rank": n,
             "spill_GBs_per_rank": round(n / (c.allmax(t1 - t0)) / 1e9, 2),
-            "fill_GBs_per_rank": round(n / (c.allmax(t2 - t1)) / 1e9, 2), "io_threads": a.io_threads,
+            "fill_GBs_per_rank": round(n / (c.allmax(t2 - t1)) / 1e9, 2),
+            "checkpoint_GBs_per_rank": round(n / (c.allmax(t5 - t3)) / 1e9, 2),
+            "resume_during_checkpoint_ms": round(1e3 * c.allmax(t4 - t3), 1),
+            "restore_GBs_per_rank": round(n / (c.allmax(t7 - t6)) / 1e9, 2), "io_threads": a.io_threads,
             "dir": a.spill_dir}, a.out)
 
 
