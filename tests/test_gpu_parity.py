@@ -494,6 +494,9 @@ def test_slab_checkpoint_and_restore(tmp_path, model, W, layout):
         m.onload(plan, slab2, new)
         for (key, kd), x in new.items():
             assert np.array_equal(bits_np(x), osh[(key, kd)]), (key, kd)
+        if not plan.rank_info(r).payload_bytes:    # all shards empty: no data to corrupt
+            m.close()
+            continue
         # a flipped data byte is caught by the next onload
         raw = bytearray(open(path, "rb").read())
         raw[-3] ^= 0x40
