@@ -241,6 +241,8 @@ typedef struct {
     int32_t which;               /* PLEX_STAT_*                              */
     float ms;                    /* CUDA-event duration of the launch/copy   */
     uint64_t bytes;              /* algorithmic bytes                        */
+    float start_ms;              /* start relative to the first timed launch of the same call */
+    int32_t call;                /* index of the blocking call it belongs to (since the last reset) */
 } plex_launch_record;
 
 #define PLEX_STAT_PACK    0      /* K1 gather-pack (+checksum)  */

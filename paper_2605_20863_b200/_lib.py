@@ -100,7 +100,8 @@ class DstDesc(C.Structure):
 
 
 class LaunchRecord(C.Structure):
-    _fields_ = [("which", C.c_int32), ("ms", C.c_float), ("bytes", C.c_uint64)]
+    _fields_ = [("which", C.c_int32), ("ms", C.c_float), ("bytes", C.c_uint64), ("start_ms", C.c_float),
+                ("call", C.c_int32)]
 
 
 class KernelStats(C.Structure):

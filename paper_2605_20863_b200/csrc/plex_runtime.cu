@@ -121,6 +121,7 @@ struct plex_ctx_s {
     std::vector<Timed> pending;
     plex_kernel_stats stats[PLEX_NUM_STATS] = {};
     std::vector<plex_launch_record> trace;   // every timed launch since the last reset
+    int32_t n_calls = 0;                     // timed blocking calls since the last reset
     // pointer tables (pinned host mirror -> device)
     uint64_t* h_ptrs = nullptr;
     uint64_t* d_ptrs = nullptr;
@@ -292,13 +293,15 @@ static plex_status timed_end(plex_ctx_s* c, cudaStream_t s, cudaEvent_t a, int w
 }
 static plex_status timed_collect(plex_ctx_s* c) {
     for (const Timed& t : c->pending) {
-        float ms = 0;
+        float ms = 0, t0 = 0;
         CK(cudaEventElapsedTime(&ms, t.a, t.b));
+        CK(cudaEventElapsedTime(&t0, c->pending.front().a, t.a));   // copy-engine / kernel timeline
         c->stats[t.which].launches += 1;
         c->stats[t.which].total_ms += ms;
         c->stats[t.which].bytes += t.bytes;
-        if (c->trace.size() < (1u << 20)) c->trace.push_back(plex_launch_record{t.which, ms, t.bytes});
+        if (c->trace.size() < (1u << 20)) c->trace.push_back(plex_launch_record{t.which, ms, t.bytes, t0, c->n_calls});
     }
+    if (!c->pending.empty()) ++c->n_calls;
     c->pending.clear();
     c->pool_used = 0;
     return PLEX_OK;
@@ -883,6 +886,7 @@ plex_status plex_ctx_reset_stats(plex_ctx_t c) {
     if (!c) { set_error("NULL ctx"); return PLEX_E_INVAL; }
     for (auto& s : c->stats) s = plex_kernel_stats{};
     c->trace.clear();
+    c->n_calls = 0;
     return PLEX_OK;
 }
 

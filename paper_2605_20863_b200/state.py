@@ -573,6 +573,17 @@ class StateManager:
         check(lib.plex_ctx_trace(self.h, buf, n.value, C.byref(n)))
         return [(L.STAT_NAMES[r.which], float(r.ms), int(r.bytes)) for r in buf[:n.value]]
 
+    def timeline(self) -> List[dict]:
+        """The same records with their start times: {kind, call, start_ms, ms, bytes},
+        start relative to the first timed launch of the same blocking call (a
+        kernel / copy-engine timeline from CUDA events, no profiler needed)."""
+        n = C.c_int32()
+        check(lib.plex_ctx_trace(self.h, None, 0, C.byref(n)))
+        buf = (L.LaunchRecord * max(1, n.value))()
+        check(lib.plex_ctx_trace(self.h, buf, n.value, C.byref(n)))
+        return [{"kind": L.STAT_NAMES[r.which], "call": int(r.call), "start_ms": float(r.start_ms),
+                 "ms": float(r.ms), "bytes": int(r.bytes)} for r in buf[:n.value]]
+
     def reset_stats(self) -> None:
         check(lib.plex_ctx_reset_stats(self.h))
 
