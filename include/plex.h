@@ -392,6 +392,23 @@ PLEX_API plex_status plex_state_switch(plex_ctx_t ctx, plex_plan_t plan_out, con
                                        plex_slab_t slab_out, plex_plan_t plan_in, plex_slab_t slab_in,
                                        void* const* dst_in, int32_t n_dst, void* caller_stream);
 
+/* NEXT-1 in-place swap (PAPER.md:555 context switch, R17 one resident job):
+ * the resident job's state (state pointers, plex_state_offload layout) and the
+ * incoming job's state (in `slab`, HOST-resident, offloaded under the same
+ * plan) trade places.  On return the tensors hold the incoming state (checksum
+ * verified) and the slab holds the outgoing state with its checksums.  Both
+ * host-link directions run at once through the two staging rings (like
+ * plex_state_switch), but only ONE device copy and ONE pinned slab exist: per
+ * bucket, the outgoing pack reads a tensor range before the incoming unpack
+ * overwrites it (same kernel stream) and the outgoing D2H overwrites a slab
+ * range only after the incoming H2D has read it.  Staging >= 2 x n_slots x
+ * bucket.  Blocking, caller-stream ordered.  E_STATE if the slab holds no
+ * offloaded state; E_INVAL for elision / carried-bucket plans.  On
+ * E_CHECKSUM the slab already holds the outgoing state (safe) and the tensors'
+ * contents are unspecified. */
+PLEX_API plex_status plex_state_swap(plex_ctx_t ctx, plex_plan_t plan, void* const* state, int32_t n_state,
+                                     plex_slab_t slab, void* caller_stream);
+
 /* ---- a8 - a11: train -> rollout weight sync ------------------------------- */
 /* Collective over the ctx's world.  src_master[t] = this rank's fp32 master
  * shard of tensor t (FSDP-world rows).  dst_arena = this rank's bf16 rollout

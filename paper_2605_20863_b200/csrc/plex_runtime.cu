@@ -1397,6 +1397,106 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     return PLEX_OK;
 }
 
+// ---- NEXT-1: in-place swap of two same-layout jobs ---------------------------------------
+// PAPER.md:555 context switch when the GPU group holds ONE job's device state
+// (R17) and the host ONE slab: the resident job A's state goes out of the
+// device tensors into the slab while the incoming job B's state comes from the
+// same slab into the same tensors.  Per bucket k: H2D B_k (slab -> in ring) ;
+// pack A_k (tensors -> out ring) ; unpack B_k (in ring -> tensors, after pack
+// A_k on the same kernel stream) ; D2H A_k (out ring -> slab, after H2D B_k
+// has read that slab range).  D2H A_k overlaps H2D B_{k+1}: both directions of
+// the host link stay busy with a single copy of each job's state.
+plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, int32_t n_state, plex_slab_t slab,
+                            void* caller_stream) {
+    plex_status st = check_common(c, plan);
+    if (st || (st = check_slab(c, plan, slab, true)) || (st = check_no_async(c))) return st;
+    const Plan& p = plan->p;
+    if (slab->residency != PLEX_RES_HOST || !slab->written) { set_error("swap needs the incoming job's state in the slab (HOST)"); return PLEX_E_STATE; }
+    if (slab->elided || (p.flags & PLEX_PLAN_ELIDE_PARAM)) { set_error("swap does not support param elision"); return PLEX_E_INVAL; }
+    if (p.ranks[c->rank].carried_out || p.ranks[c->rank].carried_in) { set_error("swap with carried buckets is not supported"); return PLEX_E_INVAL; }
+    if (c->staging_bytes < 2ull * c->n_slots * p.bucket) {
+        set_error("swap needs staging >= 2 x n_slots x bucket = %llu B", (unsigned long long)(2ull * c->n_slots * p.bucket));
+        return PLEX_E_INVAL;
+    }
+    DeviceGuard g(c->device);
+    NvtxRange nv("plex_state_swap");
+    const void* const* ptrs = reinterpret_cast<const void* const*>(state);
+    Half ho{&p, &p.ranks[c->rank], nullptr, slab, 0, {}, false, 0, nullptr, nullptr, nullptr};
+    if ((st = fill_state_ptrs(c, p, ptrs, n_state, 0)) || (st = fill_state_ptrs(c, p, ptrs, n_state, 1)) ||
+        (st = get_devplan(c, p, &ho.d)))
+        return st;
+    Half hi = ho;
+    if (!c->copy2) {
+        CK(cudaStreamCreateWithFlags(&c->copy2, cudaStreamNonBlocking));
+        c->ev_pack2.resize(c->n_slots);
+        c->ev_copy2.resize(c->n_slots);
+        for (int i = 0; i < c->n_slots; ++i) {
+            CK(cudaEventCreateWithFlags(&c->ev_pack2[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
+        }
+    }
+    Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
+            c->d_ctr, c->d_flag + 2, c->h_flag + 2};
+    Pipe pi{c->staging + (uint64_t)c->n_slots * p.bucket, c->n_slots, c->ev_pack2.data(), c->ev_copy2.data(), c->pack,
+            c->copy2, c->h_ptrs2, c->d_ptrs2, c->d_ctr + 1, c->d_flag + 1, c->h_flag + 1};
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
+    CK(cudaEventRecord(c->ev_caller, caller));
+    for (cudaStream_t s2 : {c->pack, c->copy, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
+    // on_begin uploads B's recorded checksums before anything overwrites the slab's
+    if ((st = on_begin(c, pi, hi)) || (st = off_begin(c, po, ho))) return st;
+    const RankPlan& R = p.ranks[c->rank];
+    for (int32_t k = 0; k < ho.nb; ++k) {
+        const int slot = k % c->n_slots;
+        uint8_t* so = po.staging + (uint64_t)slot * p.bucket;
+        uint8_t* si = pi.staging + (uint64_t)slot * p.bucket;
+        const uint64_t lo = (uint64_t)k * p.bucket;
+        const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
+        const uint64_t i0 = R.bucket_item_start[k], i1 = R.bucket_item_start[k + 1];
+        cudaEvent_t ta = nullptr;
+        // H2D B_k
+        if (k >= c->n_slots) CK(cudaStreamWaitEvent(pi.copy, pi.ev_k[slot], 0));
+        if ((st = tbeg(c, pi, pi.copy, &ta))) return st;
+        CK(cudaMemcpyAsync(si, slab->host + lo, len, cudaMemcpyHostToDevice, pi.copy));
+        if ((st = tend(c, pi, pi.copy, ta, PLEX_STAT_H2D, len))) return st;
+        CK(cudaEventRecord(pi.ev_c[slot], pi.copy));
+        // pack A_k
+        if (k >= c->n_slots) CK(cudaStreamWaitEvent(po.kern, po.ev_c[slot], 0));
+        if ((st = tbeg(c, po, po.kern, &ta))) return st;
+        CK(launch_pack(true, ho.d->items + i0, (uint32_t)(i1 - i0), ho.d->segs, po.d_ptrs, so, lo, ho.d->cks, po.ctr,
+                       po.kern));
+        if ((st = tend(c, po, po.kern, ta, PLEX_STAT_PACK, 2 * ho.d->bucket_payload[k]))) return st;
+        CK(cudaEventRecord(po.ev_k[slot], po.kern));
+        // unpack B_k (same stream: after pack A_k read these tensor bytes)
+        CK(cudaStreamWaitEvent(pi.kern, pi.ev_c[slot], 0));
+        if ((st = tbeg(c, pi, pi.kern, &ta))) return st;
+        CK(launch_pack(false, hi.d->items + i0, (uint32_t)(i1 - i0), hi.d->segs, pi.d_ptrs, si, lo, hi.d->cks_in,
+                       pi.ctr, pi.kern));
+        if ((st = tend(c, pi, pi.kern, ta, PLEX_STAT_UNPACK, 2 * hi.d->bucket_payload[k]))) return st;
+        CK(cudaEventRecord(pi.ev_k[slot], pi.kern));
+        // D2H A_k (after H2D B_k read this slab range)
+        CK(cudaStreamWaitEvent(po.copy, po.ev_k[slot], 0));
+        CK(cudaStreamWaitEvent(po.copy, pi.ev_c[slot], 0));
+        if ((st = tbeg(c, po, po.copy, &ta))) return st;
+        CK(cudaMemcpyAsync(slab->host + lo, so, len, cudaMemcpyDeviceToHost, po.copy));
+        if ((st = tend(c, po, po.copy, ta, PLEX_STAT_D2H, len))) return st;
+        CK(cudaEventRecord(po.ev_c[slot], po.copy));
+    }
+    if ((st = off_end(c, po, ho)) || (st = on_end(c, pi, hi))) return st;
+    CK(cudaEventRecord(c->ev_pack_done, c->copy2));
+    CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
+    CK(cudaStreamSynchronize(c->copy2));
+    if ((st = finish(c, caller))) return st;
+    slab->cks.swap(ho.cks);                    // the slab now holds A (checksums recorded by its pack)
+    slab->residency = PLEX_RES_HOST;
+    slab->written = true;
+    slab->elided = false;
+    if (*pi.h_flag) {
+        set_error("swap: %d segment checksum(s) of the incoming state differ from its offload", *pi.h_flag);
+        return PLEX_E_CHECKSUM;
+    }
+    return PLEX_OK;
+}
+
 // ---- NEXT-1: scheduler-directed prefetch and asynchronous drain -----------------------
 // PAPER.md:506 "when an upcoming context switch is predicted, StateManager can
 // proactively move state upward in the hierarchy before the corresponding

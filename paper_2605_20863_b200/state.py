@@ -446,6 +446,12 @@ class StateManager:
         check(lib.plex_state_switch(self.h, plan_out.h, a, na, slab_out.h, plan_in.h, slab_in.h, b, nb,
                                     _stream_ptr(stream)))
 
+    def swap(self, plan: Plan, shards, slab: Slab, stream=None) -> None:
+        """In-place context switch of two same-layout jobs: the resident state in
+        `shards` goes to `slab` while the slab's state comes into `shards`."""
+        arr, n = self._state_ptrs(plan, shards, slab.rank)
+        check(lib.plex_state_swap(self.h, plan.h, arr, n, slab.h, _stream_ptr(stream)))
+
     @staticmethod
     def _check_masters(plan: Plan, masters: Sequence[torch.Tensor], rank: int) -> None:
         if len(masters) != len(plan.manifest):
@@ -730,6 +736,19 @@ class Job:
                         stream)
         if release:
             self.release()
+        other.restore_replicas(stream)
+
+    def swap_with(self, other: "Job", stream=None) -> None:
+        """PAPER.md:555 switch self -> other in place (plex_state_swap): other's
+        state (HOST, in its slab, same plan layout) takes over self's device
+        tensors and self's state takes over that slab.  One device copy and one
+        pinned slab serve both jobs."""
+        if other.slab is None or other.plan.h.value != self.plan.h.value:
+            raise ValueError("swap_with needs the other job suspended in a slab of the same plan")
+        self.mgr.swap(self.plan, self.slab_shards(), other.slab, stream)
+        self.shards, other.shards = other.shards, self.shards
+        self.slab, other.slab = other.slab, self.slab
+        self.param_arena, other.param_arena = other.param_arena, self.param_arena
         other.restore_replicas(stream)
 
     def sync(self, arena: torch.Tensor, stream=None) -> None:

@@ -309,6 +309,67 @@ def test_duplex_switch_matches_oracle(models, buckets):
         m.close()
 
 
+# ---- NEXT-1 in-place swap (one device copy, one slab) ----------------------------------------------
+@pytest.mark.parametrize("model,W,layout,bucket", [("mid", 1, L.SLAB_KIND_MAJOR, 1 << 14),
+                                                   ("toy-odd", 3, L.SLAB_KIND_MAJOR, 1024),
+                                                   ("mid-moe", 4, L.SLAB_KEY_MAJOR, 1 << 15),
+                                                   ("toy", 13, L.SLAB_KIND_MAJOR, 512)])
+def test_inplace_swap_matches_oracle(model, W, layout, bucket):
+    man = manifest(model)
+    plan = P.Plan(man, world=W, slab_layout=layout, bucket_bytes=bucket, tile_bytes=512)
+    fa, fb = full_state(model, seed=31, special_bits=3), full_state(model, seed=32, special_bits=3)
+    for r in range(W):
+        m = mgr(W, r, bucket=bucket, slots=2)
+        oa, ob = fsdp_shards(fa, W, r, O.fsdp_rows), fsdp_shards(fb, W, r, O.fsdp_rows)
+        segs, size = O.slab_layout(man, W, r, layout)
+        dev = {kk: to_dev(x, kk[1]) for kk, x in ob.items()}       # B's state, offloaded into the slab
+        slab = P.Slab(plan, r)
+        m.offload(plan, dev, slab)
+        for kk, x in oa.items():                                    # A resident in the same tensors
+            dev[kk].copy_(to_dev(x, kk[1]))
+        for it, (now_dev, now_slab) in enumerate(((ob, oa), (oa, ob), (ob, oa))):
+            m.swap(plan, dev, slab)
+            for kk, x in dev.items():
+                assert np.array_equal(bits_np(x), now_dev[kk]), (it, kk)
+            assert np.array_equal(slab.host_bytes(), O.pack_slab(segs, size, now_slab)), it
+            want_ck = np.array(O.segment_checksums(segs, now_slab), dtype=np.uint64).reshape(-1, 2)
+            assert np.array_equal(slab.checksums(), want_ck), it
+            assert slab.residency == L.RES_HOST
+        # a corrupted incoming state: E_CHECKSUM, and the outgoing state is safe in the slab
+        if plan.rank_info(r).payload_bytes:
+            seg = next(s_ for s_ in plan.segments(r) if s_.nbytes)
+            slab.host_bytes()[seg.slab_offset] ^= 0x01
+            with pytest.raises(P.PlexError) as e:
+                m.swap(plan, dev, slab)
+            assert e.value.code == L.E_CHECKSUM
+            assert np.array_equal(slab.host_bytes(), O.pack_slab(segs, size, ob))
+        m.close()
+
+
+def test_job_swap_with_shares_one_device_copy():
+    man = manifest("mid")
+    m = mgr(1, 0, bucket=1 << 16)
+    plan = m.plan(man)
+    a = P.Job(m, plan, seed=1, slab=False).alloc()
+    b = P.Job(m, plan, seed=2)
+    b.shards = a.shards
+    b.init_synthetic(special_bits=3)
+    b.suspend(release=False)
+    b.shards = OrderedDict()
+    a.init_synthetic(special_bits=3)
+    fa, fb = full_state("mid", seed=1, special_bits=3), full_state("mid", seed=2, special_bits=3)
+    a.swap_with(b)
+    assert a.slab is not None and b.slab is None
+    for kk, x in b.shards.items():
+        assert np.array_equal(bits_np(x), fb[kk]), kk
+    b.swap_with(a)
+    for kk, x in a.shards.items():
+        assert np.array_equal(bits_np(x), fa[kk]), kk
+    with pytest.raises(ValueError):
+        a.swap_with(a)
+    m.close()
+
+
 # ---- NEXT-2 derived-param elision ----------------------------------------------------------------
 @pytest.mark.parametrize("model,W,bucket", [("mid", 1, 4096), ("mid", 3, 1 << 14), ("toy-odd", 2, 512)])
 def test_param_elision(model, W, bucket):
