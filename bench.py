@@ -8,7 +8,8 @@ PAPER.md:555 (resident A -> incoming B = [OFFLOAD A, ONLOAD B]) followed by the
 train->rollout weight sync of B; the next step switches back.
     suspend A (a3 gather-pack + a4 D2H into A's pinned slab)
     resume  B (a6 H2D + a7 scatter-unpack + checksum verify)   -- concurrent with
-              the suspend when both jobs fit in HBM (duplex, NEXT-1)
+              the suspend (NEXT-1): duplex when both jobs fit in HBM, else the
+              in-place swap through one device copy and one pinned slab
     sync    B (a8 fp32->bf16 RNE + a9-a11 reshard into the rollout layout)
 Workload at N GPUs: FSDP-N shards -> rollout TP-min(2,N) x DP-N/TP (configs[1]
 is N=8: FSDP-8 -> TP-2 x DP-4).  ``value`` = state bytes moved through the
@@ -53,6 +54,7 @@ def parse():
                     help="pin slabs with cudaHostAlloc instead of mmap(MADV_HUGEPAGE) + cudaHostRegister")
     ap.add_argument("--no-duplex", action="store_true", help="sequential offload then onload")
     ap.add_argument("--single-job", action="store_true", help="step = suspend + resume + sync of one job")
+    ap.add_argument("--swap", action="store_true", help="in-place swap switch even when two device copies fit")
     ap.add_argument("--no-balance", action="store_true", help="no NVLink-carried buckets (host-link balancing)")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -294,13 +296,23 @@ def run_plex(a):
     plan_s = (time.perf_counter() - t0) / 2
     plan = plans[0]
     info = plan.rank_info(rank)
-    # two jobs of the same shape (seeds 1, 2): B starts suspended in its slab,
-    # A resident -- one resident job per GPU group (R17).  If the host cannot
-    # pin both jobs' slabs (N=1: 2 x 106.6 GB), the step is the single-job
-    # round trip (suspend A, resume A, sync A) over the same bytes.
-    two_jobs = not a.single_job
+    # two jobs of the same shape (seeds 1, 2): B starts suspended, A resident --
+    # one resident job per GPU group (R17).  duplex: both jobs keep their own
+    # device tensors and slabs and the switch runs offload A || onload B
+    # (plex_state_switch).  swap: when two device copies do not fit in HBM (N=1:
+    # 2 x 106.6 GB), A and B share ONE set of device tensors and ONE slab and the
+    # switch is the in-place plex_state_swap -- both host-link directions still
+    # run at once.  sequential (--no-duplex): offload A, then onload B.
+    free0, _ = torch.cuda.mem_get_info(local)
+    fits2 = 2 * info.payload_bytes + info.dst_arena_bytes + (6 << 30) < free0
+    if a.single_job:
+        mode = "single"
+    elif a.swap or not allmin(1.0 if fits2 else 0.0) > 0.5:
+        mode = "swap"
+    else:
+        mode = "sequential" if a.no_duplex else "duplex"
     job_b = None
-    if two_jobs:
+    if mode in ("duplex", "sequential"):
         try:
             job_b = P.Job(mgr, plans[1], seed=2, hugepage=a.hugepage).alloc().init_synthetic()
             job_b.suspend()
@@ -310,20 +322,31 @@ def run_plex(a):
             if e.code != P._lib.E_TIER_FULL:
                 raise
             ok = 0.0
-        two_jobs = allmin(ok) > 0.5
-        if not two_jobs:
+        if not allmin(ok) > 0.5:                      # two slabs exceed the pinnable host memory
             job_b = job_a = None
             torch.cuda.empty_cache()
-    if not two_jobs:
+            mode = "swap"
+    if mode == "swap" and n_carried:                  # the in-place swap does not carry buckets
+        plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map)
+                 for _ in range(2)]
+        plan, n_carried = plans[0], 0
+        info = plan.rank_info(rank)
+    if mode == "swap":
+        job_a = P.Job(mgr, plans[0], seed=1, slab=False).alloc()
+        job_b = P.Job(mgr, plans[0], seed=2, hugepage=a.hugepage)
+        job_b.shards = job_a.shards                   # B's state: generated in place, offloaded
+        job_b.init_synthetic()
+        job_b.suspend(release=False)
+        job_b.shards = type(job_a.shards)()
+        job_a.init_synthetic()                        # A resident in the same tensors
+    if mode == "single":
         job_a = P.Job(mgr, plans[0], seed=1, hugepage=a.hugepage).alloc().init_synthetic()
+    two_jobs = mode != "single"
+    duplex = mode in ("duplex", "swap")
     jobs = [job_a, job_b] if two_jobs else [job_a, job_a]
     arena = mgr.arena(plan)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
-    # duplex switch (offload A || onload B) needs both jobs on the device at once
-    free, total = torch.cuda.mem_get_info(local)
-    duplex = two_jobs and (not a.no_duplex) and (info.payload_bytes + (4 << 30) < free)
-    duplex = allmin(1.0 if duplex else 0.0) > 0.5
 
     phase_ev = []
     cur = {"i": 0}
@@ -335,7 +358,9 @@ def run_plex(a):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
         if ev:
             ev[0].record()
-        if duplex:
+        if mode == "swap":
+            out.swap_with(inc)
+        elif mode == "duplex":
             out.switch_to(inc)
         else:
             out.suspend(release=out is not inc)
@@ -451,7 +476,10 @@ def run_plex(a):
             "data": "synthetic (counter-based generator, DESIGN.md §3); random-init Qwen2.5-7B-shaped state",
             "config": {"workload": (f"two {a.model}-shaped jobs (bf16 param + fp32 master/m/v each) FSDP-{world} -> "
                                     f"rollout TP-{tp}xDP-{dp}; step = context switch A->B (full suspend of A + full "
-                                    f"resume of B, {'duplex: offload || onload' if duplex else 'sequential'}) + "
+                                    f"resume of B, " + {"duplex": "duplex: offload || onload",
+                                                        "swap": "in-place swap: offload || onload through one "
+                                                                "device copy and one pinned slab",
+                                                        "sequential": "sequential"}[mode] + ") + "
                                     f"weight sync of B") if two_jobs else
                                    (f"one {a.model}-shaped job (bf16 param + fp32 master/m/v) FSDP-{world} -> rollout "
                                     f"TP-{tp}xDP-{dp}; step = full suspend + full resume + weight sync (two jobs' "
@@ -460,7 +488,7 @@ def run_plex(a):
                        "host_link_weights_GBs": [round(x, 2) for x in weights] if weights else None,
                        "carried_buckets_per_job": n_carried,
                        "model_shape": a.model, "state_bytes_per_rank_per_job": info.payload_bytes,
-                       "bytes_switched_per_step": int(S_total), "duplex": duplex,
+                       "bytes_switched_per_step": int(S_total), "duplex": duplex, "switch_mode": mode,
                        "bucket_bytes": bucket, "staging_slots": a.slots,
                        "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
                        "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
@@ -480,8 +508,11 @@ def run_plex(a):
             line["e2e"] = {"value": round(S_total / e2e["s"] / 1e9, 3), "unit": "GB/s",
                            "ms_per_step": round(e2e["s"] * 1e3, 2), "h2d_bytes_per_step": e2e["h2d"],
                            "d2h_bytes_per_step": e2e["d2h"],
-                           "api": "Job.switch_to (or suspend+resume) with storage release/acquire -> Job.sync "
-                                  "(host clock)"}
+                           "api": {"swap": "Job.swap_with (in place) -> Job.sync (host clock)",
+                                   "duplex": "Job.switch_to with storage release/acquire -> Job.sync (host clock)",
+                                   "sequential": "Job.suspend + Job.resume with storage release/acquire -> Job.sync "
+                                                 "(host clock)",
+                                   "single": "Job.suspend + Job.resume -> Job.sync (host clock)"}[mode]}
         if not a.no_cpu_baseline and world == 1:
             v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
             line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
