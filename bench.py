@@ -272,7 +272,29 @@ def run_plex(a):
             e1.synchronize()
             best = max(best, probe / (e0.elapsed_time(e1) * 1e-3) / 1e9)
         bw[direction] = best
-    del h, dbuf
+    # ... and both directions at once (what a duplex / swap switch can get per direction)
+    h2 = torch.empty(probe, dtype=torch.uint8).pin_memory()
+    dbuf2 = torch.empty(probe, dtype=torch.uint8, device=f"cuda:{local}")
+    s_d, s_h = torch.cuda.Stream(local), torch.cuda.Stream(local)
+    bw2 = {"d2h": 0.0, "h2d": 0.0}
+    for _ in range(3):
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        cur_s = torch.cuda.current_stream(local)
+        s_d.wait_stream(cur_s)
+        s_h.wait_stream(cur_s)
+        with torch.cuda.stream(s_d):
+            ev[0].record(s_d)
+            h.copy_(dbuf, non_blocking=True)
+            ev[1].record(s_d)
+        with torch.cuda.stream(s_h):
+            ev[2].record(s_h)
+            dbuf2.copy_(h2, non_blocking=True)
+            ev[3].record(s_h)
+        torch.cuda.synchronize(local)
+        bw2["d2h"] = max(bw2["d2h"], probe / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
+        bw2["h2d"] = max(bw2["h2d"], probe / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9)
+    del h, dbuf, h2, dbuf2
     torch.cuda.empty_cache()
 
     # NEXT-1 host-link balancing: every rank's rate for one offload + one onload
@@ -280,7 +302,10 @@ def run_plex(a):
     # to fast-link ranks over NVLink when that shortens the slowest rank
     weights = None
     if world > 1 and not a.no_balance:
-        w_local = 1.0 / (1.0 / bw["d2h"] + 1.0 / bw["h2d"])
+        # a duplex switch takes max(S/d2h, S/h2d) at the both-directions rates;
+        # a sequential one S/d2h + S/h2d at the one-direction rates
+        w_local = (1.0 / (1.0 / bw["d2h"] + 1.0 / bw["h2d"]) if a.no_duplex
+                   else min(bw2["d2h"], bw2["h2d"]))
         wt = torch.tensor([w_local], dtype=torch.float64, device=f"cuda:{local}")
         allw = [torch.zeros_like(wt) for _ in range(world)]
         dist.all_gather(allw, wt)
@@ -439,7 +464,8 @@ def run_plex(a):
             rl[k] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak_hbm, "unit": "GB/s",
                      "frac": frac(gbs, peak_hbm), "launches_per_step": v["launches"] / a.steps,
                      "ms_per_step": round(v["ms"] / a.steps, 3)}
-    for k, v, ref in (("d2h", d2h, bw["d2h"]), ("h2d", h2d, bw["h2d"])):
+    bw_ref = bw2 if duplex else bw                      # duplex / swap: both directions share the link
+    for k, v, ref in (("d2h", d2h, bw_ref["d2h"]), ("h2d", h2d, bw_ref["h2d"])):
         gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else 0.0
         lo, hi = allmin(gbs), allmax(gbs)
         ref_lo = allmin(ref)
@@ -448,7 +474,10 @@ def run_plex(a):
                                "unit": "GB/s", "frac": frac(gbs, ref),
                                "achieved_min_max_over_ranks": [round(lo, 2), round(hi, 2)],
                                "peak_min_over_ranks": round(ref_lo, 2),
-                               "peak_kind": f"measured pinned copy, {world} GPU(s) concurrently (rank 0)"}
+                               "peak_kind": (f"measured pinned copy, {world} GPU(s) concurrently, "
+                                             + ("both directions at once" if duplex else "one direction")
+                                             + " (this rank)"),
+                               "peak_one_direction": round(bw[k], 2)}
     if world > 1:
         # NVLink: max over ranks of max(send, recv) bytes ÷ the data-moving part
         # of the sync (the push kernel, or the NCCL exchange rounds), max over ranks
