@@ -142,3 +142,70 @@ def test_fullsize_qwen05_every_byte():
     import gc
     gc.collect()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_fullsize_qwen7b_swap_one_gpu():
+    """bench.py's N=1 switch: two Qwen2.5-7B-shaped jobs sharing one set of
+    device tensors and one pinned slab, switched in place (plex_state_swap)."""
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    torch.cuda.set_device(0)
+    model, sa, sb = "qwen2.5-7b", 1, 2
+    man = manifest(model)
+    mgr = P.StateManager(device=0, bucket_bytes=2 << 30, n_slots=2, bootstrap=False)
+    plan = mgr.plan(man)
+    a = P.Job(mgr, plan, seed=sa, slab=False).alloc()
+    b = P.Job(mgr, plan, seed=sb)
+    b.shards = a.shards
+    b.init_synthetic()
+    segs = plan.segments(0)
+
+    def dev_cks(shards):
+        ck = torch.zeros((len(segs), 2), dtype=torch.int64, device="cuda")
+        for i, s in enumerate(segs):
+            P.checksum(shards[(man[s.tensor][0], s.kind)], s.index_base, out=ck[i])
+        return ck.cpu().numpy().view(np.uint64).copy()
+
+    ck_b = dev_cks(b.shards)
+    b.suspend(release=False)
+    b.shards = type(a.shards)()
+    assert np.array_equal(b.slab.checksums(), ck_b)
+    a.init_synthetic()
+    ck_a = dev_cks(a.shards)
+    sample = ["lm_head.weight", "model.layers.0.self_attn.q_proj.weight", "model.layers.27.mlp.down_proj.weight",
+              "model.norm.weight"]
+
+    def check_slab(slab, seed, cks):
+        assert np.array_equal(slab.checksums(), cks)
+        host = slab.host_bytes()
+        ends = [s.slab_offset + s.nbytes for s in segs]
+        starts = [s.slab_offset for s in segs[1:]] + [host.size]
+        for e, nxt in zip(ends, starts):
+            assert nxt - e < 256 and not host[e:nxt].any()
+        for i, s in enumerate(segs):
+            key = man[s.tensor][0]
+            if key in sample:
+                want = gen_range(seed, key, s.kind, s.index_base, s.nbytes // (2 if s.kind == 0 else 4))
+                assert np.array_equal(host[s.slab_offset:s.slab_offset + s.nbytes].view(want.dtype), want), key
+                assert tuple(int(v) for v in cks[i]) == O.checksum(want, s.index_base)
+
+    def check_dev(shards, seed, cks):
+        assert np.array_equal(dev_cks(shards), cks)
+        for key in sample:
+            for kd in range(4):
+                x = shards[(key, kd)]
+                want = gen_range(seed, key, kd, 0, x.numel())
+                assert np.array_equal(bits_np(x).reshape(-1), want), (key, kd)
+
+    a.swap_with(b)                              # A -> slab, B -> device
+    check_dev(b.shards, sb, ck_b)
+    check_slab(a.slab, sa, ck_a)
+    b.swap_with(a)                              # and back
+    check_dev(a.shards, sa, ck_a)
+    check_slab(b.slab, sb, ck_b)
+    del a, b, plan
+    mgr.close()
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
