@@ -40,10 +40,27 @@ def _worker(rank, world, port, q):
         sr = [None] * world
         dist.all_gather_object(sr, (info.send_bytes, info.recv_bytes))
         L = plan.ledger()
+        # NEXT-1 balancing: every rank contributes its own link rate, all-gathered
+        # (as bench.py does); every rank must derive the same carried buckets
+        import torch
+        w = torch.tensor([10.0 + 5.0 * rank])
+        ws = [torch.zeros(1) for _ in range(world)]
+        dist.all_gather(ws, w)
+        cp = Plan(manifest(model), world=world, bucket_bytes=(1 << 30) if world == 2 else (1 << 14), link_weights=[float(x) for x in ws])
+        carry = [(c.owner, c.bucket, c.carrier, c.slab_offset, c.bytes, c.carry_offset) for c in cp.carry()]
+        carries = [None] * world
+        dist.all_gather_object(carries, carry)
+        # NEXT-2 replica plans: the all-gather ledger is symmetric
+        rp = Plan(manifest(model), world=world, replica_param=True)
+        gi = rp.rank_info(rank)
+        gs = [None] * world
+        dist.all_gather_object(gs, (gi.gather_send_bytes, gi.gather_recv_bytes))
         ok = (all(i == ids[0] for i in ids) and len(ids[0]) == 128 and any(ids[0])
               and all(d == digs[0] for d in digs)
               and sr[rank][0] == int(L[rank].sum() - L[rank, rank])
-              and sum(s for s, _ in sr) == sum(r for _, r in sr))
+              and sum(s for s, _ in sr) == sum(r for _, r in sr)
+              and all(c == carries[0] for c in carries) and len(carries[0]) > 0
+              and sum(a for a, _ in gs) == sum(b for _, b in gs) > 0)
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
