@@ -105,6 +105,32 @@ def main():
                     print(f"[rank {rank}] replica restore mismatch {model} {k}/{kd} iter {it}", flush=True)
                     bad += 1
         del arena, job
+    # NEXT-1 in-place swap of two same-layout jobs on every rank, then the collective sync
+    man = manifest("mid")
+    plan = mgr.plan(man, head_dim=MODELS["mid"].head_dim, tp=1, dp=world, tile_bytes=2048)
+    ja = P.Job(mgr, plan, seed=41, slab=False).alloc()
+    jb = P.Job(mgr, plan, seed=42)
+    jb.shards = ja.shards
+    jb.init_synthetic(special_bits=3)
+    jb.suspend(release=False)
+    jb.shards = type(ja.shards)()
+    ja.init_synthetic(special_bits=3)
+    arena = mgr.arena(plan)
+    for it, (out, inc, seed_in) in enumerate(((ja, jb, 42), (jb, ja, 41))):
+        out.swap_with(inc)
+        inc.sync(arena)
+        full = full_state("mid", seed=seed_in, special_bits=3)
+        osh = fsdp_shards(full, world, rank, O.fsdp_rows)
+        for k, v in inc.shards.items():
+            if not np.array_equal(bits_np(v), osh[k]):
+                print(f"[rank {rank}] swap restore mismatch {k} iter {it}", flush=True)
+                bad += 1
+        want = O.weight_sync(master_shards(full, world, O.fsdp_rows), 1, world, 1, 0, MODELS["mid"].head_dim)[rank]
+        for name, v in P.StateManager.rollout_views(plan, rank, arena).items():
+            if not np.array_equal(bits_np(v), want[name]):
+                print(f"[rank {rank}] sync after swap mismatch {name} iter {it}", flush=True)
+                bad += 1
+    del arena, ja, jb
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()

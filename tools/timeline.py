@@ -41,18 +41,33 @@ def main():
     ap.add_argument("--model", default="qwen2.5-1.5b")
     ap.add_argument("--bucket-mb", type=int, default=512)
     ap.add_argument("--sequential", action="store_true", help="offload then onload instead of the duplex switch")
+    ap.add_argument("--swap", action="store_true", help="in-place swap (one device copy, one slab): bench N=1 mode")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     mgr = P.StateManager(device=0, bucket_bytes=a.bucket_mb << 20, n_slots=2, timing=True, bootstrap=False)
-    plans = [mgr.plan(manifest(a.model)) for _ in range(2)]
-    jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic() for pl, s in zip(plans, (0, 1))]
-    jobs[1].suspend()
-    for _ in range(2):                                   # warm up both directions
-        jobs[0].switch_to(jobs[1])
-        jobs[1].switch_to(jobs[0])
+    if a.swap:
+        plan = mgr.plan(manifest(a.model))
+        jobs = [P.Job(mgr, plan, seed=0, slab=False).alloc(), P.Job(mgr, plan, seed=1)]
+        jobs[1].shards = jobs[0].shards
+        jobs[1].init_synthetic()
+        jobs[1].suspend(release=False)
+        jobs[1].shards = type(jobs[0].shards)()
+        jobs[0].init_synthetic()
+        for _ in range(2):
+            jobs[0].swap_with(jobs[1])
+            jobs[1].swap_with(jobs[0])
+    else:
+        plans = [mgr.plan(manifest(a.model)) for _ in range(2)]
+        jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic() for pl, s in zip(plans, (0, 1))]
+        jobs[1].suspend()
+        for _ in range(2):                               # warm up both directions
+            jobs[0].switch_to(jobs[1])
+            jobs[1].switch_to(jobs[0])
     torch.cuda.synchronize()
     mgr.reset_stats()
-    if a.sequential:
+    if a.swap:
+        jobs[0].swap_with(jobs[1])
+    elif a.sequential:
         jobs[0].suspend()
         jobs[1].resume()
     else:
@@ -70,7 +85,8 @@ def main():
                 r["start_ms"] += end0
     iv = {k: [(r["start_ms"] - t0, r["start_ms"] - t0 + r["ms"]) for r in v] for k, v in lanes.items()}
     span = max(b for v in iv.values() for _, b in v)
-    summ = {"model": a.model, "mode": "sequential" if a.sequential else "duplex", "bucket_MiB": a.bucket_mb,
+    summ = {"model": a.model, "mode": "swap" if a.swap else "sequential" if a.sequential else "duplex",
+            "bucket_MiB": a.bucket_mb,
             "span_ms": round(span, 2)}
     for k, v in iv.items():
         byts = sum(r["bytes"] for r in lanes[k])
