@@ -742,3 +742,34 @@ def test_async_prefetch_and_drain(elide):
         for kk, x in job.shards.items():
             assert np.array_equal(bits_np(x), osh[kk]), (j, kk)
     m.close()
+
+
+def test_timeline_records_cover_the_switch():
+    """Launch records (PLEX_CTX_TIMING) carry start times per blocking call: every
+    bucket of a duplex switch has its pack, D2H, H2D and unpack, each inside the call."""
+    man = manifest("mid")
+    m = mgr(1, 0, bucket=1 << 15, timing=True)
+    plans = [m.plan(man) for _ in range(2)]
+    a = P.Job(m, plans[0], seed=1).alloc().init_synthetic()
+    b = P.Job(m, plans[1], seed=2).alloc().init_synthetic()
+    b.suspend()
+    m.reset_stats()
+    a.switch_to(b)
+    recs = m.timeline()
+    nb = plans[0].rank_info(0).n_buckets
+    kinds = [r["kind"] for r in recs]
+    for k in ("pack", "d2h", "h2d", "unpack"):
+        assert kinds.count(k) == nb, k
+    assert {r["call"] for r in recs} == {0}
+    t0 = min(r["start_ms"] for r in recs)
+    assert t0 == 0.0 and all(r["ms"] >= 0 for r in recs)
+    # per bucket: the D2H starts after its pack ended, the unpack after its H2D ended
+    packs = [r for r in recs if r["kind"] == "pack"]
+    d2hs = [r for r in recs if r["kind"] == "d2h"]
+    h2ds = [r for r in recs if r["kind"] == "h2d"]
+    unps = [r for r in recs if r["kind"] == "unpack"]
+    for p_, d_ in zip(packs, d2hs):
+        assert d_["start_ms"] >= p_["start_ms"] + p_["ms"] - 0.01
+    for h_, u_ in zip(h2ds, unps):
+        assert u_["start_ms"] >= h_["start_ms"] + h_["ms"] - 0.01
+    m.close()
