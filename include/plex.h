@@ -402,8 +402,13 @@ PLEX_API plex_status plex_state_switch(plex_ctx_t ctx, plex_plan_t plan_out, con
  * bucket, the outgoing pack reads a tensor range before the incoming unpack
  * overwrites it (same kernel stream) and the outgoing D2H overwrites a slab
  * range only after the incoming H2D has read it.  Staging >= 2 x n_slots x
- * bucket.  Blocking, caller-stream ordered.  E_STATE if the slab holds no
- * offloaded state; E_INVAL for elision / carried-bucket plans.  On
+ * bucket.  Blocking, caller-stream ordered.  With PLEX_PLAN_ELIDE_PARAM: an
+ * elided incoming slab and a derivable outgoing job both walk the shifted
+ * grid (no param byte moves); an elided incoming slab and a non-derivable
+ * outgoing job first store the outgoing PARAM prefix (slab bytes the
+ * incoming state does not use); a fully stored incoming slab makes the
+ * outgoing job go in full.  E_STATE if the slab holds no offloaded state;
+ * E_INVAL for carried-bucket plans.  On
  * E_CHECKSUM the slab already holds the outgoing state (safe) and the tensors'
  * contents are unspecified. */
 PLEX_API plex_status plex_state_swap(plex_ctx_t ctx, plex_plan_t plan, void* const* state, int32_t n_state,

@@ -1412,7 +1412,6 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
     if (st || (st = check_slab(c, plan, slab, true)) || (st = check_no_async(c))) return st;
     const Plan& p = plan->p;
     if (slab->residency != PLEX_RES_HOST || !slab->written) { set_error("swap needs the incoming job's state in the slab (HOST)"); return PLEX_E_STATE; }
-    if (slab->elided || (p.flags & PLEX_PLAN_ELIDE_PARAM)) { set_error("swap does not support param elision"); return PLEX_E_INVAL; }
     if (p.ranks[c->rank].carried_out || p.ranks[c->rank].carried_in) { set_error("swap with carried buckets is not supported"); return PLEX_E_INVAL; }
     if (c->staging_bytes < 2ull * c->n_slots * p.bucket) {
         set_error("swap needs staging >= 2 x n_slots x bucket = %llu B", (unsigned long long)(2ull * c->n_slots * p.bucket));
@@ -1442,45 +1441,84 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     CK(cudaEventRecord(c->ev_caller, caller));
     for (cudaStream_t s2 : {c->pack, c->copy, c->copy2}) CK(cudaStreamWaitEvent(s2, c->ev_caller, 0));
-    // on_begin uploads B's recorded checksums before anything overwrites the slab's
+    // on_begin uploads B's recorded checksums before anything overwrites the slab's;
+    // off_begin runs A's NEXT-2 derivability check (elision plans)
     if ((st = on_begin(c, pi, hi)) || (st = off_begin(c, po, ho))) return st;
     const RankPlan& R = p.ranks[c->rank];
-    for (int32_t k = 0; k < ho.nb; ++k) {
-        const int slot = k % c->n_slots;
-        uint8_t* so = po.staging + (uint64_t)slot * p.bucket;
-        uint8_t* si = pi.staging + (uint64_t)slot * p.bucket;
-        const uint64_t lo = (uint64_t)k * p.bucket;
+    // Grids (NEXT-2): B elided -> both halves walk the shifted grid from the first
+    // MASTER byte; if A's params are not derivable its PARAM prefix goes out
+    // first on its own (B never reads slab bytes below that point).  B stored
+    // in full -> A goes in full too, even if derivable.
+    bool a_prefix = false;
+    if (!hi.elide && ho.elide) {
+        CK(cudaMemsetAsync(ho.d->cks, 0, 16 * std::max<size_t>(1, R.segs.size()), po.kern));
+        use_grid(ho, false);
+    } else if (hi.elide && !ho.elide) {
+        a_prefix = true;
+        use_grid(ho, true);
+    }
+    const bool shifted = hi.elide;
+    int32_t oseq = 0;                                   // out-ring sequence number (slot = oseq % n_slots)
+    cudaEvent_t ta = nullptr;
+    if (a_prefix) {                                     // A's PARAM prefix [0, elide_start), full-grid buckets
+        const uint64_t e0 = R.elide_start;
+        for (int32_t k = 0; (uint64_t)k * p.bucket < e0; ++k, ++oseq) {
+            const int slot = oseq % c->n_slots;
+            uint8_t* so = po.staging + (uint64_t)slot * p.bucket;
+            const uint64_t lo = (uint64_t)k * p.bucket, hi_b = std::min<uint64_t>(e0, lo + p.bucket);
+            const uint64_t i0 = R.bucket_item_start[k];
+            const uint64_t i1 = std::min<uint64_t>(R.bucket_item_start[k + 1], R.n_param_items);
+            if (oseq >= c->n_slots) CK(cudaStreamWaitEvent(po.kern, po.ev_c[slot], 0));
+            if ((st = tbeg(c, po, po.kern, &ta))) return st;
+            CK(launch_pack(true, ho.d->items + i0, (uint32_t)(i1 - i0), ho.d->segs, po.d_ptrs, so, lo, ho.d->cks,
+                           po.ctr, po.kern));
+            if ((st = tend(c, po, po.kern, ta, PLEX_STAT_PACK, 2 * (hi_b - lo)))) return st;
+            CK(cudaEventRecord(po.ev_k[slot], po.kern));
+            CK(cudaStreamWaitEvent(po.copy, po.ev_k[slot], 0));
+            if ((st = tbeg(c, po, po.copy, &ta))) return st;
+            CK(cudaMemcpyAsync(slab->host + lo, so, hi_b - lo, cudaMemcpyDeviceToHost, po.copy));
+            if ((st = tend(c, po, po.copy, ta, PLEX_STAT_D2H, hi_b - lo))) return st;
+            CK(cudaEventRecord(po.ev_c[slot], po.copy));
+        }
+    }
+    const int32_t nb = shifted ? hi.nb : ho.nb;
+    const uint64_t base = shifted ? R.elide_start : 0;
+    for (int32_t k = 0; k < nb; ++k, ++oseq) {
+        const int si_slot = k % c->n_slots, so_slot = oseq % c->n_slots;
+        uint8_t* so = po.staging + (uint64_t)so_slot * p.bucket;
+        uint8_t* si = pi.staging + (uint64_t)si_slot * p.bucket;
+        const uint64_t lo = base + (uint64_t)k * p.bucket;
         const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
-        const uint64_t i0 = R.bucket_item_start[k], i1 = R.bucket_item_start[k + 1];
-        cudaEvent_t ta = nullptr;
+        const uint64_t i0 = hi.bstart[k], i1 = hi.bstart[k + 1];
         // H2D B_k
-        if (k >= c->n_slots) CK(cudaStreamWaitEvent(pi.copy, pi.ev_k[slot], 0));
+        if (k >= c->n_slots) CK(cudaStreamWaitEvent(pi.copy, pi.ev_k[si_slot], 0));
         if ((st = tbeg(c, pi, pi.copy, &ta))) return st;
         CK(cudaMemcpyAsync(si, slab->host + lo, len, cudaMemcpyHostToDevice, pi.copy));
         if ((st = tend(c, pi, pi.copy, ta, PLEX_STAT_H2D, len))) return st;
-        CK(cudaEventRecord(pi.ev_c[slot], pi.copy));
+        CK(cudaEventRecord(pi.ev_c[si_slot], pi.copy));
         // pack A_k
-        if (k >= c->n_slots) CK(cudaStreamWaitEvent(po.kern, po.ev_c[slot], 0));
+        if (oseq >= c->n_slots) CK(cudaStreamWaitEvent(po.kern, po.ev_c[so_slot], 0));
         if ((st = tbeg(c, po, po.kern, &ta))) return st;
-        CK(launch_pack(true, ho.d->items + i0, (uint32_t)(i1 - i0), ho.d->segs, po.d_ptrs, so, lo, ho.d->cks, po.ctr,
+        CK(launch_pack(true, hi.grid_items + i0, (uint32_t)(i1 - i0), ho.d->segs, po.d_ptrs, so, lo, ho.d->cks, po.ctr,
                        po.kern));
-        if ((st = tend(c, po, po.kern, ta, PLEX_STAT_PACK, 2 * ho.d->bucket_payload[k]))) return st;
-        CK(cudaEventRecord(po.ev_k[slot], po.kern));
+        if ((st = tend(c, po, po.kern, ta, PLEX_STAT_PACK, 2 * hi.payload[k]))) return st;
+        CK(cudaEventRecord(po.ev_k[so_slot], po.kern));
         // unpack B_k (same stream: after pack A_k read these tensor bytes)
-        CK(cudaStreamWaitEvent(pi.kern, pi.ev_c[slot], 0));
+        CK(cudaStreamWaitEvent(pi.kern, pi.ev_c[si_slot], 0));
         if ((st = tbeg(c, pi, pi.kern, &ta))) return st;
-        CK(launch_pack(false, hi.d->items + i0, (uint32_t)(i1 - i0), hi.d->segs, pi.d_ptrs, si, lo, hi.d->cks_in,
+        CK(launch_pack(false, hi.grid_items + i0, (uint32_t)(i1 - i0), hi.d->segs, pi.d_ptrs, si, lo, hi.d->cks_in,
                        pi.ctr, pi.kern));
-        if ((st = tend(c, pi, pi.kern, ta, PLEX_STAT_UNPACK, 2 * hi.d->bucket_payload[k]))) return st;
-        CK(cudaEventRecord(pi.ev_k[slot], pi.kern));
+        if ((st = tend(c, pi, pi.kern, ta, PLEX_STAT_UNPACK, 2 * hi.payload[k]))) return st;
+        CK(cudaEventRecord(pi.ev_k[si_slot], pi.kern));
         // D2H A_k (after H2D B_k read this slab range)
-        CK(cudaStreamWaitEvent(po.copy, po.ev_k[slot], 0));
-        CK(cudaStreamWaitEvent(po.copy, pi.ev_c[slot], 0));
+        CK(cudaStreamWaitEvent(po.copy, po.ev_k[so_slot], 0));
+        CK(cudaStreamWaitEvent(po.copy, pi.ev_c[si_slot], 0));
         if ((st = tbeg(c, po, po.copy, &ta))) return st;
         CK(cudaMemcpyAsync(slab->host + lo, so, len, cudaMemcpyDeviceToHost, po.copy));
         if ((st = tend(c, po, po.copy, ta, PLEX_STAT_D2H, len))) return st;
-        CK(cudaEventRecord(po.ev_c[slot], po.copy));
+        CK(cudaEventRecord(po.ev_c[so_slot], po.copy));
     }
+    // on_end re-derives B's params (elided) after every A pack on the same stream
     if ((st = off_end(c, po, ho)) || (st = on_end(c, pi, hi))) return st;
     CK(cudaEventRecord(c->ev_pack_done, c->copy2));
     CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
@@ -1489,7 +1527,7 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
     slab->cks.swap(ho.cks);                    // the slab now holds A (checksums recorded by its pack)
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
-    slab->elided = false;
+    slab->elided = shifted && !a_prefix;
     if (*pi.h_flag) {
         set_error("swap: %d segment checksum(s) of the incoming state differ from its offload", *pi.h_flag);
         return PLEX_E_CHECKSUM;

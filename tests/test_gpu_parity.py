@@ -346,6 +346,53 @@ def test_inplace_swap_matches_oracle(model, W, layout, bucket):
         m.close()
 
 
+@pytest.mark.parametrize("model,W,bucket", [("mid", 1, 1 << 14), ("toy-odd", 3, 1024)])
+@pytest.mark.parametrize("a_derived,b_derived", [(True, True), (True, False), (False, True), (False, False)])
+def test_inplace_swap_with_elision(model, W, bucket, a_derived, b_derived):
+    """NEXT-2 inside the swap: both jobs derivable -> both walk the shifted grid
+    (params derived, not moved); only the incoming one elided -> the outgoing
+    PARAM prefix goes out first; only the outgoing derivable -> it goes in full."""
+    man = manifest(model)
+    plan = P.Plan(man, world=W, bucket_bytes=bucket, tile_bytes=512, elide_param=True)
+
+    def state(seed, derived):
+        f = full_state(model, seed=seed, special_bits=0 if derived else 3)
+        if derived:
+            for (k, kd) in list(f):
+                if kd == 1:
+                    f[(k, 0)] = O.rne_bf16(f[(k, 1)])
+        return f
+
+    fa, fb = state(51, a_derived), state(52, b_derived)
+    for r in range(W):
+        m = mgr(W, r, bucket=bucket, slots=2)
+        oa, ob = fsdp_shards(fa, W, r, O.fsdp_rows), fsdp_shards(fb, W, r, O.fsdp_rows)
+        segs, size = O.slab_layout(man, W, r)
+        cut = plan.rank_info(r).elide_bytes
+        dev = {kk: to_dev(x, kk[1]) for kk, x in ob.items()}
+        slab = P.Slab(plan, r)
+        m.offload(plan, dev, slab)
+        assert slab.elided == b_derived
+        for kk, x in oa.items():
+            dev[kk].copy_(to_dev(x, kk[1]))
+        derived = {"a": a_derived, "b": b_derived}
+        cur_in, cur_out = "b", "a"
+        for it in range(3):
+            want_el = slab.elided and derived[cur_out]
+            m.swap(plan, dev, slab)
+            now_dev = ob if cur_in == "b" else oa
+            now_slab = oa if cur_out == "a" else ob
+            for kk, x in dev.items():
+                assert np.array_equal(bits_np(x), now_dev[kk]), (it, kk)
+            assert slab.elided == want_el, it
+            c0 = cut if want_el else 0
+            assert np.array_equal(slab.host_bytes()[c0:], O.pack_slab(segs, size, now_slab)[c0:]), it
+            want_ck = np.array(O.segment_checksums(segs, now_slab), dtype=np.uint64).reshape(-1, 2)
+            assert np.array_equal(slab.checksums(), want_ck), it
+            cur_in, cur_out = cur_out, cur_in
+        m.close()
+
+
 def test_job_swap_with_shares_one_device_copy():
     man = manifest("mid")
     m = mgr(1, 0, bucket=1 << 16)
