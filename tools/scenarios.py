@@ -139,9 +139,10 @@ def scen_duplex(a, c: Ctx):
 
 
 def scen_elide(a, c: Ctx):
-    """NEXT-2: the duplex switch of `duplex` with bf16 params = RNE(master) (what a
+    """NEXT-2: the bench step (switch + sync) with bf16 params = RNE(master) (what a
     mixed-precision optimizer step leaves) and PLEX_PLAN_ELIDE_PARAM: the param
-    buckets are checked on the device and re-derived on resume instead of moved."""
+    buckets are checked on the device and re-derived on resume instead of moved.
+    Duplex switch when two device copies fit, else the in-place swap (bench N=1)."""
     shape = MODELS[a.model]
     tp = a.tp or min(2, c.world)
     mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
@@ -149,21 +150,32 @@ def scen_elide(a, c: Ctx):
     for elide in (False, True):
         plans = [mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, elide_param=elide)
                  for _ in range(2)]
-        jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic(derived_param=True) for pl, s in zip(plans, (1, 2))]
+        info = plans[0].rank_info(c.rank)
+        free, _ = torch.cuda.mem_get_info(c.local)
+        swap = c.allmin(1.0 if 2 * info.payload_bytes + info.dst_arena_bytes + (6 << 30) < free else 0.0) < 0.5
+        if swap:
+            jobs = [P.Job(mgr, plans[0], seed=1, slab=False).alloc(), P.Job(mgr, plans[0], seed=2)]
+            jobs[1].shards = jobs[0].shards
+            jobs[1].init_synthetic(derived_param=True)
+            jobs[1].suspend(release=False)
+            jobs[1].shards = type(jobs[0].shards)()
+            jobs[0].init_synthetic(derived_param=True)
+        else:
+            jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic(derived_param=True) for pl, s in zip(plans, (1, 2))]
+            jobs[1].suspend()
         arena = mgr.arena(plans[0])
-        jobs[1].suspend()
         state = {"cur": 0}
 
         def step():
             i = state["cur"]
-            jobs[i].switch_to(jobs[1 - i])
+            (jobs[i].swap_with if swap else jobs[i].switch_to)(jobs[1 - i])
             jobs[1 - i].sync(arena)
             state["cur"] = 1 - i
 
         ms, clk = timed(c, step, a.steps, a.warmup)
-        out["elided" if elide else "full"] = {"switch_plus_sync_ms": round(ms, 2),
+        out["elided" if elide else "full"] = {"switch_plus_sync_ms": round(ms, 2), "mode": "swap" if swap else "duplex",
                                               "slab_elided": bool(jobs[1 - state["cur"]].slab.elided),
-                                              "elide_bytes_per_rank": plans[0].rank_info(c.rank).elide_bytes}
+                                              "elide_bytes_per_rank": info.elide_bytes}
         del jobs, arena, plans
         torch.cuda.empty_cache()
     c.emit({"scenario": "elide", "model": a.model, "n_gpus": c.world, "layout": f"FSDP-{c.world}->TP-{tp}",
