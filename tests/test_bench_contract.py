@@ -23,3 +23,32 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["unit"] == d["unit"]
     assert d["value"] > 0
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [[], ["--swap"]])
+def test_cuda_arm_json_line(extra):
+    """The CUDA arm on a small shape: every contract key, a roofline object for the
+    dominant kernel, clocks sampled during the timed region, our launches counted."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--model", "mid", "--steps", "3",
+                        "--warmup", "3", "--bucket-mb", "1", "--no-cpu-baseline"] + extra,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "rooflines", "clocks", "e2e",
+              "gpu_launches"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    rl = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in rl, k
+    assert rl["bound"] == "hbm" and 0 < rl["frac"] < 1.5 and rl["unit"] == "GB/s"
+    assert d["config"]["workload"] and d["config"]["switch_mode"] == ("swap" if extra else "duplex")
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] > 0 and d["clocks"]["samples"] > 0
