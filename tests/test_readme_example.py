@@ -1,0 +1,23 @@
+"""The README's usage block runs as written (checkpoint path redirected to tmp)."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+def test_readme_usage_block(tmp_path):
+    text = open(os.path.join(ROOT, "README.md")).read()
+    code = re.search(r"## Using it\n\n```python\n(.*?)```", text, re.S).group(1)
+    code = code.replace("/nvme/a.safetensors", str(tmp_path / "a.safetensors"))
+    ns = {}
+    exec(compile(code, "README.md", "exec"), ns)
+    ns["a"].slab  # the background checkpoint thread runs on
+    import threading
+    for t in threading.enumerate():
+        if t is not threading.current_thread() and t.daemon:
+            t.join(timeout=120)
+    assert os.path.getsize(tmp_path / "a.safetensors") > 0
+    ns["mgr"].close()
