@@ -54,7 +54,14 @@ def main():
     tp = min(2, world)
     dp = world // tp
     mgr = P.StateManager(device=local, rank=rank, world=world)
-    plans = [mgr.plan(man, head_dim=shape.head_dim, tp=tp, dp=dp) for _ in range(2)]
+    # bench.py's launch configuration: AUTO rank map, host-link balancing (here
+    # with rank 0's link twice as fast, so the other ranks' buckets are carried)
+    weights = [2.0 if r == 0 else 1.0 for r in range(world)]
+    plans = [mgr.plan(man, head_dim=shape.head_dim, tp=tp, dp=dp, rank_map=2, link_weights=weights)
+             for _ in range(2)]
+    for pl in plans:
+        mgr.enable_carry(pl)
+    rmap = plans[0].stats().rank_map
     b = P.Job(mgr, plans[1], seed=2).alloc().init_synthetic()
     ck_b = dev_checksums(plans[1], b, rank)
     b.suspend()
@@ -94,7 +101,7 @@ def main():
         if ".gate_proj." in key:
             keys += [key.replace(".gate_proj.", ".up_proj.")]
         cast = {k: O.rne_bf16(gen_tensor(1, k, 1, shapes[k])) for k in keys}
-        want = O.rollout_tensors(cast, tp, dp, 1, rank, O.TP_FAST, shape.head_dim)
+        want = O.rollout_tensors(cast, tp, dp, 1, rank, rmap, shape.head_dim)
         for name, x in want.items():
             if not np.array_equal(bits_np(views[name]), x):
                 print(f"[rank {rank}] sync mismatch {name}", flush=True)
@@ -111,12 +118,35 @@ def main():
         if ".gate_proj." in key:
             keys += [key.replace(".gate_proj.", ".up_proj.")]
         cast = {k: O.rne_bf16(gen_tensor(1, k, 1, shapes[k])) for k in keys}
-        want = O.rollout_tensors(cast, tp, dp, 1, rank, O.TP_FAST, shape.head_dim)
+        want = O.rollout_tensors(cast, tp, dp, 1, rank, rmap, shape.head_dim)
         for name, x in want.items():
             if not np.array_equal(bits_np(views[name]), x):
                 print(f"[rank {rank}] nccl sync mismatch {name}", flush=True)
                 bad += 1
     mgr_nccl.close()
+    if rank == 0:
+        print(f"carried buckets per job: {len(plans[0].carry())}, rank map {rmap}", flush=True)
+    del a, b, arena, views
+    torch.cuda.empty_cache()
+    # NEXT-2 ZeRO-2 replicas at full size: dedup slab + NVLink all-gather
+    rp = mgr.plan(man, replica_param=True)
+    r = P.Job(mgr, rp, seed=3).alloc().init_synthetic()
+    ck_p = torch.zeros((len(man), 2), dtype=torch.int64, device="cuda")
+    for t_, (key, _) in enumerate(man):
+        P.checksum(r.shards[(key, 0)], 0, out=ck_p[t_])
+    r.suspend()
+    r.resume()
+    ck_p2 = torch.zeros_like(ck_p)
+    for t_, (key, _) in enumerate(man):
+        P.checksum(r.shards[(key, 0)], 0, out=ck_p2[t_])
+    if not torch.equal(ck_p, ck_p2):
+        print(f"[rank {rank}] replica restore mismatch", flush=True)
+        bad += 1
+    for key in SAMPLE[:3]:
+        if not np.array_equal(bits_np(r.shards[(key, 0)]).reshape(-1), gen_tensor(3, key, 0, shapes[key]).reshape(-1)):
+            print(f"[rank {rank}] replica sample mismatch {key}", flush=True)
+            bad += 1
+    del r
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()
