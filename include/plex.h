@@ -91,6 +91,9 @@ typedef int plex_status;
 
 /* Context flags. */
 #define PLEX_CTX_TIMING    0x1u  /* record CUDA events around every kernel/copy */
+#define PLEX_CTX_CARRY_NCCL 0x4u /* carried buckets (NEXT-1 balancing) via NCCL send/recv
+                                    through the carrier's staging instead of the default
+                                    peer-memory transport (baseline) */
 #define PLEX_CTX_SYNC_NCCL 0x2u  /* weight sync via K4 pack + NCCL send/recv + K5
                                     unpack instead of the fused NVLink push     */
 

@@ -21,7 +21,7 @@ SLAB_KIND_MAJOR, SLAB_KEY_MAJOR = 0, 1
 RANKMAP_TP_FAST, RANKMAP_DP_FAST, RANKMAP_AUTO = 0, 1, 2
 OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
 RES_DEVICE, RES_HOST, RES_DISK = 0, 1, 2
-CTX_TIMING, CTX_SYNC_NCCL = 0x1, 0x2
+CTX_TIMING, CTX_SYNC_NCCL, CTX_CARRY_NCCL = 0x1, 0x2, 0x4
 SLAB_HUGEPAGE = 0x1
 STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE, \
     STAT_BARRIER, STAT_GATHER = range(11)

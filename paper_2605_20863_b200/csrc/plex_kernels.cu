@@ -607,6 +607,48 @@ cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, cons
     return cudaGetLastError();
 }
 
+// ---- NEXT-1 carried buckets over peer memory: cross-GPU stream handshakes --------------
+// One thread.  signal: make this stream's prior work visible system-wide, then
+// publish `v` at `flag` (local or peer-mapped).  wait: spin (acquire, system
+// scope) until `*flag >= v`; gives up after `timeout_ns` and raises `*err`
+// instead of hanging the GPU.
+__global__ void signal_kernel(unsigned long long* flag, unsigned long long v) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void wait_kernel(const unsigned long long* flag, unsigned long long v, unsigned long long timeout_ns,
+                            int* err) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (;;) {
+        unsigned long long x;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(flag) : "memory");
+        if (x >= v) return;
+        if (globaltimer_ns() - t0 > timeout_ns) {
+            atomicExch(err, 1);
+            return;
+        }
+        __nanosleep(1000);
+    }
+}
+
+cudaError_t launch_signal(unsigned long long* flag, unsigned long long v, cudaStream_t s) {
+    signal_kernel<<<1, 1, 0, s>>>(flag, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wait(const unsigned long long* flag, unsigned long long v, unsigned long long timeout_ns, int* err,
+                        cudaStream_t s) {
+    wait_kernel<<<1, 1, 0, s>>>(flag, v, timeout_ns, err);
+    return cudaGetLastError();
+}
+
 static inline uint32_t grid_for(uint64_t work, uint32_t per_block) {
     uint64_t b = (work + per_block - 1) / per_block;
     const uint64_t cap = 148ull * 16;

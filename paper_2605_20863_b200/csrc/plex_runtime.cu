@@ -44,6 +44,9 @@ cudaError_t launch_synth(void* dst, int kind, uint64_t base, uint64_t index_base
 cudaError_t launch_mutate(void* buf, int esize, uint64_t base, uint64_t index_base, uint64_t n, cudaStream_t s);
 cudaError_t launch_checksum(const void* src, int es, uint64_t index_base, uint64_t n, unsigned long long* out,
                             cudaStream_t s);
+cudaError_t launch_signal(unsigned long long* flag, unsigned long long v, cudaStream_t s);
+cudaError_t launch_wait(const unsigned long long* flag, unsigned long long v, unsigned long long timeout_ns, int* err,
+                        cudaStream_t s);
 cudaError_t launch_derive(bool check, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                           uint32_t n_tensors, unsigned long long* cks, int* bad, cudaStream_t s);
 // NCCL-baseline sync kernels (plex_nccl_sync.cu)
@@ -146,6 +149,14 @@ struct plex_ctx_s {
     cudaStream_t ckern = nullptr, cstream = nullptr, ccopy = nullptr;
     cudaEvent_t ev_cs[4] = {}, ev_cc[4] = {}, ev_cbeg = nullptr, ev_cend = nullptr;
     bool carry_used = false;            // the current blocking op enqueued carry work
+    // peer-memory carry transport (default): handshake flags READY[4] FREE[4]
+    // per rank (u64 sequence numbers) + a timeout flag; peers' carry staging
+    // and flags mapped over CUDA IPC; one sequence epoch per carry phase
+    unsigned long long* cflags = nullptr;
+    int* cerr = nullptr;
+    int* h_cerr = nullptr;
+    std::vector<void*> peer_cstaging, peer_cflags;
+    uint64_t cepoch = 0;
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
@@ -157,8 +168,9 @@ struct plex_ctx_s {
     // peer arenas opened over CUDA IPC: rank -> (peer's buffer id, mapped base)
     // peer mappings per (arena role, rank): role 0 = rollout arena, 1 = param arena
     std::map<int, std::pair<uint64_t, void*>> peers;
-    uint64_t my_buffer_id[2] = {0, 0};  // arena last exported per role (and its cached handle)
-    cudaIpcMemHandle_t my_handle[2]{};
+    // roles: 0 rollout arena, 1 param arena, 2 carry staging, 3 carry flags
+    uint64_t my_buffer_id[4] = {0, 0, 0, 0};  // buffer last exported per role (and its cached handle)
+    cudaIpcMemHandle_t my_handle[4]{};
     std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
     cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
 };
@@ -180,6 +192,10 @@ struct plex_slab_s {
     uint64_t carry_bytes = 0;
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
 };
+
+extern "C" {
+static plex_status exchange_arenas(plex_ctx_s* c, int role, void* arena, std::vector<void*>& arenas);
+}
 
 namespace plex {
 
@@ -339,6 +355,15 @@ static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
             CK(cudaStreamSynchronize(s2));
         }
         c->carry_used = false;
+        if (c->cerr) {
+            CK(cudaMemcpy(c->h_cerr, c->cerr, sizeof(int), cudaMemcpyDeviceToHost));
+            if (*c->h_cerr) {
+                CK(cudaMemset(c->cerr, 0, sizeof(int)));
+                *c->h_cerr = 0;
+                set_error("carried-bucket handshake with a peer timed out (a rank did not take part?)");
+                return PLEX_E_CUDA;
+            }
+        }
     }
     CK(cudaStreamSynchronize(c->pack));
     CK(cudaStreamSynchronize(c->copy));
@@ -444,12 +469,26 @@ static void use_grid(Half& h, bool elide) {
 }
 
 // ---- NEXT-1 host-link balancing: carried buckets -----------------------------------
-// Every rank walks the plan's global carry list in order and issues only the
-// NCCL sends/receives it takes part in, on its one carry stream: both ends of
-// every pair see their common transfers in the same order, and the global
-// order rules out cycles.  Offload: the owner packs a carried bucket into a
-// carry slot (ckern) and sends it; the carrier receives it into its slot and
-// D2H-copies it into its pinned carry region (ccopy).  Onload mirrors it.
+// Every rank walks the plan's global carry list in order and takes part only in
+// the transfers it owns or carries, on its carry streams: both ends of every
+// pair see their common transfers in the same order, and the global order
+// rules out cycles.
+//
+// Default transport, over peer memory (no NCCL, no carrier staging):
+//   offload  owner:   [wait FREE[s]] pack bucket -> own slot s ; READY[s] = seq
+//            carrier: wait owner's READY[s] ; D2H owner's slot (its copy engine
+//                     reads the peer over NVLink) -> pinned carry region ;
+//                     owner's FREE[s] = seq
+//   onload   carrier: [wait owner's FREE[s]] H2D carry region -> owner's slot
+//                     (written over NVLink) ; owner's READY[s] = seq
+//            owner:   wait READY[s] ; unpack own slot s ; FREE[s] = seq
+// Flags are u64 sequence numbers (epoch << 20 | transfer + 1) in the owner's
+// memory, set by one-thread release stores and polled by one-thread acquire
+// spins (timeout -> PLEX_E_CUDA, never a hung GPU).  PLEX_CTX_CARRY_NCCL keeps
+// the NCCL send/recv transport (owner slot -> carrier slot -> D2H) as baseline.
+static constexpr unsigned long long kCarryTimeoutNs = 120ull * 1000000000ull;
+enum { kReady = 0, kFree = 4 };
+
 static plex_status carry_ready(plex_ctx_s* c, const Plan& p) {
     if (p.carry.empty()) return PLEX_OK;
     if (!c->comm) { set_error("carried buckets need a ctx with an NCCL communicator"); return PLEX_E_INVAL; }
@@ -468,6 +507,114 @@ static plex_status carry_ready(plex_ctx_s* c, const Plan& p) {
         CK(cudaEventCreateWithFlags(&c->ev_cbeg, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_cend, cudaEventDisableTiming));
     }
+    if (!(c->flags & PLEX_CTX_CARRY_NCCL)) {
+        if (!c->cflags) {
+            void* f = nullptr;
+            CK(cudaMalloc(&f, 4096));
+            CK(cudaMemset(f, 0, 4096));
+            c->cflags = reinterpret_cast<unsigned long long*>(f);
+            c->cerr = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(f) + 2048);
+            CK(cudaHostAlloc(&c->h_cerr, sizeof(int), cudaHostAllocDefault));
+            *c->h_cerr = 0;
+        }
+        plex_status st;
+        if ((st = exchange_arenas(c, 2, c->cstaging, c->peer_cstaging)) ||
+            (st = exchange_arenas(c, 3, c->cflags, c->peer_cflags)))
+            return st;
+    }
+    return PLEX_OK;
+}
+
+static unsigned long long* peer_flag(plex_ctx_s* c, int rank, int idx) {
+    return reinterpret_cast<unsigned long long*>(c->peer_cflags[rank]) + idx;
+}
+
+// offload direction over peer memory (owner slots 0-1)
+static plex_status carry_out_p2p(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const Plan& p = *h.p;
+    const RankPlan& R = *h.R;
+    const unsigned long long epoch = ++c->cepoch;
+    std::vector<int> k_of(p.world, 0);                          // transfers per owner so far
+    std::vector<unsigned long long> last(2, 0);                 // own slots: seq of their last use
+    plex_status st;
+    for (size_t i = 0; i < p.carry.size(); ++i) {
+        const CarryXfer& x = p.carry[i];
+        const int k = k_of[x.owner]++;
+        const int sl = k % 2;
+        const unsigned long long seq = (epoch << 20) | (unsigned long long)(i + 1);
+        cudaEvent_t ta = nullptr;
+        if (x.owner == c->rank) {
+            if (last[sl]) CK(launch_wait(peer_flag(c, c->rank, kFree + sl), last[sl], kCarryTimeoutNs, c->cerr, c->ckern));
+            uint8_t* slot = c->cstaging + (uint64_t)sl * p.bucket;
+            const uint64_t i0 = R.bucket_item_start[x.bucket], i1 = R.bucket_item_start[x.bucket + 1];
+            if ((st = tbeg(c, pp, c->ckern, &ta))) return st;
+            CK(launch_pack(true, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, slot, x.lo, h.d->cks,
+                           c->d_ctr + 4, c->ckern));
+            if ((st = tend(c, pp, c->ckern, ta, PLEX_STAT_PACK, 2 * h.d->bucket_payload[x.bucket]))) return st;
+            CK(launch_signal(peer_flag(c, c->rank, kReady + sl), seq, c->ckern));
+            last[sl] = seq;
+        } else if (x.carrier == c->rank) {
+            CK(launch_wait(peer_flag(c, x.owner, kReady + sl), seq, kCarryTimeoutNs, c->cerr, c->ccopy));
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(c->peer_cstaging[x.owner]) + (uint64_t)sl * p.bucket;
+            if ((st = tbeg(c, pp, c->ccopy, &ta))) return st;
+            CK(cudaMemcpyAsync(h.slab->carry_host + x.coff, src, x.len, cudaMemcpyDeviceToHost, c->ccopy));
+            if ((st = tend(c, pp, c->ccopy, ta, PLEX_STAT_D2H, x.len))) return st;
+            CK(launch_signal(peer_flag(c, x.owner, kFree + sl), seq, c->ccopy));
+        }
+    }
+    // the call ends only when every carrier has copied this rank's slots out
+    for (int sl = 0; sl < 2; ++sl)
+        if (last[sl]) CK(launch_wait(peer_flag(c, c->rank, kFree + sl), last[sl], kCarryTimeoutNs, c->cerr, c->ckern));
+    return PLEX_OK;
+}
+
+// onload direction over peer memory (owner slots 2-3)
+static plex_status carry_in_p2p(plex_ctx_s* c, Pipe& pp, Half& h) {
+    const Plan& p = *h.p;
+    const RankPlan& R = *h.R;
+    const unsigned long long epoch = ++c->cepoch;
+    std::vector<int> k_of(p.world, 0);
+    std::vector<std::vector<unsigned long long>> last(p.world, std::vector<unsigned long long>(2, 0));
+    plex_status st;
+    for (size_t i = 0; i < p.carry.size(); ++i) {
+        const CarryXfer& x = p.carry[i];
+        const int k = k_of[x.owner]++;
+        const int sl = 2 + k % 2;
+        const unsigned long long seq = (epoch << 20) | (unsigned long long)(i + 1);
+        const unsigned long long prev = last[x.owner][sl - 2];
+        last[x.owner][sl - 2] = seq;
+        cudaEvent_t ta = nullptr;
+        if (x.carrier == c->rank) {
+            if (prev) CK(launch_wait(peer_flag(c, x.owner, kFree + sl), prev, kCarryTimeoutNs, c->cerr, c->ccopy));
+            uint8_t* dst = reinterpret_cast<uint8_t*>(c->peer_cstaging[x.owner]) + (uint64_t)sl * p.bucket;
+            if ((st = tbeg(c, pp, c->ccopy, &ta))) return st;
+            CK(cudaMemcpyAsync(dst, h.slab->carry_host + x.coff, x.len, cudaMemcpyHostToDevice, c->ccopy));
+            if ((st = tend(c, pp, c->ccopy, ta, PLEX_STAT_H2D, x.len))) return st;
+            CK(launch_signal(peer_flag(c, x.owner, kReady + sl), seq, c->ccopy));
+        } else if (x.owner == c->rank) {
+            CK(launch_wait(peer_flag(c, c->rank, kReady + sl), seq, kCarryTimeoutNs, c->cerr, c->ckern));
+            uint8_t* slot = c->cstaging + (uint64_t)sl * p.bucket;
+            const uint64_t i0 = R.bucket_item_start[x.bucket], i1 = R.bucket_item_start[x.bucket + 1];
+            if ((st = tbeg(c, pp, c->ckern, &ta))) return st;
+            CK(launch_pack(false, h.d->items + i0, (uint32_t)(i1 - i0), h.d->segs, pp.d_ptrs, slot, x.lo,
+                           h.d->cks_in, c->d_ctr + 5, c->ckern));
+            if ((st = tend(c, pp, c->ckern, ta, PLEX_STAT_UNPACK, 2 * h.d->bucket_payload[x.bucket]))) return st;
+            CK(launch_signal(peer_flag(c, c->rank, kFree + sl), seq, c->ckern));
+        }
+    }
+    // a carrier's call ends only when the owners have unpacked what it wrote
+    {
+        std::vector<int> k2(p.world, 0);
+        std::vector<std::vector<unsigned long long>> mine(p.world, std::vector<unsigned long long>(2, 0));
+        for (size_t i = 0; i < p.carry.size(); ++i) {
+            const CarryXfer& x = p.carry[i];
+            const int k = k2[x.owner]++;
+            if (x.carrier == c->rank) mine[x.owner][k % 2] = (epoch << 20) | (unsigned long long)(i + 1);
+        }
+        for (int g = 0; g < p.world; ++g)
+            for (int j = 0; j < 2; ++j)
+                if (mine[g][j]) CK(launch_wait(peer_flag(c, g, kFree + 2 + j), mine[g][j], kCarryTimeoutNs, c->cerr, c->ccopy));
+    }
     return PLEX_OK;
 }
 
@@ -478,6 +625,12 @@ static plex_status carry_out(plex_ctx_s* c, Pipe& pp, Half& h) {
     plex_status st;
     if ((st = carry_ready(c, p))) return st;
     c->carry_used = true;
+    if (!(c->flags & PLEX_CTX_CARRY_NCCL)) {
+        CK(cudaEventRecord(c->ev_cbeg, pp.kern));             // pointer table + zeroed checksums
+        CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
+        CK(cudaStreamWaitEvent(c->ccopy, c->ev_cbeg, 0));
+        return carry_out_p2p(c, pp, h);
+    }
     CK(cudaEventRecord(c->ev_cbeg, pp.kern));                 // pointer table + zeroed checksums
     CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
     CK(cudaStreamWaitEvent(c->cstream, c->ev_cbeg, 0));
@@ -522,6 +675,12 @@ static plex_status carry_in(plex_ctx_s* c, Pipe& pp, Half& h) {
     plex_status st;
     if ((st = carry_ready(c, p))) return st;
     c->carry_used = true;
+    if (!(c->flags & PLEX_CTX_CARRY_NCCL)) {
+        CK(cudaEventRecord(c->ev_cbeg, pp.kern));
+        CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
+        CK(cudaStreamWaitEvent(c->ccopy, c->ev_cbeg, 0));
+        return carry_in_p2p(c, pp, h);
+    }
     CK(cudaEventRecord(c->ev_cbeg, pp.kern));
     CK(cudaStreamWaitEvent(c->ckern, c->ev_cbeg, 0));
     CK(cudaStreamWaitEvent(c->cstream, c->ev_cbeg, 0));
@@ -844,6 +1003,8 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     cudaFree(c->d_ctr);
     cudaFree(c->d_scratch);
     cudaFreeHost(c->h_scratch);
+    if (c->cflags) cudaFree(c->cflags);
+    if (c->h_cerr) cudaFreeHost(c->h_cerr);
     delete c;
     return PLEX_OK;
 }

@@ -359,7 +359,7 @@ class StateManager:
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 2 << 30,
                  n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
-                 nccl_id: Optional[bytes] = None, duplex: bool = True):
+                 nccl_id: Optional[bytes] = None, duplex: bool = True, carry_nccl: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("StateManager needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -377,7 +377,8 @@ class StateManager:
             if nccl_id is None:
                 nccl_id = self._bootstrap_id()
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
-        flags = (L.CTX_TIMING if timing else 0) | (L.CTX_SYNC_NCCL if sync_nccl else 0)
+        flags = ((L.CTX_TIMING if timing else 0) | (L.CTX_SYNC_NCCL if sync_nccl else 0)
+                 | (L.CTX_CARRY_NCCL if carry_nccl else 0))
         h = C.c_void_p()
         check(lib.plex_ctx_create(device, self.staging.data_ptr(), self.staging.numel(), n_slots,
                                   self.pack_stream.cuda_stream, self.copy_stream.cuda_stream,

@@ -34,8 +34,20 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    bad = 0
+    for carry_nccl in (False, True):          # peer-memory transport (default), NCCL baseline
+        bad += run(rank, world, local, carry_nccl)
+    t = torch.tensor([bad], device=f"cuda:{local}")
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mp_carry_worker world={world} mismatches={int(t.item())}", flush=True)
+    sys.exit(1 if int(t.item()) else 0)
+
+
+def run(rank, world, local, carry_nccl):
     bucket = 1 << 16
-    mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=2)
+    mgr = P.StateManager(device=local, rank=rank, world=world, bucket_bytes=bucket, n_slots=2, carry_nccl=carry_nccl)
     weights = [1.0] + [4.0] * (world - 1)
     bad = 0
     models = ("mid", "mid-moe")
@@ -93,13 +105,16 @@ def main():
     check_shards(1)
     jobs[1].switch_to(jobs[0])
     check_shards(0)
-    t = torch.tensor([bad], device=f"cuda:{local}")
-    dist.all_reduce(t)
+    for _ in range(3):                      # repeated calls reuse the carry slots and flags
+        jobs[0].switch_to(jobs[1])
+        jobs[1].switch_to(jobs[0])
+    check_shards(0)
+    check_slabs(1)
     mgr.close()
-    dist.destroy_process_group()
     if rank == 0:
-        print(f"mp_carry_worker world={world} carried={len(plans[0].carry())} mismatches={int(t.item())}", flush=True)
-    sys.exit(1 if int(t.item()) else 0)
+        print(f"transport={'nccl' if carry_nccl else 'peer-memory'} carried={len(plans[0].carry())} "
+              f"mismatches(rank0)={bad}", flush=True)
+    return bad
 
 
 if __name__ == "__main__":
