@@ -573,9 +573,50 @@ def scen_zero2(a, c: Ctx):
             "speedup": round(ms2 / ms, 3), "clocks": clk}, a.out)
 
 
+def scen_carry(a, c: Ctx):
+    """NEXT-1 host-link balancing transports: the 7B duplex switch with rank 0's
+    link declared at half speed (so its last buckets are carried by the other
+    ranks), carried over peer memory (default: the carrier's copy engine reads /
+    writes the owner's slot over NVLink) vs NCCL send/recv through the
+    carrier's staging, and without carrying.  Bit-exact restores checked by
+    checksums."""
+    man = manifest(a.model)
+    shape = MODELS[a.model]
+    tp = a.tp or min(2, c.world)
+    out = {}
+    for name, kw, weights in (("no_carry", {}, None),
+                              ("peer_memory", {}, [0.5] + [1.0] * (c.world - 1)),
+                              ("nccl", {"carry_nccl": True}, [0.5] + [1.0] * (c.world - 1))):
+        mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20,
+                             timing=True, **kw)
+        plans = [mgr.plan(man, head_dim=shape.head_dim, tp=tp, dp=c.world // tp, link_weights=weights)
+                 for _ in range(2)]
+        for pl in plans:
+            mgr.enable_carry(pl)
+        jobs = [P.Job(mgr, pl, seed=s).alloc().init_synthetic() for pl, s in zip(plans, (1, 2))]
+        ref = [{k: P.checksum(v).cpu() for k, v in j.shards.items()} for j in jobs]
+        jobs[1].suspend()
+        state = {"cur": 0}
+
+        def step():
+            i = state["cur"]
+            jobs[i].switch_to(jobs[1 - i])
+            state["cur"] = 1 - i
+
+        ms, clk = timed(c, step, a.steps, a.warmup)
+        cur = jobs[state["cur"]]
+        ok = all(torch.equal(P.checksum(v).cpu(), ref[state["cur"]][k]) for k, v in cur.shards.items())
+        out[name] = {"switch_ms": round(ms, 1), "carried_buckets_per_job": len(plans[0].carry()),
+                     "bit_exact": bool(c.allmin(1.0 if ok else 0.0) > 0.5)}
+        del jobs, plans
+        mgr.close()
+        torch.cuda.empty_cache()
+    c.emit({"scenario": "carry", "model": a.model, "n_gpus": c.world, **out}, a.out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync", "zero2"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync", "zero2", "carry"])
     ap.add_argument("--spill-dir", default="/tmp")
     ap.add_argument("--io-threads", type=int, default=8)
     ap.add_argument("--time-scale", type=float, default=0.005)
@@ -592,10 +633,10 @@ def main():
     a = ap.parse_args()
     c = Ctx(a.gpus)
     if not a.model:
-        a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b", "zero2": "qwen2.5-7b"}.get(a.scenario, "")
+        a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b", "zero2": "qwen2.5-7b", "carry": "qwen2.5-7b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
      "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme,
-     "sync": scen_sync, "zero2": scen_zero2}[a.scenario](a, c)
+     "sync": scen_sync, "zero2": scen_zero2, "carry": scen_carry}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
         dist.destroy_process_group()
