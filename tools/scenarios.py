@@ -454,10 +454,14 @@ def scen_sync(a, c: Ctx):
     shape = MODELS[model]
     tp = a.tp or min(4, c.world)
     out = {}
-    for transport in ("push", "nccl"):
+    runs = [("push", 64 << 10), ("nccl", 64 << 10)]
+    if a.tiles:
+        runs = [("push", int(t)) for t in a.tiles.split(",")]
+    for transport, tile in runs:
         mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=256 << 20, timing=True,
                              sync_nccl=transport == "nccl", duplex=False)
-        plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO)
+        plan = mgr.plan(manifest(model), head_dim=shape.head_dim, tp=tp, dp=c.world // tp, rank_map=L.RANKMAP_AUTO,
+                        tile_bytes=tile)
         job = P.Job(mgr, plan, seed=2, slab=False).alloc(kinds=(1,)).init_synthetic()
         arena = mgr.arena(plan)
         mgr.reset_stats()
@@ -468,7 +472,7 @@ def scen_sync(a, c: Ctx):
         # data-moving time: the push kernel, or (NCCL) the whole call -- the
         # per-round exchange events include waiting for peers' K4 rounds
         t_x = c.allmax(st["push"]["ms"] / max(1, st["push"]["launches"])) if transport == "push" else ms
-        out[transport] = {"sync_ms": round(ms, 3), "data_ms": round(t_x, 3),
+        out[transport if not a.tiles else f"push_tile_{tile >> 10}KiB"] = {"sync_ms": round(ms, 3), "data_ms": round(t_x, 3),
                           "nvlink_GBs": round(nv / (t_x * 1e-3) / 1e9, 1) if c.world > 1 and t_x > 0 else None}
         del job, arena, plan
         mgr.close()
@@ -629,6 +633,7 @@ def main():
     ap.add_argument("--units", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--duplex", action="store_true")
+    ap.add_argument("--tiles", default="", help="sync scenario: push-kernel tile sizes (bytes) to compare")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     c = Ctx(a.gpus)
