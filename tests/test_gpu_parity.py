@@ -820,3 +820,34 @@ def test_timeline_records_cover_the_switch():
     for h_, u_ in zip(h2ds, unps):
         assert u_["start_ms"] >= h_["start_ms"] + h_["ms"] - 0.01
     m.close()
+
+
+def test_swap_with_replica_params_world1():
+    """In-place swap of two ZeRO-2 (replica_param) jobs: the full replicated
+    params travel with the device tensors; a non-replica plan is refused by
+    the all-gather."""
+    man = manifest("mid")
+    m = mgr(1, 0, bucket=1 << 15)
+    plan = m.plan(man, replica_param=True)
+    a = P.Job(m, plan, seed=61, slab=False).alloc()
+    b = P.Job(m, plan, seed=62)
+    b.shards, b.param_arena = a.shards, a.param_arena
+    b.init_synthetic(special_bits=3)
+    b.suspend(release=False)
+    b.shards, b.param_arena = OrderedDict(), None
+    a.init_synthetic(special_bits=3)
+    fa, fb = full_state("mid", seed=61, special_bits=3), full_state("mid", seed=62, special_bits=3)
+    a.swap_with(b)
+    assert b.param_arena is not None and a.param_arena is None
+    for kk, x in b.shards.items():
+        assert np.array_equal(bits_np(x), fb[kk]), kk
+    b.swap_with(a)
+    for kk, x in a.shards.items():
+        assert np.array_equal(bits_np(x), fa[kk]), kk
+    plain = m.plan(man)
+    with pytest.raises(ValueError):
+        m.param_allgather(plain, a.param_arena)
+    with pytest.raises(P.PlexError) as e:
+        P._lib.check(P._lib.lib.plex_param_allgather(m.h, plain.h, a.param_arena.data_ptr(), None))
+    assert e.value.code == L.E_INVAL
+    m.close()
