@@ -16,7 +16,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 
 #include "plex_internal.h"
 
@@ -408,62 +407,6 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
     }
 }
 
-// Variant of the push for destinations where large writes matter (peer arenas
-// over NVLink): the block casts its rectangle into shared memory, then one
-// thread stores it with TMA bulk copies (one per destination row).  Items the
-// bulk path cannot take (misaligned, > 32 KiB of bf16) use push_kernel's code.
-constexpr uint32_t kBulkSmem = 32u << 10;
-
-template <bool kCast>
-__global__ void __launch_bounds__(kThreads) push_bulk_kernel(const PushItem* __restrict__ items,
-                                                             const uint64_t* __restrict__ src_ptrs,
-                                                             const uint64_t* __restrict__ dst_arenas) {
-    extern __shared__ __align__(128) uint8_t sbuf[];
-    const PushItem it = items[blockIdx.x];
-    constexpr int kSrcEs = kCast ? 4 : 2;
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(src_ptrs[it.tensor]) + (uint64_t)it.src_elem * kSrcEs;
-    uint16_t* dst = reinterpret_cast<uint16_t*>(dst_arenas[it.dst_rank]) + it.dst_elem;
-    const uint32_t rows = it.rows, cols = it.cols, ss = it.src_stride, ds = it.dst_stride;
-    const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
-                     (cols % 8 == 0) && ((ss * kSrcEs) % 16 == 0) && (ds % 8 == 0) &&
-                     (uint64_t)rows * cols * 2 <= kBulkSmem;
-    auto load8 = [&](uint64_t e) -> uint4 {
-        if (kCast) {
-            const uint4 a = ld_stream(src + 4 * e), b = ld_stream(src + 4 * e + 16);
-            return rne_8(a, b);
-        } else {
-            return ld_stream(src + 2 * e);
-        }
-    };
-    if (!vec) {                                   // scalar fallback (as push_kernel)
-        const uint64_t total = (uint64_t)rows * cols;
-        for (uint64_t e = threadIdx.x; e < total; e += kThreads) {
-            const uint64_t r = e / cols, c = e - r * cols;
-            const uint64_t si = r * ss + c;
-            dst[r * ds + c] = kCast ? (uint16_t)rne_bf16(reinterpret_cast<const uint32_t*>(src)[si])
-                                    : reinterpret_cast<const uint16_t*>(src)[si];
-        }
-        return;
-    }
-    const uint32_t vpr = cols / 8, total = rows * vpr;
-    uint4* sv = reinterpret_cast<uint4*>(sbuf);
-    for (uint32_t v = threadIdx.x; v < total; v += kThreads) {
-        const uint32_t r = v / vpr, c = v - r * vpr;
-        sv[v] = load8((uint64_t)r * ss + 8 * c);                       // rows packed back to back
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // generic -> async proxy
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (ds == cols || rows == 1) {
-            bulk_store(dst, sbuf, rows * cols * 2);
-        } else {
-            for (uint32_t r = 0; r < rows; ++r) bulk_store(dst + (uint64_t)r * ds, sbuf + r * cols * 2, cols * 2);
-        }
-        bulk_commit();
-        bulk_wait_all();
-    }
-}
-
 // ---- NEXT-2: derived-param check / re-derivation -------------------------------
 // Over PackItems of PARAM segments: kCheck -> count elements whose bf16 param
 // differs from RNE(master) (R8) and checksum the params; !kCheck -> write
@@ -658,15 +601,8 @@ cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, cons
     const uint64_t kMax = 1ull << 30;
     for (uint64_t o = 0; o < n_items; o += kMax) {
         const uint64_t n = n_items - o < kMax ? n_items - o : kMax;
-        static const bool bulk = getenv("PLEX_PUSH_BULK") && getenv("PLEX_PUSH_BULK")[0] == '1';
-        if (bulk) {
-            if (cast) push_bulk_kernel<true><<<(uint32_t)n, kThreads, kBulkSmem, s>>>(items + o, src_ptrs, dst_arenas);
-            else push_bulk_kernel<false><<<(uint32_t)n, kThreads, kBulkSmem, s>>>(items + o, src_ptrs, dst_arenas);
-        } else if (cast) {
-            push_kernel<true><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
-        } else {
-            push_kernel<false><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
-        }
+        if (cast) push_kernel<true><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
+        else push_kernel<false><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
     }
     return cudaGetLastError();
 }
