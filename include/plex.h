@@ -103,6 +103,7 @@ typedef int plex_status;
 typedef struct plex_plan_s* plex_plan_t;
 typedef struct plex_ctx_s*  plex_ctx_t;
 typedef struct plex_slab_s* plex_slab_t;
+typedef struct plex_ckpt_s* plex_ckpt_t;     /* a background checkpoint */
 
 /* One logical (unsharded) tensor of the job's manifest, in canonical order
  * (R4).  2-D view [d0, d1]; 1-D tensors have d1 = 1, ndim = 1.
@@ -450,6 +451,15 @@ PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int
  * params; E_INVAL for plans that carry this rank's buckets; E_TIER_FULL on I/O
  * errors. */
 PLEX_API plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t slab, const char* path, int32_t threads);
+/* The same write on a library-owned background thread.  All checks run, and
+ * the slab becomes read-only, in the calling thread before this returns, so a
+ * swap / offload / restore issued right after it is refused (E_STATE) until
+ * plex_ckpt_wait; onload and sync-from-slab may proceed.  *out is released by
+ * plex_ckpt_wait, which joins the writer and returns its status (message via
+ * plex_last_error). */
+PLEX_API plex_status plex_slab_checkpoint_start(plex_plan_t plan, plex_slab_t slab, const char* path, int32_t threads,
+                                                plex_ckpt_t* out);
+PLEX_API plex_status plex_ckpt_wait(plex_ckpt_t ckpt);
 /* Inverse: fill an idle slab of `plan` from a checkpoint written by
  * plex_slab_checkpoint for the same plan and rank; residency becomes HOST with
  * the file's checksums, so the next onload verifies every tensor

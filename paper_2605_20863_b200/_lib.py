@@ -42,7 +42,7 @@ EXPORTS = [
     "plex_state_drain", "plex_state_prefetch", "plex_state_wait", "plex_state_poll", "plex_weight_sync_rank",
     "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
     "plex_plan_param_arena", "plex_param_allgather", "plex_param_allgather_rank",
-    "plex_slab_checkpoint", "plex_slab_restore", "plex_state_swap",
+    "plex_slab_checkpoint", "plex_slab_checkpoint_start", "plex_ckpt_wait", "plex_slab_restore", "plex_state_swap",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
 ]
 
@@ -154,6 +154,8 @@ def _load() -> C.CDLL:
         "plex_weight_sync_rank_from_slab": (C.c_int, [VP, VP, I32, VP, P(VP), I32, VP]),
         "plex_state_swap": (C.c_int, [VP, VP, P(VP), I32, VP, VP]),
         "plex_slab_checkpoint": (C.c_int, [VP, VP, C.c_char_p, I32]),
+        "plex_slab_checkpoint_start": (C.c_int, [VP, VP, C.c_char_p, I32, P(VP)]),
+        "plex_ckpt_wait": (C.c_int, [VP]),
         "plex_slab_restore": (C.c_int, [VP, VP, C.c_char_p, I32]),
         "plex_plan_param_arena": (C.c_int, [VP, I32, P(U64), P(U64)]),
         "plex_param_allgather": (C.c_int, [VP, VP, VP, VP]),

@@ -23,6 +23,7 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <string>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -79,6 +80,10 @@ struct DevPlan {
     unsigned long long* cks = nullptr;        // computed (S1,S2) per segment
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
     unsigned long long* cks_in = nullptr;     // recomputed at onload
+    // pinned host mirrors of the checksum tables: a device<->pageable copy would
+    // block the calling thread until the stream drains (async drain/prefetch)
+    uint64_t* h_cks_out = nullptr;            // offload: recorded (S1,S2), read back here
+    uint64_t* h_cks_want = nullptr;           // onload: expected (S1,S2), uploaded from here
     std::vector<uint64_t> bucket_payload;     // data bytes per bucket (stats)
     uint64_t elide_payload = 0;               // PARAM data bytes (derived when eliding)
     PackItem* items_el = nullptr;             // NEXT-2 shifted grid
@@ -157,6 +162,7 @@ struct plex_ctx_s {
     int* h_cerr = nullptr;
     std::vector<void*> peer_cstaging, peer_cflags;
     uint64_t cepoch = 0;
+    std::vector<std::vector<unsigned long long>> carry_in_last;   // [owner][onload slot] last seq written
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
@@ -175,6 +181,12 @@ struct plex_ctx_s {
     cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
 };
 
+struct plex_ckpt_s {                   // a background checkpoint (plex_slab_checkpoint_start)
+    std::thread th;
+    plex_status status = PLEX_OK;
+    std::string error;
+};
+
 struct plex_slab_s {
     uint64_t plan_id = 0;
     int rank = 0;
@@ -188,6 +200,7 @@ struct plex_slab_s {
     bool elided = false;                // NEXT-2: leading PARAM buckets derived, not stored
     std::atomic<bool> busy{false};      // an async drain / prefetch or a restore of this slab is in flight
     std::atomic<int> ckpt{0};           // checkpoints reading the slab (it is read-only meanwhile)
+    std::mutex mu;                      // makes "start a checkpoint" and "start a restore" exclusive
     uint8_t* carry_host = nullptr;      // other ranks' carried buckets (pinned)
     uint64_t carry_bytes = 0;
     std::vector<uint64_t> cks;          // 2 per segment, recorded at offload
@@ -214,6 +227,8 @@ static void free_devplan(DevPlan& d) {
     cudaFree(d.local);
     cudaFree(d.rpack);
     cudaFree(d.runpack);
+    cudaFreeHost(d.h_cks_out);
+    cudaFreeHost(d.h_cks_want);
     d = DevPlan{};
 }
 
@@ -239,7 +254,10 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     }
     const size_t nck = std::max<size_t>(1, 2 * R.segs.size());
     if (cudaMalloc(&d.cks, nck * 8) != cudaSuccess || cudaMalloc(&d.cks_want, nck * 8) != cudaSuccess ||
-        cudaMalloc(&d.cks_in, nck * 8) != cudaSuccess) {
+        cudaMalloc(&d.cks_in, nck * 8) != cudaSuccess ||
+        cudaHostAlloc(&d.h_cks_out, nck * 8, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&d.h_cks_want, nck * 8, cudaHostAllocDefault) != cudaSuccess) {
+        (void)cudaGetLastError();
         free_devplan(d);
         set_error("cudaMalloc of checksum tables failed");
         return PLEX_E_CUDA;
@@ -360,6 +378,12 @@ static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
             if (*c->h_cerr) {
                 CK(cudaMemset(c->cerr, 0, sizeof(int)));
                 *c->h_cerr = 0;
+                // nothing of this call may still write the slab or the tensors once it
+                // returns, and its events / pool slots must not leak into the next call
+                CK(cudaStreamSynchronize(c->pack));
+                CK(cudaStreamSynchronize(c->copy));
+                plex_status st2 = timed_collect(c);
+                if (st2) return st2;
                 set_error("carried-bucket handshake with a peer timed out (a rank did not take part?)");
                 return PLEX_E_CUDA;
             }
@@ -574,7 +598,11 @@ static plex_status carry_in_p2p(plex_ctx_s* c, Pipe& pp, Half& h) {
     const RankPlan& R = *h.R;
     const unsigned long long epoch = ++c->cepoch;
     std::vector<int> k_of(p.world, 0);
-    std::vector<std::vector<unsigned long long>> last(p.world, std::vector<unsigned long long>(2, 0));
+    // last sequence number written into (owner, onload slot), kept across calls:
+    // the first write of a call into a slot must wait for that slot's FREE flag of
+    // the previous call too (every rank derives the same values from the carry lists)
+    auto& last = c->carry_in_last;
+    if (last.size() != (size_t)p.world) last.assign(p.world, std::vector<unsigned long long>(2, 0));
     plex_status st;
     for (size_t i = 0; i < p.carry.size(); ++i) {
         const CarryXfer& x = p.carry[i];
@@ -779,8 +807,13 @@ static plex_status off_bucket(plex_ctx_s* c, Pipe& pp, Half& h, int32_t b) {
 
 static plex_status off_end(plex_ctx_s* c, Pipe& pp, Half& h) {
     (void)c;
-    if (!h.cks.empty()) CK(cudaMemcpyAsync(h.cks.data(), h.d->cks, 8 * h.cks.size(), cudaMemcpyDeviceToHost, pp.kern));
+    if (!h.cks.empty()) CK(cudaMemcpyAsync(h.d->h_cks_out, h.d->cks, 8 * h.cks.size(), cudaMemcpyDeviceToHost, pp.kern));
     return PLEX_OK;
+}
+
+// After the offload's streams completed: the recorded checksums, from the pinned mirror.
+static void off_collect(Half& h) {
+    if (!h.cks.empty()) std::memcpy(h.cks.data(), h.d->h_cks_out, 8 * h.cks.size());
 }
 
 static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
@@ -788,7 +821,13 @@ static plex_status on_begin(plex_ctx_s* c, Pipe& pp, Half& h) {
     const size_t nck = 2 * h.R->segs.size();
     CK(cudaMemcpyAsync(pp.d_ptrs, pp.h_ptrs, np * 8, cudaMemcpyHostToDevice, pp.kern));
     CK(cudaMemsetAsync(h.d->cks_in, 0, 8 * std::max<size_t>(2, nck), pp.kern));
-    if (nck) CK(cudaMemcpyAsync(h.d->cks_want, h.slab->cks.data(), 8 * nck, cudaMemcpyHostToDevice, pp.kern));
+    if (nck) {
+        // the pinned mirror is read by the copy engine after this returns; no
+        // earlier upload from it can still be pending (one onload per plan and
+        // ctx at a time: blocking ones complete, a prefetch is waited first)
+        std::memcpy(h.d->h_cks_want, h.slab->cks.data(), 8 * nck);
+        CK(cudaMemcpyAsync(h.d->cks_want, h.d->h_cks_want, 8 * nck, cudaMemcpyHostToDevice, pp.kern));
+    }
     CK(cudaMemsetAsync(pp.d_flag, 0, sizeof(int), pp.kern));
     use_grid(h, h.slab->elided);
     return PLEX_OK;
@@ -848,10 +887,18 @@ struct AsyncState {
     Pipe pp;
     plex_slab_s* slab = nullptr;
     cudaEvent_t done_k = nullptr, done_c = nullptr;
+    // A drain of an elision plan must read the derivability flag on the host
+    // before it can lay out its buckets; that wait (for the caller's prior work
+    // plus the check kernel) runs on this worker thread, not the caller's.
+    std::thread worker;
+    std::atomic<bool> enqueued{true};
+    plex_status enq_status = PLEX_OK;
+    std::string enq_error;
 };
 
 static void async_free(AsyncState* a) {
     if (!a) return;
+    if (a->worker.joinable()) a->worker.join();
     if (a->done_k) cudaEventDestroy(a->done_k);
     if (a->done_c) cudaEventDestroy(a->done_c);
     delete a;
@@ -956,6 +1003,8 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
         g_ctxs.erase(c);
     }
     DeviceGuard g(c->device);
+    for (auto& a : c->async)               // an enqueue worker must be done before the streams drain
+        if (a && a->worker.joinable()) a->worker.join();
     if (c->pack) cudaStreamSynchronize(c->pack);
     if (c->copy) cudaStreamSynchronize(c->copy);
     if (c->copy2) cudaStreamSynchronize(c->copy2);
@@ -1303,13 +1352,22 @@ static plex_status ckpt_check(plex_plan_t plan, plex_slab_t s, const char* path)
     return PLEX_OK;
 }
 
-plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
+// The slab becomes read-only (ckpt > 0) in the CALLER's thread, before any
+// background writer starts, under the slab mutex that restore also takes.
+static plex_status ckpt_begin(plex_plan_t plan, plex_slab_t s, const char* path) {
     plex_status st = ckpt_check(plan, s, path);
     if (st) return st;
+    std::lock_guard<std::mutex> lk(s->mu);
     if (s->residency != PLEX_RES_HOST || !s->host || !s->written) { set_error("checkpoint needs an offloaded (HOST) slab"); return PLEX_E_STATE; }
     if (s->elided) { set_error("slab holds derived (elided) params: offload without elision to checkpoint"); return PLEX_E_STATE; }
-    if (s->busy) { set_error("an async transfer of this slab is in flight"); return PLEX_E_STATE; }
+    if (s->busy) { set_error("an async transfer or a restore of this slab is in flight"); return PLEX_E_STATE; }
     s->ckpt.fetch_add(1);
+    return PLEX_OK;
+}
+
+// The write itself (slab already marked by ckpt_begin; unmarks it).
+static plex_status ckpt_write(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
+    plex_status st = PLEX_OK;
     const Plan& p = plan->p;
     const std::string h = ckpt_header(p, s->rank, s->cks);
     int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
@@ -1327,11 +1385,51 @@ plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* pa
     return st;
 }
 
+plex_status plex_slab_checkpoint(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
+    plex_status st = ckpt_begin(plan, s, path);
+    return st ? st : ckpt_write(plan, s, path, threads);
+}
+
+plex_status plex_slab_checkpoint_start(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads,
+                                       plex_ckpt_t* out) {
+    if (!out) { set_error("NULL out"); return PLEX_E_INVAL; }
+    *out = nullptr;
+    plex_status st = ckpt_begin(plan, s, path);
+    if (st) return st;
+    auto* h = new plex_ckpt_s();
+    const std::string pth(path);
+    try {
+        h->th = std::thread([h, plan, s, pth, threads]() {
+            h->status = ckpt_write(plan, s, pth.c_str(), threads);
+            if (h->status) h->error = plex_last_error();
+        });
+    } catch (...) {
+        s->ckpt.fetch_sub(1);
+        delete h;
+        set_error("cannot start the checkpoint thread");
+        return PLEX_E_INVAL;
+    }
+    *out = h;
+    return PLEX_OK;
+}
+
+plex_status plex_ckpt_wait(plex_ckpt_t h) {
+    if (!h) { set_error("NULL checkpoint handle"); return PLEX_E_INVAL; }
+    if (h->th.joinable()) h->th.join();
+    const plex_status st = h->status;
+    if (st) set_error("%s", h->error.c_str());
+    delete h;
+    return st;
+}
+
 plex_status plex_slab_restore(plex_plan_t plan, plex_slab_t s, const char* path, int32_t threads) {
     plex_status st = ckpt_check(plan, s, path);
     if (st) return st;
-    bool idle = false;
-    if (s->ckpt.load() || !s->busy.compare_exchange_strong(idle, true)) { set_error("slab is busy"); return PLEX_E_STATE; }
+    {
+        std::lock_guard<std::mutex> lk(s->mu);
+        if (s->ckpt.load() || s->busy.load()) { set_error("slab is busy (checkpoint, restore or async transfer)"); return PLEX_E_STATE; }
+        s->busy = true;
+    }
     const Plan& p = plan->p;
     const RankPlan& R = p.ranks[s->rank];
     int fd = open(path, O_RDONLY);
@@ -1430,6 +1528,7 @@ plex_status plex_state_offload(plex_ctx_t c, plex_plan_t plan, const void* const
     for (int32_t b = 0; b < h.nb; ++b)
         if ((st = off_bucket(c, pp, h, b))) return st;
     if ((st = carry_join(c, pp, h)) || (st = off_end(c, pp, h)) || (st = finish(c, caller))) return st;
+    off_collect(h);
     slab->cks.swap(h.cks);
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
@@ -1543,6 +1642,7 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
     CK(cudaStreamSynchronize(c->copy2));
     if ((st = finish(c, caller))) return st;
     if (do_off) {
+        off_collect(ho);
         slab_out->cks.swap(ho.cks);
         slab_out->residency = PLEX_RES_HOST;
         slab_out->written = true;
@@ -1685,6 +1785,7 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
     CK(cudaStreamWaitEvent(caller, c->ev_pack_done, 0));
     CK(cudaStreamSynchronize(c->copy2));
     if ((st = finish(c, caller))) return st;
+    off_collect(ho);
     slab->cks.swap(ho.cks);                    // the slab now holds A (checksums recorded by its pack)
     slab->residency = PLEX_RES_HOST;
     slab->written = true;
@@ -1762,14 +1863,37 @@ plex_status plex_state_drain(plex_ctx_t c, plex_plan_t plan, const void* const* 
         set_error("drain: stream ordering failed");
         return fail(PLEX_E_CUDA);
     }
-    if ((st = off_begin(c, a->pp, a->h))) return fail(st);
-    for (int32_t b = 0; b < a->h.nb; ++b)
-        if ((st = off_bucket(c, a->pp, a->h, b))) return fail(st);
-    if ((st = off_end(c, a->pp, a->h))) return fail(st);
-    if (cudaEventRecord(a->done_k, c->kasync) != cudaSuccess || cudaEventRecord(a->done_c, c->copy3) != cudaSuccess) {
-        (void)cudaGetLastError();
-        set_error("drain: event record failed");
-        return fail(PLEX_E_CUDA);
+    auto enqueue = [c, a]() -> plex_status {
+        plex_status s2;
+        if ((s2 = off_begin(c, a->pp, a->h))) return s2;
+        for (int32_t b = 0; b < a->h.nb; ++b)
+            if ((s2 = off_bucket(c, a->pp, a->h, b))) return s2;
+        if ((s2 = off_end(c, a->pp, a->h))) return s2;
+        if (cudaEventRecord(a->done_k, c->kasync) != cudaSuccess || cudaEventRecord(a->done_c, c->copy3) != cudaSuccess) {
+            (void)cudaGetLastError();
+            set_error("drain: event record failed");
+            return PLEX_E_CUDA;
+        }
+        return PLEX_OK;
+    };
+    if (plan->p.ranks[c->rank].elide_start) {
+        // NEXT-2 elision plan: the derivability check is read back on the host
+        // (off_begin) -- on a worker thread, so this call returns at once
+        a->enqueued = false;
+        const int dev = c->device;
+        try {
+            a->worker = std::thread([a, enqueue, dev]() {
+                cudaSetDevice(dev);
+                a->enq_status = enqueue();
+                if (a->enq_status) a->enq_error = plex_last_error();
+                a->enqueued = true;
+            });
+        } catch (...) {
+            set_error("drain: cannot start the enqueue thread");
+            return fail(PLEX_E_INVAL);
+        }
+    } else if ((st = enqueue())) {
+        return fail(st);
     }
     slab->busy = true;
     c->async[0] = a;
@@ -1835,6 +1959,7 @@ plex_status plex_state_poll(plex_ctx_t c, int32_t op, int32_t* done) {
     if (!c || !done || (op != PLEX_OP_OFFLOAD && op != PLEX_OP_ONLOAD)) { set_error("bad poll"); return PLEX_E_INVAL; }
     AsyncState* a = c->async[op == PLEX_OP_OFFLOAD ? 0 : 1];
     if (!a) { *done = 1; return PLEX_OK; }
+    if (!a->enqueued.load()) { *done = 0; return PLEX_OK; }   // events not recorded yet
     DeviceGuard g(c->device);
     const cudaError_t ek = cudaEventQuery(a->done_k), ec = cudaEventQuery(a->done_c);
     if ((ek != cudaSuccess && ek != cudaErrorNotReady) || (ec != cudaSuccess && ec != cudaErrorNotReady)) {
@@ -1855,6 +1980,15 @@ plex_status plex_state_wait(plex_ctx_t c, int32_t op, void* caller_stream) {
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(caller_stream);
     c->async[k] = nullptr;
     a->slab->busy = false;
+    if (a->worker.joinable()) a->worker.join();
+    if (a->enq_status) {
+        set_error("%s", a->enq_error.c_str());
+        const plex_status es = a->enq_status;
+        (void)cudaStreamSynchronize(c->kasync);            // nothing it enqueued is still running
+        (void)cudaStreamSynchronize(c->copy3);
+        async_free(a);
+        return es;
+    }
     cudaError_t e = cudaEventSynchronize(a->done_k);
     if (e == cudaSuccess) e = cudaEventSynchronize(a->done_c);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, a->done_k, 0);
@@ -1867,6 +2001,7 @@ plex_status plex_state_wait(plex_ctx_t c, int32_t op, void* caller_stream) {
     }
     plex_status st = PLEX_OK;
     if (k == 0) {
+        off_collect(a->h);
         a->slab->cks.swap(a->h.cks);
         a->slab->residency = PLEX_RES_HOST;
         a->slab->written = true;
@@ -2093,6 +2228,13 @@ plex_status plex_param_allgather(plex_ctx_t c, plex_plan_t plan, void* param_are
 // plex_weight_sync.
 static plex_status slab_master_ptrs(const Plan& p, plex_slab_t slab, std::vector<const void*>& src) {
     if (!slab || slab->plan_id != p.id) { set_error("slab does not belong to this plan"); return PLEX_E_INVAL; }
+    // carried buckets live in the carrier's carry region, not in this slab: any
+    // master rows there would be read as stale bytes
+    if (p.ranks[slab->rank].carried_out) {
+        set_error("sync from slab: %d of this rank's buckets are carried by other ranks (plan with link_weights)",
+                  p.ranks[slab->rank].carried_out);
+        return PLEX_E_INVAL;
+    }
     if (slab->residency != PLEX_RES_HOST || !slab->written || slab->busy) {
         set_error("sync from slab needs HOST-resident offloaded state (and no transfer in flight)");
         return PLEX_E_STATE;

@@ -285,24 +285,16 @@ class Slab:
 
     def checkpoint(self, path: str, threads: int = 8, background: bool = False):
         """NEXT-3: materialise the offloaded state as a safetensors checkpoint
-        (PAPER.md:510, :513).  background=True runs the host-only write on a
-        thread (the library call releases the GIL) and returns it; the slab is
-        busy until it finishes."""
+        (PAPER.md:510, :513).  background=True starts the host-only write on a
+        library-owned thread (plex_slab_checkpoint_start: the slab is marked
+        read-only before this returns) and returns a handle; ``handle.join()``
+        waits for it and fills ``handle.errors``."""
         if not background:
             check(lib.plex_slab_checkpoint(self.plan.h, self.h, path.encode(), threads))
             return None
-        import threading
-        err = []
-
-        def run():
-            code = lib.plex_slab_checkpoint(self.plan.h, self.h, path.encode(), threads)
-            if code != L.OK:
-                err.append(PlexError(code, lib.plex_last_error().decode(errors="replace")))
-
-        th = threading.Thread(target=run, daemon=True)
-        th.errors = err
-        th.start()
-        return th
+        h = C.c_void_p()
+        check(lib.plex_slab_checkpoint_start(self.plan.h, self.h, path.encode(), threads, C.byref(h)))
+        return CheckpointHandle(h, self)
 
     def restore(self, path: str, threads: int = 8) -> None:
         """Fill this slab from a checkpoint of the same plan/rank (residency HOST)."""
@@ -321,6 +313,23 @@ class Slab:
         buf = (C.c_uint64 * max(1, n))()
         check(lib.plex_slab_checksums(self.h, buf, n))
         return np.frombuffer(buf, dtype=np.uint64)[:n].reshape(-1, 2).copy()
+
+
+class CheckpointHandle:
+    """A background checkpoint (plex_slab_checkpoint_start); join() = plex_ckpt_wait."""
+
+    def __init__(self, h: C.c_void_p, slab: "Slab"):
+        self.h, self.slab, self.errors = h, slab, []
+
+    def join(self) -> None:
+        if self.h is not None and self.h.value:
+            code = lib.plex_ckpt_wait(self.h)
+            self.h = None
+            if code != L.OK:
+                self.errors.append(PlexError(code, lib.plex_last_error().decode(errors="replace")))
+
+    def __del__(self):
+        self.join()
 
 
 def bootstrap_nccl_id(rank: int) -> bytes:

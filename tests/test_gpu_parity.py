@@ -666,6 +666,52 @@ def test_sync_from_slab(model, W, tp, dp, ep, elide):
     assert e.value.code == L.E_STATE
 
 
+def test_sync_from_slab_refuses_carried_buckets():
+    """A rank whose buckets are carried by a peer (NEXT-1 link balancing) does
+    not hold its tail master rows in its own slab: sync-from-slab must refuse
+    instead of reading stale bytes (E_INVAL before any residency check)."""
+    man = manifest("mid")
+    plan = P.Plan(man, head_dim=MODELS["mid"].head_dim, world=2, tp=2, dp=1, bucket_bytes=1 << 14,
+                  tile_bytes=1024, link_weights=[1.0, 0.05])
+    assert plan.rank_info(1).carried_out > 0
+    m = mgr(2, 1, bucket=1 << 14)
+    slab = P.Slab(plan, 1)
+    arenas = [m.arena(plan, g) for g in range(2)]
+    with pytest.raises(P.PlexError) as e:
+        m.sync_rank_from_slab(plan, 1, slab, arenas)
+    assert e.value.code == L.E_INVAL and "carried" in str(e.value)
+    m.close()
+
+
+def test_background_checkpoint_marks_slab_before_returning(tmp_path):
+    """plex_slab_checkpoint_start: the slab is read-only from the moment the
+    call returns (swap into it / restore refused with E_STATE) until join();
+    onload from it proceeds meanwhile; afterwards the slab is writable again."""
+    man = manifest("mid")
+    plan = P.Plan(man, world=1, bucket_bytes=1 << 16, tile_bytes=4096)
+    m = mgr(1, 0, bucket=1 << 16)
+    sh = rank_shards(plan, 0, seed=23)
+    slab = P.Slab(plan, 0)
+    m.offload(plan, sh, slab)
+    want = slab.host_bytes().copy()
+    path = str(tmp_path / "bg.safetensors")
+    th = slab.checkpoint(path, threads=2, background=True)
+    with pytest.raises(P.PlexError) as e:
+        m.swap(plan, sh, slab)                        # would overwrite the slab being written out
+    assert e.value.code == L.E_STATE
+    with pytest.raises(P.PlexError) as e:
+        slab.restore(path)
+    assert e.value.code == L.E_STATE
+    m.onload(plan, slab, sh)                          # reading the slab is fine
+    th.join()
+    assert not th.errors
+    assert np.array_equal(slab.host_bytes(), want)
+    slab2 = P.Slab(plan, 0)
+    slab2.restore(path)                               # the file is complete and consistent
+    assert np.array_equal(slab2.host_bytes(), want)
+    m.close()
+
+
 # ---- NEXT-4 NVMe cold tier ----------------------------------------------------------------------
 def test_slab_nvme_tier(tmp_path):
     man = manifest("mid")

@@ -102,12 +102,39 @@ def test_tp_semantics_matmul(tp, model):
                 y = x @ _f64(out[t][p + "mlp.gate_up_proj.weight"]).T
                 assert np.array_equal(y[:, :half], (x @ Wg.T)[:, t * half:(t + 1) * half])
                 assert np.array_equal(y[:, half:], (x @ Wu.T)[:, t * half:(t + 1) * half])
+            # row parallel (down_proj, R3): each rank multiplies its slice of the
+            # intermediate activation (the columns its gate_up rows produced) by its
+            # column slice of down_proj; the partial products sum to x W_down^T.
+            # A dim-0 (row) split, a transposed slice or a wrong tp offset fails.
+            Wd = _f64(O.rne_bf16(full[(p + "mlp.down_proj.weight", 1)]))
+            hin = rng.standard_normal((3, Wd.shape[1]))
+            ref = hin @ Wd.T
+            c = Wd.shape[1] // tp
+            parts = []
+            for t in range(tp):
+                Wd_t = _f64(out[t][p + "mlp.down_proj.weight"])
+                assert Wd_t.shape == (Wd.shape[0], c)
+                parts.append(hin[:, t * c:(t + 1) * c] @ Wd_t.T)
+            assert np.allclose(sum(parts), ref, rtol=1e-12, atol=1e-12)
+            if tp > 1:   # every partial product differs from the full one: no rank holds it all
+                assert not any(np.allclose(pp, ref) for pp in parts)
     # vocab-parallel embedding lookup
     E = O.rne_bf16(full[("model.embed_tokens.weight", 1)])
     V = E.shape[0]
     for v in rng.integers(0, V, size=20):
         t = v // (V // tp)
         assert np.array_equal(out[t]["model.embed_tokens.weight"][v - t * (V // tp)], E[v])
+    # vocab-parallel lm_head (untied models): logits of rank t are the vocab
+    # rows [t*V/tp, (t+1)*V/tp) of h W_lm^T; concatenating them over tp (the
+    # all-gather a TP engine does) gives the full logits.
+    if "lm_head.weight" in man:
+        Wl = _f64(O.rne_bf16(full[("lm_head.weight", 1)]))
+        h = rng.standard_normal((3, Wl.shape[1]))
+        ref = h @ Wl.T
+        got = np.concatenate([h @ _f64(out[t]["lm_head.weight"]).T for t in range(tp)], axis=1)
+        assert np.array_equal(got, ref)
+        for t in range(tp):
+            assert out[t]["lm_head.weight"].shape == (V // tp, Wl.shape[1])
 
 
 @pytest.mark.parametrize("ep", [1, 2, 4])
