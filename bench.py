@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--no-balance", action="store_true", help="no NVLink-carried buckets (host-link balancing)")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default = steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-derived-variant", action="store_true",
+                    help="skip the labelled N=1 derived-param (elision) sub-measurement")
+    ap.add_argument("--cpu-ranks", type=int, default=8,
+                    help="simulated ranks of the per-rank CPU-oracle setting (0 = skip)")
     ap.add_argument("--cpu-sample-layers", type=int, default=2)
     ap.add_argument("--sync-nccl", action="store_true", help="NCCL send/recv sync transport (baseline)")
     ap.add_argument("--out", default="")
@@ -175,6 +179,107 @@ def cpu_oracle_sample(model: str, world: int, tp: int, ep: int, layers: int):
     return v, dt, sample
 
 
+def box_info() -> dict:
+    """The host the oracle runs on: lscpu model / sockets /
+    cores, the CPUs this process may use, host memory."""
+    out = {"affinity_cpus": len(os.sched_getaffinity(0)), "logical_cpus": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        want = {"Model name": "model", "Socket(s)": "sockets", "Core(s) per socket": "cores_per_socket",
+                "Thread(s) per core": "threads_per_core", "NUMA node(s)": "numa_nodes"}
+        for ln in txt.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in want:
+                v = v.strip()
+                out[want[k.strip()]] = int(v) if v.isdigit() else v
+        if "sockets" in out and "cores_per_socket" in out:
+            out["physical_cores"] = out["sockets"] * out["cores_per_socket"]
+    except Exception as e:                                  # lscpu missing: say so
+        out["lscpu"] = f"unavailable ({type(e).__name__})"
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal:"):
+                out["mem_total_gb"] = round(int(ln.split()[1]) * 1024 / 1e9, 1)
+    except OSError:
+        pass
+    return out
+
+
+def _max_rss_gb(who) -> float:
+    import resource
+    return round(resource.getrusage(who).ru_maxrss * 1024 / 1e9, 2)
+
+
+def _oracle_rank_worker(args):
+    """One simulated rank of the per-rank CPU setting (runs in its own process):
+    rank r's o4 pack + o5 parse of its FSDP-W shard of the sample, and o6/o7
+    gather -> RNE -> slice/fuse of its own rollout tensors (g = r).  Inputs are
+    generated before the common start barrier; the timed part is the oracle as it stands."""
+    model, W, tp, ep, layers, r, barrier = args
+    import numpy as np
+
+    from oracle import plex_oracle as O
+    from plexgen import gen_range, manifest
+    man = [(k, s) for k, s in manifest(model)
+           if any(k.startswith(f"model.layers.{l}.") for l in range(layers)) or k == "model.norm.weight"]
+    dp = W // tp
+    shards, ms = {}, {}
+    for k, s in man:
+        re_ = int(np.prod(s[1:])) if len(s) > 1 else 1
+        parts = []
+        for q in range(W):
+            a, b = O.fsdp_rows(s[0], W, q)
+            parts.append(gen_range(0, k, 1, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:])))
+        ms[k] = parts
+        a, b = O.fsdp_rows(s[0], W, r)
+        for kd in range(4):
+            shards[(k, kd)] = parts[r] if kd == 1 else \
+                gen_range(0, k, kd, a * re_, (b - a) * re_).reshape((b - a,) + tuple(s[1:]))
+    S = sum(x.nbytes for x in shards.values())
+    barrier.wait()                                           # every rank starts together
+    t0 = time.perf_counter()
+    segs, size = O.slab_layout(man, W, r)
+    slab = O.pack_slab(segs, size, shards)
+    O.parse_slab(slab, segs, dict(man))
+    from collections import OrderedDict
+    full = OrderedDict((k, O.rne_bf16(O.gather(v))) for k, v in ms.items())
+    O.rollout_tensors(full, tp, dp, ep, r)
+    dt = time.perf_counter() - t0
+    return S, dt, _max_rss_gb(0)
+
+
+def cpu_oracle_ranks(model: str, W: int, tp: int, ep: int, layers: int) -> dict:
+    """SURVEY §8(d) D5 second setting: one process per simulated rank (W cores),
+    all starting together; value = all ranks' state bytes / the slowest rank."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m, ctx.Pool(W) as pool:
+        bar = m.Barrier(W)
+        res = pool.map(_oracle_rank_worker, [(model, W, tp, ep, layers, r, bar) for r in range(W)], chunksize=1)
+    S = sum(r[0] for r in res)
+    dt = max(r[1] for r in res)
+    dp = W // tp
+    return {"value": round(S / dt / 1e9, 4), "unit": "GB/s", "cores": W, "kind": "oracle",
+            "sample": (f"{model} layers[0:{layers}]+norm, FSDP-{W} -> TP-{tp}xDP-{dp} (configs[1] layout), one "
+                       f"process per simulated rank: o4 pack + o5 parse of its shard ({S / W / 1e9:.3f} GB) + "
+                       f"o6/o7 gather-RNE-reshard of its own rollout tensors"),
+            "seconds_max_rank": round(dt, 2), "max_rss_gb_per_rank": max(r[2] for r in res)}
+
+
+def cpu_baseline(a, world: int, tp: int) -> dict:
+    """cpu_baseline of the bench line: the oracle, as it stands, on the box's host
+    cores -- single process (headline, as the reference arm) plus the per-rank setting."""
+    v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
+    out = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+           "seconds": round(dt, 2), "max_rss_gb": _max_rss_gb(0), "box": box_info()}
+    if a.cpu_ranks > 1:
+        try:
+            out["per_rank"] = cpu_oracle_ranks(a.model, a.cpu_ranks, min(2, a.cpu_ranks), a.ep, 1)
+        except Exception as e:                               # never lose the bench line over the baseline
+            out["per_rank"] = {"error": f"{type(e).__name__}: {e}"}
+    return out
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -198,7 +303,8 @@ def run_reference(a):
                                     f"rollout TP-{tp}xDP-{world // tp}; step = context switch + weight sync -- the "
                                     f"CPU oracle runs a bounded sample of it (see cpu_baseline.sample)"),
                        "model_shape": a.model, "impl_note": "CPU oracle (NumPy), no GPU"},
-            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "box": box_info()},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -369,12 +475,25 @@ def run_plex(a):
     two_jobs = mode != "single"
     duplex = mode in ("duplex", "swap")
     jobs = [job_a, job_b] if two_jobs else [job_a, job_a]
+    group = None
+    if two_jobs:
+        # the GPU group's residency authority (plex_group) decides and
+        # executes every switch: swap for jobs sharing one device copy, duplex when
+        # both fit, sequential under an HBM budget of one job (--no-duplex)
+        budget = None
+        if mode == "sequential":
+            budget = sum(v.numel() * v.element_size() for v in job_a.slab_shards().values())
+        group = P.Group(mgr, hbm_budget=budget)
+        shared = 0 if mode == "swap" else None
+        group.add(job_a, resident=True, storage=shared)
+        group.add(job_b, storage=shared)
     arena = mgr.arena(plan)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
     phase_ev = []
     cur = {"i": 0}
+    modes_seen = set()
 
     def step(record=False):
         """PAPER.md:555 transition: resident A -> incoming B = [OFFLOAD A, ONLOAD B], then SYNC B."""
@@ -383,16 +502,18 @@ def run_plex(a):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
         if ev:
             ev[0].record()
-        if mode == "swap":
-            out.swap_with(inc)
-        elif mode == "duplex":
-            out.switch_to(inc)
+        if group is not None:
+            res = group.transition(inc)                  # the library decides [OFFLOAD A, ONLOAD B] and runs it
+            modes_seen.add(res["mode"])
         else:
-            out.suspend(release=out is not inc)
+            out.suspend(release=False)
             inc.resume()
         if ev:
             ev[1].record()
-        inc.sync(arena)
+        if group is not None:
+            group.transition(inc, sync=arena)            # resident: [SYNC B]
+        else:
+            inc.sync(arena)
         if ev:
             ev[2].record()
             phase_ev.append(ev)
@@ -435,6 +556,94 @@ def run_plex(a):
         barrier()
         e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
         e2e = {"s": e2e_s, "h2d": info.slab_bytes, "d2h": info.slab_bytes + 16 * info.n_segments}
+
+    # ---- diagnostic (N>1, outside the timed region): the fused push split into its
+    # local (HBM-only) and remote (NVLink) items, timed as two launches so that each
+    # gets its own roofline fraction (PLEX_CTX_SPLIT_PUSH)
+    split = None
+    if world > 1 and not a.sync_nccl and two_jobs:
+        inc = jobs[cur["i"]]                            # the resident job after the last step
+        mgr.set_split_push(True)
+        for _ in range(2):
+            group.transition(inc, sync=arena)
+        mgr.reset_stats()
+        n_sp = max(3, min(a.steps, 10))
+        for _ in range(n_sp):
+            barrier()
+            group.transition(inc, sync=arena)
+        mgr.set_split_push(False)
+        sst = mgr.stats()
+        pk_hbm, pk_kind = load_peaks()
+        t_l = allmax(sst["push_local"]["ms"] / n_sp)
+        t_r = allmax(sst["push_remote"]["ms"] / n_sp)
+        nvb = allmax(float(max(info.send_bytes, info.recv_bytes)))
+        loc_gbs = (sst["push_local"]["bytes"] / n_sp) / (max(t_l, 1e-9) * 1e-3) / 1e9
+        rem_gbs = nvb / (max(t_r, 1e-9) * 1e-3) / 1e9
+        split = {"local": {"bound": "hbm", "achieved": round(loc_gbs, 1), "peak": pk_hbm, "unit": "GB/s",
+                           "frac": round(loc_gbs / pk_hbm, 4), "ms": round(t_l, 3),
+                           "note": "local push items alone (split launch, diagnostic after the timed region)"},
+                 "remote": {"bound": "nvlink", "achieved": round(rem_gbs, 1), "peak": 770.0, "unit": "GB/s",
+                            "frac": round(rem_gbs / 770.0, 4), "frac_of_nominal": round(rem_gbs / 900.0, 4),
+                            "bytes_max_rank": nvb, "ms": round(t_r, 3),
+                            "peak_kind": "measured peer copy 770 GB/s/dir (B200_PROFILING.md); nominal 900",
+                            "note": ("remote push items alone (split launch, diagnostic after the timed region): "
+                                     "max over ranks of max(send, recv) / max over ranks of the launch time")}}
+
+    # ---- labelled variant (N=1): the realistic post-optimizer-step state -------------
+    # param == RNE(master) (what a mixed-precision step leaves), so
+    # NEXT-2 elision derives the bf16 params on resume instead of moving them
+    # through the host link.  Same workload and step; the headline above keeps the
+    # conservative independent-param state (reading D2').
+    variant = None
+    if world == 1 and mode == "swap" and not a.no_derived_variant:
+        del group, jobs, job_a, job_b
+        group = job_a = job_b = jobs = None
+        torch.cuda.empty_cache()
+        plan_el = mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map,
+                           elide_param=True)
+        va = P.Job(mgr, plan_el, seed=1, slab=False).alloc()
+        vb = P.Job(mgr, plan_el, seed=2, hugepage=a.hugepage)
+        vb.shards = va.shards
+        vb.init_synthetic(derived_param=True)
+        vb.suspend(release=False)
+        vb.shards = type(va.shards)()
+        va.init_synthetic(derived_param=True)
+        vgroup = P.Group(mgr)
+        vgroup.add(va, resident=True, storage=0)
+        vgroup.add(vb, storage=0)
+        vjobs, vcur = [va, vb], {"i": 0}
+
+        def vstep():
+            inc = vjobs[1 - vcur["i"]]
+            vgroup.transition(inc)
+            vgroup.transition(inc, sync=arena)
+            vcur["i"] = 1 - vcur["i"]
+
+        vsteps, vwarm = max(1, min(a.steps, 10)), max(3, min(a.warmup, 3))
+        for _ in range(vwarm):
+            vstep()
+        mgr.reset_stats()
+        barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record()
+        for _ in range(vsteps):
+            vstep()
+        v1.record()
+        barrier()
+        vms = allmax(v0.elapsed_time(v1) / vsteps)
+        vst = mgr.stats()
+        vinfo = plan_el.rank_info(rank)
+        variant = {"label": "derived_param (param == RNE(master)): NEXT-2 elision active",
+                   "value": round(2 * vinfo.payload_bytes / (vms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                   "ms_per_step": round(vms, 2), "steps": vsteps, "warmup": vwarm,
+                   "elided": bool(vjobs[1 - vcur["i"]].slab.elided),     # the slab holder: the suspended job
+                   "host_link_bytes_per_step": int((vst["d2h"]["bytes"] + vst["h2d"]["bytes"]) / vsteps),
+                   "state_bytes_switched_per_step": int(2 * vinfo.payload_bytes),
+                   "derive_ms_per_step": round(vst["derive"]["ms"] / vsteps, 3),
+                   "note": ("value = state bytes switched (both jobs' full 4-kind state) / step time; the bf16 "
+                            "params (1/7 of the bytes) are re-derived on the device, not moved")}
+        del vgroup, vjobs, va, vb
+        torch.cuda.empty_cache()
 
     S_total = allsum(float(2 * info.payload_bytes))      # offloaded + onloaded state per switch
     value = S_total / (ms * 1e-3) / 1e9
@@ -479,18 +688,35 @@ def run_plex(a):
                                              + " (this rank)"),
                                "peak_one_direction": round(bw[k], 2)}
     if world > 1:
-        # NVLink: max over ranks of max(send, recv) bytes ÷ the data-moving part
-        # of the sync (the push kernel, or the NCCL exchange rounds), max over ranks
+        # The fused cast+push kernel moves local casts through HBM and remote ones
+        # over NVLink at once: its roofline is the slower of the two resources
+        # (B200_PROFILING.md: fused compute+collective kernels).  Per rank
+        # T_hbm = (fp32 read + local bf16 writes + incoming bf16 writes) / HBM peak,
+        # T_nvl = max(send, recv) / 770 GB/s measured peer copy; bound = max over
+        # ranks of max(T_hbm, T_nvl); frac = bound / measured push time (max over ranks).
         nv = allmax(float(max(info.send_bytes, info.recv_bytes)))
-        t_x = st["nccl"]["ms"] if st["nccl"]["launches"] else st["push"]["ms"]
-        t_x = allmax(t_x / a.steps)
-        gbs = nv / (t_x * 1e-3) / 1e9
-        rl["nvlink"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": 900.0, "unit": "GB/s",
-                        "frac": frac(gbs, 900.0), "frac_of_measured_peer_copy": frac(gbs, 770.0),
-                        "bytes_max_rank": nv, "ms": round(t_x, 3),
-                        "over": "NCCL exchange rounds" if st["nccl"]["launches"] else
-                                "fused cast+push kernel (local casts included)",
-                        "peak_kind": "nominal 900 GB/s/dir; measured peer copy 770 (B200_PROFILING.md)"}
+        hbm_b = float(info.src_read_bytes + info.local_bytes + info.recv_bytes)
+        t_hbm = allmax(hbm_b / (peak_hbm * 1e9) * 1e3)
+        t_nvl = allmax(float(max(info.send_bytes, info.recv_bytes)) / 770e9 * 1e3)
+        if not st["nccl"]["launches"]:
+            t_push = allmax(st["push"]["ms"] / a.steps)
+            bound = "nvlink" if t_nvl >= t_hbm else "hbm"
+            rl["push_fused"] = {"bound": bound, "lower_bound_ms": round(max(t_hbm, t_nvl), 3),
+                                "t_hbm_ms": round(t_hbm, 3), "t_nvlink_ms": round(t_nvl, 3),
+                                "achieved_ms": round(t_push, 3), "frac": frac(max(t_hbm, t_nvl), t_push),
+                                "nvlink_bytes_max_rank": nv, "hbm_bytes_this_rank": hbm_b,
+                                "peak_kind": f"HBM {peak_hbm} GB/s ({peak_kind}); NVLink 770 GB/s measured peer copy "
+                                             "(900 nominal)"}
+        else:
+            t_x = allmax(st["nccl"]["ms"] / a.steps)
+            gbs = nv / (t_x * 1e-3) / 1e9
+            rl["nvlink"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": 770.0, "unit": "GB/s",
+                            "frac": frac(gbs, 770.0), "frac_of_nominal": frac(gbs, 900.0),
+                            "bytes_max_rank": nv, "ms": round(t_x, 3), "over": "NCCL exchange rounds",
+                            "peak_kind": "measured peer copy 770 GB/s/dir (B200_PROFILING.md); nominal 900"}
+        if split is not None:
+            rl["push_local"] = split["local"]
+            rl["nvlink"] = split["remote"]
 
         if st["nccl"]["launches"]:
             rl["nccl_exchange"] = {"ms_per_step": round(st["nccl"]["ms"] / a.steps, 3),
@@ -522,6 +748,8 @@ def run_plex(a):
                        "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
                        "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
                        "sync_transport": "nccl" if a.sync_nccl else "nvlink-push",
+                       "executor": ("plex_group_transition (library residency map decides every switch; modes "
+                                    f"seen: {sorted(modes_seen)})") if group is not None else "direct calls",
                        "rank_map": ["tp_fast (g = dp*TP + tp)", "dp_fast (g = tp*DP + dp)"][plan.stats().rank_map]},
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
                          "unit": "GB/s", "frac": frac(achieved, peak_hbm), "traffic": traffic,
@@ -537,21 +765,24 @@ def run_plex(a):
             line["e2e"] = {"value": round(S_total / e2e["s"] / 1e9, 3), "unit": "GB/s",
                            "ms_per_step": round(e2e["s"] * 1e3, 2), "h2d_bytes_per_step": e2e["h2d"],
                            "d2h_bytes_per_step": e2e["d2h"],
-                           "api": {"swap": "Job.swap_with (in place) -> Job.sync (host clock)",
-                                   "duplex": "Job.switch_to with storage release/acquire -> Job.sync (host clock)",
-                                   "sequential": "Job.suspend + Job.resume with storage release/acquire -> Job.sync "
+                           "api": {"swap": "Group.transition(B) (in-place swap) -> Group.transition(B, sync=arena) "
+                                           "(host clock)",
+                                   "duplex": "Group.transition(B) (duplex, storage release/acquire) -> "
+                                             "Group.transition(B, sync=arena) (host clock)",
+                                   "sequential": "Group.transition(B) (sequential under a one-job HBM budget, "
+                                                 "storage release/acquire) -> Group.transition(B, sync=arena) "
                                                  "(host clock)",
                                    "single": "Job.suspend + Job.resume -> Job.sync (host clock)"}[mode]}
+        if variant is not None:
+            line["derived_param"] = variant
         if not a.no_cpu_baseline and world == 1:
-            v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
-            line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                                    "sample": sample, "seconds": round(dt, 2)}
+            line["cpu_baseline"] = cpu_baseline(a, world, tp)
         print(json.dumps(line), flush=True)
         if a.out:
             with open(a.out, "w") as f:
                 json.dump(line, f, indent=1)
     barrier()
-    del jobs, job_a, job_b, arena
+    del jobs, job_a, job_b, arena, group
     mgr.close()
     if world > 1:
         dist.destroy_process_group()

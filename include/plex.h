@@ -69,6 +69,8 @@ typedef int plex_status;
 #define PLEX_ROLE_COL         1   /* dim-0 split by TP; pieces of one group fused  */
 #define PLEX_ROLE_ROW         2   /* dim-1 split by TP                             */
 #define PLEX_ROLE_EXPERT      3   /* whole tensor on EP rank floor(e / (E/EP))     */
+#define PLEX_ROLE_AUTO       -1   /* the planner classifies the tensor from its key (R3):
+                                     group / slot / expert / unit are then ignored   */
 
 #define PLEX_SLAB_KIND_MAJOR  0   /* R4: for kind: for key   (default)  */
 #define PLEX_SLAB_KEY_MAJOR   1   /* R4: for key: for kind   (per-expert units) */
@@ -96,6 +98,10 @@ typedef int plex_status;
                                     peer-memory transport (baseline) */
 #define PLEX_CTX_SYNC_NCCL 0x2u  /* weight sync via K4 pack + NCCL send/recv + K5
                                     unpack instead of the fused NVLink push     */
+#define PLEX_CTX_SPLIT_PUSH 0x8u /* diagnostic: the fused push runs as two launches, the
+                                    local (HBM-only) items then the remote (NVLink)
+                                    items, timed separately (PLEX_STAT_PUSH_LOCAL /
+                                    _REMOTE) so each gets its own roofline fraction */
 
 /* Slab flags. */
 #define PLEX_SLAB_HUGEPAGE 0x1u  /* mmap + MADV_HUGEPAGE + cudaHostRegister      */
@@ -107,7 +113,26 @@ typedef struct plex_ckpt_s* plex_ckpt_t;     /* a background checkpoint */
 
 /* One logical (unsharded) tensor of the job's manifest, in canonical order
  * (R4).  2-D view [d0, d1]; 1-D tensors have d1 = 1, ndim = 1.
- *   role   : PLEX_ROLE_*.
+ *   role   : PLEX_ROLE_*, or PLEX_ROLE_AUTO for every tensor of the manifest:
+ *            the planner then derives role, group, slot, expert and unit from
+ *            the Hugging Face / Qwen parameter key alone (reading R3,
+ *            PAPER.md:576 "target parallel layout"):
+ *              *embed_tokens.weight, lm_head.weight        COL (vocab-parallel)
+ *              model.layers.N.self_attn.{q,k,v}_proj.{weight,bias}
+ *                                                          COL, fused into
+ *                   "model.layers.N.self_attn.qkv_proj.{weight,bias}" (slots q,k,v;
+ *                   unit = plex_plan_req.head_dim)
+ *              model.layers.N.self_attn.o_proj.weight      ROW
+ *              model.layers.N.mlp.{gate,up}_proj.weight    COL, fused into
+ *                   "model.layers.N.mlp.gate_up_proj.weight" (slots gate, up)
+ *              model.layers.N.mlp.down_proj.weight         ROW
+ *              model.layers.N.mlp.experts.E.{gate,up}_proj.weight
+ *                   EXPERT E, stacked into "model.layers.N.mlp.experts.w13_weight"
+ *              model.layers.N.mlp.experts.E.down_proj.weight
+ *                   EXPERT E, stacked into "model.layers.N.mlp.experts.w2_weight"
+ *              anything else (norms, q_norm/k_norm, router)  REPLICATED
+ *            Group ids follow first appearance; plex_plan_group_name names
+ *            them.  Mixing AUTO and explicit roles is E_INVAL.
  *   group  : destination tensor id; tensors sharing a group are fused into
  *            one rollout tensor, pieces concatenated along dim 0 in `slot`
  *            order (qkv = q|k|v, gate_up = gate|up, w13 = gate_e|up_e ...).
@@ -153,6 +178,9 @@ typedef struct {
      * longer than the group average hand whole buckets over NVLink to ranks
      * with spare host bandwidth, which keep them in a pinned carry region. */
     const float* link_weights;
+    /* PLEX_ROLE_AUTO manifests: rows per attention head (q/k/v split unit);
+     * 0 = 1 (no head-granularity check). */
+    int32_t head_dim;
 } plex_plan_req;
 
 /* Plan flags. */
@@ -260,11 +288,38 @@ typedef struct {
 #define PLEX_STAT_DERIVE  8      /* NEXT-2 param check / re-derivation */
 #define PLEX_STAT_BARRIER 9      /* sync entry barrier (time spent waiting for the slowest rank) */
 #define PLEX_STAT_GATHER  10     /* NEXT-2 replicated-param all-gather push */
-#define PLEX_NUM_STATS    11
+#define PLEX_STAT_PUSH_LOCAL  11 /* PLEX_CTX_SPLIT_PUSH: local items (bytes: 4 read + 2 written per element) */
+#define PLEX_STAT_PUSH_REMOTE 12 /* PLEX_CTX_SPLIT_PUSH: remote items (bytes: 2 sent over NVLink per element) */
+#define PLEX_NUM_STATS    13
+
+/* a1 transition decision and what the group executor did. */
+#define PLEX_SWITCH_NONE        0   /* incoming job already resident: no transfer      */
+#define PLEX_SWITCH_LOAD        1   /* nothing resident: onload only                   */
+#define PLEX_SWITCH_SWAP        2   /* in-place plex_state_swap (shared device storage) */
+#define PLEX_SWITCH_DUPLEX      3   /* plex_state_switch: offload || onload            */
+#define PLEX_SWITCH_SEQUENTIAL  4   /* offload, release, acquire, onload               */
+
+typedef struct {
+    int32_t n_ops;               /* op list of PAPER.md:555 (PLEX_OP_*)          */
+    int32_t ops[4];
+    int64_t op_jobs[4];
+    int32_t mode;                /* PLEX_SWITCH_* (plex_group_transition only)    */
+    int64_t resident_before;     /* -1 = no job resident on the group             */
+    int64_t resident_after;
+} plex_transition;
 
 /* ---- errors / version ---------------------------------------------------- */
 PLEX_API const char* plex_last_error(void);
 PLEX_API const char* plex_version(void);
+
+/* ---- a1: transition decision (pure host) ----------------------------------- */
+/* PAPER.md:555 (_handle_job_transition): if the incoming operation's job
+ * differs from the job resident on the GPU group, prepend OFFLOAD(resident)
+ * (when one is resident, i.e. resident >= 0) and ONLOAD(incoming); op ==
+ * PLEX_OP_SYNC appends SYNC(incoming).  resident == incoming gives no
+ * transfer.  Fills n_ops/ops/op_jobs and resident_before/after (mode = NONE).
+ * plex_transition_plan and plex_group_transition use this same decision. */
+PLEX_API plex_status plex_transition_decide(int64_t resident, int64_t incoming, int32_t op, plex_transition* out);
 
 /* ---- a1 + a2: transition decision and plan (pure host, no CUDA calls) ----- */
 /* Deterministic: identical requests give identical plans on every rank.
@@ -275,6 +330,13 @@ PLEX_API plex_status plex_plan_query(plex_plan_t plan, plex_plan_stats* out);
 PLEX_API plex_status plex_plan_rank_info(plex_plan_t plan, int32_t rank, plex_rank_info* out);
 PLEX_API plex_status plex_plan_segment(plex_plan_t plan, int32_t rank, int32_t i, plex_seg_desc* out);
 PLEX_API plex_status plex_plan_dst_tensor(plex_plan_t plan, int32_t rank, int32_t i, plex_dst_desc* out);
+/* Name of destination group `group` (PLEX_ROLE_AUTO plans: the fused rollout
+ * tensor name, e.g. "model.layers.0.self_attn.qkv_proj.weight"; explicit-role
+ * plans: the key of the group's first tensor).  Copies at most cap-1 bytes +
+ * NUL into buf; *len = full length.  Also: *role / *n_experts of the group
+ * (n_experts = experts stacked in an EXPERT group, else 0); any out may be NULL. */
+PLEX_API plex_status plex_plan_group(plex_plan_t plan, int32_t group, char* buf, int32_t cap, int32_t* len,
+                                     int32_t* role, int32_t* n_experts);
 /* FSDP rows [row0, row1) of tensor t held by `rank` (R2; empty when row0 == row1). */
 PLEX_API plex_status plex_plan_shard_rows(plex_plan_t plan, int32_t rank, int32_t t, int64_t* row0, int64_t* row1);
 /* i-th carried bucket of the plan (0 <= i < plex_plan_n_carry). */
@@ -308,6 +370,9 @@ PLEX_API plex_status plex_ctx_destroy(plex_ctx_t ctx);
  * plan). */
 PLEX_API plex_status plex_ctx_set_carry_staging(plex_ctx_t ctx, void* staging, uint64_t bytes);
 PLEX_API plex_status plex_ctx_stats(plex_ctx_t ctx, int32_t which, plex_kernel_stats* out);
+/* flags = (flags & ~mask) | (value & mask); only PLEX_CTX_TIMING and
+ * PLEX_CTX_SPLIT_PUSH may change after creation (E_INVAL otherwise). */
+PLEX_API plex_status plex_ctx_set_flags(plex_ctx_t ctx, uint32_t value, uint32_t mask);
 PLEX_API plex_status plex_ctx_reset_stats(plex_ctx_t ctx);
 /* Per-launch records behind plex_ctx_stats (PLEX_CTX_TIMING), oldest first,
  * since the last reset; *n = how many exist (copies min(cap, *n)). */
@@ -434,6 +499,71 @@ PLEX_API plex_status plex_weight_sync(plex_ctx_t ctx, plex_plan_t plan, const vo
  * and by plex_weight_sync itself.  Ordered on stream, blocking. */
 PLEX_API plex_status plex_weight_sync_rank(plex_ctx_t ctx, plex_plan_t plan, int32_t rank, const void* const* src_master,
                                   int32_t n_src, void* const* dst_arenas, int32_t n_arenas, void* stream);
+
+/* ---- a1 executed: the GPU group's residency authority ---------------------- */
+/* PAPER.md:555 ("the scheduler maintains a map (group_executor_gpu_job)
+ * tracking the Job ID currently resident on each GPU group ... If they differ,
+ * the system automatically prepends offload and load operations") and :506
+ * (StateManager, the "single node-local authority over residency").  A group
+ * lives on one ctx (this rank's GPU of the group); every rank of the group
+ * keeps its own group object and calls the same transitions in the same order.
+ *
+ * Storage (a5): the library never allocates device memory.  `storage` is
+ * called to (re)acquire a job's device state before an onload (acquire = 1:
+ * allocate and write the PLEX_NUM_KINDS x n_tensors pointer table into
+ * `state`, same layout as plex_state_offload's src) and to release it after an
+ * offload (acquire = 0).  It returns 0 on success, nonzero when the memory
+ * cannot be acquired (then the executor switches sequentially: offload and
+ * release the resident job first).  NULL storage = device state is never
+ * released (pointer tables given at plex_group_add_job stay valid). */
+typedef struct plex_group_s* plex_group_t;
+typedef int32_t (*plex_storage_fn)(void* user, int64_t job, int32_t acquire, void** state, int32_t n_state);
+
+PLEX_API plex_status plex_group_create(plex_ctx_t ctx, plex_storage_fn storage, void* user, plex_group_t* out);
+PLEX_API plex_status plex_group_destroy(plex_group_t group);
+
+/* Register job `job` (>= 0, unique) with its plan and pinned slab (NULL only
+ * for a swap partner that never leaves the device alone: see storage_id).
+ *   flags & PLEX_GROUP_RESIDENT: the job's state is on the device now (state =
+ *     its pointer table; at most one resident job per group, R17); else the
+ *     job is HOST-resident: slab must hold its offloaded state.
+ *   state / n_state: pointer table of already-allocated device storage (or
+ *     NULL: acquired through `storage` at its first onload).
+ *   storage_id >= 0: jobs with equal ids share ONE set of device tensors
+ *     (same plan required); switches between them are in-place swaps
+ *     (plex_state_swap) and the pair's slab moves with the state.  -1 = own
+ *     storage.
+ * Errors: E_INVAL (duplicate id, plan of another world, bad table, replica
+ * plans on a ctx without NCCL), E_STATE (second resident job, HOST job whose
+ * slab holds no state). */
+#define PLEX_GROUP_RESIDENT 0x1u
+PLEX_API plex_status plex_group_add_job(plex_group_t group, int64_t job, plex_plan_t plan, plex_slab_t slab,
+                                        int64_t storage_id, uint32_t flags, void* const* state, int32_t n_state);
+/* *job = the job resident on the group (-1 = none). */
+PLEX_API plex_status plex_group_resident(plex_group_t group, int64_t* job);
+/* The slab currently holding `job`'s offloaded state (swaps move slabs). */
+PLEX_API plex_status plex_group_job_slab(plex_group_t group, int64_t job, plex_slab_t* slab);
+
+/* Run operation `op` (PLEX_OP_NONE, or PLEX_OP_SYNC for a weight sync) of job
+ * `incoming` on the group: decides the ops with plex_transition_decide, then
+ * executes them, choosing per switch
+ *   SWAP        the two jobs share device storage (plex_state_swap);
+ *   DUPLEX      the incoming job's storage can be acquired while the resident
+ *               one is still on the device and staging holds both rings
+ *               (plex_state_switch; then the outgoing storage is released);
+ *   SEQUENTIAL  otherwise (offload, release, acquire, onload).
+ * Replicated-param plans (PLEX_PLAN_REPLICA_PARAM) are all-gathered after
+ * their onload.  SYNC: n_arenas == 1 -> collective plex_weight_sync into
+ * dst_arenas[0]; n_arenas == world -> this rank's share into every given
+ * arena (plex_weight_sync_rank, single-process emulation).  Blocking,
+ * ordered after prior work on caller_stream.  *out (may be NULL) reports the
+ * ops, the mode and the residency.  On error the group's map follows the
+ * slabs (a failed onload leaves no job resident; E_CHECKSUM keeps the
+ * outgoing state safe in its slab).  Plans with carried buckets must not fail
+ * to acquire storage (E_TIER_FULL instead of a per-rank fallback, so that
+ * every rank takes the same collective path). */
+PLEX_API plex_status plex_group_transition(plex_group_t group, int64_t incoming, int32_t op, void* const* dst_arenas,
+                                           int32_t n_arenas, void* caller_stream, plex_transition* out);
 
 /* ---- NEXT-3: checkpoint materialisation from the offloaded state ---------- */
 /* a checkpoint is a materialisation of managed (possibly

@@ -8,8 +8,8 @@ is missing: there is no CPU fallback.
 """
 from . import _lib  # noqa: F401  (loads libplex.so or raises ImportError)
 from ._lib import PlexError  # noqa: F401
-from .state import (Job, Plan, Slab, StateManager, cast_rne, checksum, describe,  # noqa: F401
-                    synth_fill, synth_mutate)
+from .state import (Group, Job, Plan, Slab, StateManager, cast_rne, checksum, synth_fill,  # noqa: F401
+                    synth_mutate, transition_decide)
 
-__all__ = ["Job", "Plan", "Slab", "StateManager", "PlexError", "describe", "synth_fill", "synth_mutate",
-           "checksum", "cast_rne"]
+__all__ = ["Group", "Job", "Plan", "Slab", "StateManager", "PlexError", "synth_fill", "synth_mutate",
+           "checksum", "cast_rne", "transition_decide"]

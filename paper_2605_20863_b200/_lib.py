@@ -16,26 +16,30 @@ OK, E_INVAL, E_LAYOUT, E_TIER_FULL, E_STATE, E_CUDA, E_NCCL, E_CHECKSUM = 0, -1,
 KIND_PARAM, KIND_MASTER, KIND_EXP_AVG, KIND_EXP_AVG_SQ = 0, 1, 2, 3
 NUM_KINDS = 4
 KINDMASK_ALL, KINDMASK_OPTIM = 0xF, 0xE
-ROLE_REPLICATED, ROLE_COL, ROLE_ROW, ROLE_EXPERT = 0, 1, 2, 3
+ROLE_REPLICATED, ROLE_COL, ROLE_ROW, ROLE_EXPERT, ROLE_AUTO = 0, 1, 2, 3, -1
 SLAB_KIND_MAJOR, SLAB_KEY_MAJOR = 0, 1
 RANKMAP_TP_FAST, RANKMAP_DP_FAST, RANKMAP_AUTO = 0, 1, 2
 OP_NONE, OP_OFFLOAD, OP_ONLOAD, OP_SYNC = 0, 1, 2, 3
 RES_DEVICE, RES_HOST, RES_DISK = 0, 1, 2
-CTX_TIMING, CTX_SYNC_NCCL, CTX_CARRY_NCCL = 0x1, 0x2, 0x4
+CTX_TIMING, CTX_SYNC_NCCL, CTX_CARRY_NCCL, CTX_SPLIT_PUSH = 0x1, 0x2, 0x4, 0x8
 SLAB_HUGEPAGE = 0x1
 STAT_PACK, STAT_UNPACK, STAT_PUSH, STAT_D2H, STAT_H2D, STAT_NCCL, STAT_RPACK, STAT_RUNPACK, STAT_DERIVE, \
-    STAT_BARRIER, STAT_GATHER = range(11)
-STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive", "barrier", "gather")
-NUM_STATS = 11
+    STAT_BARRIER, STAT_GATHER, STAT_PUSH_LOCAL, STAT_PUSH_REMOTE = range(13)
+STAT_NAMES = ("pack", "unpack", "push", "d2h", "h2d", "nccl", "rpack", "runpack", "derive", "barrier", "gather",
+              "push_local", "push_remote")
+NUM_STATS = 13
 PLAN_ELIDE_PARAM = 0x1
 PLAN_REPLICA_PARAM = 0x2
+SWITCH_NONE, SWITCH_LOAD, SWITCH_SWAP, SWITCH_DUPLEX, SWITCH_SEQUENTIAL = 0, 1, 2, 3, 4
+SWITCH_NAMES = ("none", "load", "swap", "duplex", "sequential")
+GROUP_RESIDENT = 0x1
 
 EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_plan_n_carry", "plex_plan_carry", "plex_ctx_set_carry_staging", "plex_slab_carry",
     "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
-    "plex_ctx_trace",
+    "plex_ctx_trace", "plex_ctx_set_flags",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_slab_spill", "plex_slab_fill",
     "plex_state_offload", "plex_state_onload", "plex_state_switch", "plex_weight_sync",
@@ -44,6 +48,8 @@ EXPORTS = [
     "plex_plan_param_arena", "plex_param_allgather", "plex_param_allgather_rank",
     "plex_slab_checkpoint", "plex_slab_checkpoint_start", "plex_ckpt_wait", "plex_slab_restore", "plex_state_swap",
     "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
+    "plex_transition_decide", "plex_plan_group", "plex_group_create", "plex_group_destroy", "plex_group_add_job",
+    "plex_group_resident", "plex_group_job_slab", "plex_group_transition",
 ]
 
 
@@ -65,7 +71,7 @@ class PlanReq(C.Structure):
                 ("slab_layout", C.c_int32), ("kind_mask", C.c_uint32), ("n_subset", C.c_int32),
                 ("subset", C.POINTER(C.c_int32)), ("bucket_bytes", C.c_uint64), ("tile_bytes", C.c_uint64),
                 ("resident_job", C.c_int64), ("incoming_job", C.c_int64), ("op", C.c_int32), ("flags", C.c_uint32),
-                ("link_weights", C.POINTER(C.c_float))]
+                ("link_weights", C.POINTER(C.c_float)), ("head_dim", C.c_int32)]
 
 
 class PlanStats(C.Structure):
@@ -104,6 +110,14 @@ class LaunchRecord(C.Structure):
                 ("call", C.c_int32)]
 
 
+class Transition(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("ops", C.c_int32 * 4), ("op_jobs", C.c_int64 * 4), ("mode", C.c_int32),
+                ("resident_before", C.c_int64), ("resident_after", C.c_int64)]
+
+
+STORAGE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_void_p), C.c_int32)
+
+
 class KernelStats(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("total_ms", C.c_double), ("bytes", C.c_uint64)]
 
@@ -133,6 +147,7 @@ def _load() -> C.CDLL:
         "plex_ctx_destroy": (C.c_int, [VP]),
         "plex_ctx_stats": (C.c_int, [VP, I32, P(KernelStats)]),
         "plex_ctx_reset_stats": (C.c_int, [VP]),
+        "plex_ctx_set_flags": (C.c_int, [VP, U32, U32]),
         "plex_ctx_trace": (C.c_int, [VP, P(LaunchRecord), I32, P(I32)]),
         "plex_slab_create": (C.c_int, [VP, I32, U32, P(VP)]),
         "plex_slab_destroy": (C.c_int, [VP]),
@@ -164,6 +179,14 @@ def _load() -> C.CDLL:
         "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
         "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),
         "plex_cast_rne": (C.c_int, [VP, VP, U64, VP]),
+        "plex_transition_decide": (C.c_int, [I64, I64, I32, P(Transition)]),
+        "plex_plan_group": (C.c_int, [VP, I32, C.c_char_p, I32, P(I32), P(I32), P(I32)]),
+        "plex_group_create": (C.c_int, [VP, STORAGE_FN, VP, P(VP)]),
+        "plex_group_destroy": (C.c_int, [VP]),
+        "plex_group_add_job": (C.c_int, [VP, I64, VP, VP, I64, U32, P(VP), I32]),
+        "plex_group_resident": (C.c_int, [VP, P(I64)]),
+        "plex_group_job_slab": (C.c_int, [VP, I64, P(VP)]),
+        "plex_group_transition": (C.c_int, [VP, I64, I32, P(VP), I32, VP, P(Transition)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

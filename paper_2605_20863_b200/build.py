@@ -12,7 +12,7 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libplex.so")
-SOURCES = ["plex_plan.cpp", "plex_kernels.cu", "plex_runtime.cu"]
+SOURCES = ["plex_plan.cpp", "plex_group.cpp", "plex_kernels.cu", "plex_runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -121,7 +121,21 @@ struct Plan {
     uint64_t param_arena_bytes = 0;
     plex_plan_stats stats{};
     uint64_t id = 0;                            // unique per plan (device cache key)
+    // destination groups (index = group id): name, role, experts stacked (EXPERT)
+    std::vector<std::string> group_names;
+    std::vector<int32_t> group_role, group_experts;
 };
+
+// What the group executor needs to know about a ctx (plex_runtime.cu).
+struct CtxInfo {
+    uint64_t staging_bytes;
+    int32_t n_slots, rank, world, device;
+    bool has_comm;
+};
+void ctx_query(plex_ctx_t c, CtxInfo* out);
+
+// a1: the op list of one transition.
+void transition_ops(int64_t resident, int64_t incoming, int32_t op, plex_transition* out);
 
 inline int32_t n_buckets(const Plan& p, const RankPlan& r) {
     return (int32_t)((r.slab_bytes + p.bucket - 1) / p.bucket);

@@ -12,7 +12,8 @@
 //    bucket; the checksum is folded from shared memory.
 //  * push / cast / derive: one 256-thread CTA per planner work item, 16-B
 //    vectorised streaming loads (ld.global.nc.L1::no_allocate) and stores;
-//    the push kernel's stores go to peer-mapped arenas over NVLink.
+//    the push kernel's stores go to peer-mapped arenas over NVLink; strided
+//    (row-parallel) rectangles use a 2-D warp-per-row mapping.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -86,15 +87,18 @@ __device__ __forceinline__ void block_reduce_add(Cks c, unsigned long long* out)
 }
 
 // ---- K1 / K2: pack (tensor -> staging) or unpack (staging -> tensor) -------
-// Persistent, one CTA per SM, TMA bulk-copy pipeline (cp.async.bulk, SASS
-// UBLKCP): warp 4 lane 0 streams 32 KiB chunks global->shared into a 6-stage
-// ring (mbarrier complete_tx); consumer warps 0-3 fold the R14 checksum from
-// shared memory while consumer thread 0 streams the same stage back out
-// shared->global (bulk_group).  Each stage is released once the bulk store has
-// read it.  Byte ranges that TMA cannot move (a tensor not 16-B aligned, or
-// the <16-B tail of a segment) go through the consumer threads directly;
-// padding bytes of a slot are written as zeros on pack and skipped on unpack.
-// Work: the bucket's PackItems (slot byte ranges <= 64 KiB), strided over CTAs.
+// Persistent, PackCfg = TmaCfg<3, 32, 4, 2>: two CTAs per SM, each a TMA
+// bulk-copy pipeline (cp.async.bulk, SASS UBLKCP) with a 3-stage ring of
+// 32 KiB chunks.  The producer warp (warp 4, lane 0) claims PackItems from a
+// per-launch counter (dynamic balancing, see below) and streams their chunks
+// global->shared (mbarrier complete_tx); consumer warps 0-3 fold the R14
+// checksum from shared memory while consumer thread 0 streams the same stage
+// back out shared->global (bulk_group).  A stage is released once every
+// consumer warp and the bulk store have read it.  Byte ranges that TMA cannot
+// move (a tensor not 16-B aligned, or the <16-B tail of a segment) go through
+// the consumer threads directly; padding bytes of a slot are written as zeros
+// on pack and skipped on unpack.  Work: the bucket's PackItems (slot byte
+// ranges <= 64 KiB).
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -380,8 +384,8 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
     };
     if (vec) {
         const uint32_t vpr = cols / 8;
-        const uint32_t total = rows * vpr;
         if (rows == 1) {
+            const uint32_t total = vpr;
             uint32_t v = threadIdx.x;
             for (; v + kThreads < total; v += 2 * kThreads) {
                 const uint4 x0 = load8(8ull * v);
@@ -391,9 +395,29 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
             }
             for (; v < total; v += kThreads) st_v4(dst + 8ull * v, load8(8ull * v));
         } else {
-            for (uint32_t v = threadIdx.x; v < total; v += kThreads) {
-                const uint32_t r = v / vpr, c = v - r * vpr;
-                st_v4(dst + (uint64_t)r * ds + 8 * c, load8((uint64_t)r * ss + 8 * c));
+            // Strided rectangle (row-parallel o_proj / down_proj slices, fused-group
+            // pieces): a 2-D warp mapping, no per-vector index division.  wpr warps
+            // share one row (lanes stride its 16-B vectors, coalesced on both
+            // sides); rows_in_flight rows are processed at once, the CTA strides
+            // over the rest.  The one division is per thread, not per vector.
+            constexpr uint32_t kWarps = kThreads / 32;
+            const uint32_t wpr = rows >= kWarps ? 1u : kWarps / rows;
+            const uint32_t rif = kWarps / wpr;
+            const uint32_t w = threadIdx.x >> 5;
+            const uint32_t r0 = w / wpr;
+            const uint32_t c0 = (w - r0 * wpr) * 32 + (threadIdx.x & 31), cs = wpr * 32;
+            if (r0 < rif) {
+                for (uint32_t r = r0; r < rows; r += rif) {
+                    const uint64_t so = (uint64_t)r * ss, dof = (uint64_t)r * ds;
+                    uint32_t c = c0;
+                    for (; c + cs < vpr; c += 2 * cs) {                 // two 32-B fp32 loads in flight
+                        const uint4 x0 = load8(so + 8 * c);
+                        const uint4 x1 = load8(so + 8 * (c + cs));
+                        st_v4(dst + dof + 8 * c, x0);
+                        st_v4(dst + dof + 8 * (c + cs), x1);
+                    }
+                    for (; c < vpr; c += cs) st_v4(dst + dof + 8 * c, load8(so + 8 * c));
+                }
             }
         }
     } else {

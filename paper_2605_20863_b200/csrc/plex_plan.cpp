@@ -11,8 +11,10 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <new>
 
 #include "plex_internal.h"
@@ -29,6 +31,91 @@ void set_error(const char* fmt, ...) {
 }
 
 static std::atomic<uint64_t> g_plan_ids{1};
+
+// a1 -- PAPER.md:555 (§5.2.2): "compares the incoming operation's target Job ID
+// with this map.  If they differ, the system automatically prepends offload and
+// load operations".  resident < 0 = nothing resident (load only).
+void transition_ops(int64_t resident, int64_t incoming, int32_t op, plex_transition* out) {
+    plex_transition t{};
+    t.mode = PLEX_SWITCH_NONE;
+    t.resident_before = resident < 0 ? -1 : resident;
+    auto add = [&](int32_t o, int64_t j) { t.ops[t.n_ops] = o; t.op_jobs[t.n_ops] = j; ++t.n_ops; };
+    if (resident != incoming) {
+        if (resident >= 0) add(PLEX_OP_OFFLOAD, resident);
+        if (incoming >= 0) add(PLEX_OP_ONLOAD, incoming);
+    }
+    if (op == PLEX_OP_SYNC) add(PLEX_OP_SYNC, incoming);
+    t.resident_after = incoming >= 0 ? incoming : t.resident_before;
+    *out = t;
+}
+
+// ---- R3 roles from parameter keys (PLEX_ROLE_AUTO) -----------------------------
+// Hugging Face / Qwen key conventions -> (role, fused group name, slot, expert,
+// unit).  Plain string parsing (75k keys for Qwen3-30B-A3B).
+static bool starts(const std::string& s, const char* p) { return s.compare(0, strlen(p), p) == 0; }
+static bool ends(const std::string& s, const char* p) {
+    const size_t n = strlen(p);
+    return s.size() >= n && s.compare(s.size() - n, n, p) == 0;
+}
+
+// "model.layers.<N>." prefix length (0 if the key is not a layer parameter)
+static size_t layer_prefix(const std::string& k) {
+    static const char* L = "model.layers.";
+    if (!starts(k, L)) return 0;
+    size_t i = strlen(L), j = i;
+    while (j < k.size() && k[j] >= '0' && k[j] <= '9') ++j;
+    if (j == i || j >= k.size() || k[j] != '.') return 0;
+    return j + 1;
+}
+
+struct AutoRole {
+    int32_t role, slot, expert, unit;
+    std::string group;
+};
+
+static AutoRole classify(const std::string& key, int32_t head_dim) {
+    AutoRole a{PLEX_ROLE_REPLICATED, 0, -1, 1, key};
+    if (ends(key, "embed_tokens.weight") || key == "lm_head.weight") { a.role = PLEX_ROLE_COL; return a; }
+    const size_t n = layer_prefix(key);
+    if (!n) return a;
+    const std::string pre = key.substr(0, n), rest = key.substr(n);
+    for (int q = 0; q < 3; ++q) {
+        const char* nm[3] = {"self_attn.q_proj.", "self_attn.k_proj.", "self_attn.v_proj."};
+        if (starts(rest, nm[q])) {
+            const std::string suf = rest.substr(strlen(nm[q]));
+            if (suf == "weight" || suf == "bias") {
+                a.role = PLEX_ROLE_COL;
+                a.slot = q;
+                a.unit = head_dim > 0 ? head_dim : 1;
+                a.group = pre + "self_attn.qkv_proj." + suf;
+            }
+            return a;
+        }
+    }
+    if (rest == "self_attn.o_proj.weight" || rest == "mlp.down_proj.weight") { a.role = PLEX_ROLE_ROW; return a; }
+    if (rest == "mlp.gate_proj.weight" || rest == "mlp.up_proj.weight") {
+        a.role = PLEX_ROLE_COL;
+        a.slot = rest == "mlp.gate_proj.weight" ? 0 : 1;
+        a.group = pre + "mlp.gate_up_proj.weight";
+        return a;
+    }
+    static const char* E = "mlp.experts.";
+    if (starts(rest, E)) {
+        size_t i = strlen(E), j = i;
+        while (j < rest.size() && rest[j] >= '0' && rest[j] <= '9') ++j;
+        if (j == i || j >= rest.size() || rest[j] != '.' || j - i > 9) return a;
+        const int32_t e = (int32_t)std::strtol(rest.substr(i, j - i).c_str(), nullptr, 10);
+        const std::string w = rest.substr(j + 1);
+        if (w == "gate_proj.weight" || w == "up_proj.weight") {
+            a.role = PLEX_ROLE_EXPERT; a.expert = e; a.slot = 2 * e + (w == "gate_proj.weight" ? 0 : 1);
+            a.group = pre + "mlp.experts.w13_weight";
+        } else if (w == "down_proj.weight") {
+            a.role = PLEX_ROLE_EXPERT; a.expert = e; a.slot = e;
+            a.group = pre + "mlp.experts.w2_weight";
+        }
+    }
+    return a;
+}
 
 // R2: FSDP-N dim-0 chunk of rank r: rows [min(d0, r*c), min(d0, (r+1)*c)).
 static inline void fsdp_rows(int64_t d0, int32_t world, int32_t r, int64_t* a, int64_t* b) {
@@ -434,15 +521,45 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
     if (sync && p.world % p.ep) { set_error("EP %d must divide world %d", p.ep, p.world); return PLEX_E_LAYOUT; }
     p.tensors.reserve(q->n_tensors);
     uint64_t total = 0;
+    const bool autoroles = q->tensors[0].role == PLEX_ROLE_AUTO;
+    std::unordered_map<std::string, int32_t> gid;
     for (int32_t i = 0; i < q->n_tensors; ++i) {
         const plex_tensor_desc& d = q->tensors[i];
         if (d.d0 < 0 || d.d1 < 1 || (d.ndim != 1 && d.ndim != 2) || (d.ndim == 1 && d.d1 != 1)) {
             set_error("tensor %d: bad shape", i); return PLEX_E_INVAL;
         }
         if (d.d1 > 0x7FFFFFFF || d.d0 > 0x7FFFFFFF) { set_error("tensor %d: dim too large", i); return PLEX_E_INVAL; }
-        if (d.role < 0 || d.role > PLEX_ROLE_EXPERT) { set_error("tensor %d: bad role", i); return PLEX_E_INVAL; }
-        if (d.role == PLEX_ROLE_EXPERT && d.expert < 0) { set_error("tensor %d: expert index", i); return PLEX_E_INVAL; }
-        p.tensors.push_back(Tensor{d.key ? d.key : "", d.d0, d.d1, d.ndim, d.role, d.group, d.slot, d.expert, d.unit});
+        if ((d.role == PLEX_ROLE_AUTO) != autoroles) {
+            set_error("tensor %d: PLEX_ROLE_AUTO must be used for every tensor or none", i); return PLEX_E_INVAL;
+        }
+        Tensor T{d.key ? d.key : "", d.d0, d.d1, d.ndim, d.role, d.group, d.slot, d.expert, d.unit};
+        if (autoroles) {
+            if (!d.key) { set_error("tensor %d: PLEX_ROLE_AUTO needs a key", i); return PLEX_E_INVAL; }
+            const AutoRole a = classify(T.key, q->head_dim);
+            auto it = gid.find(a.group);
+            if (it == gid.end()) {
+                it = gid.emplace(a.group, (int32_t)p.group_names.size()).first;
+                p.group_names.push_back(a.group);
+                p.group_role.push_back(a.role);
+                p.group_experts.push_back(0);
+            }
+            T.role = a.role; T.group = it->second; T.slot = a.slot; T.expert = a.expert; T.unit = a.unit;
+            if (a.role == PLEX_ROLE_EXPERT)
+                p.group_experts[T.group] = std::max(p.group_experts[T.group], a.expert + 1);
+        } else {
+            if (d.role < 0 || d.role > PLEX_ROLE_EXPERT) { set_error("tensor %d: bad role", i); return PLEX_E_INVAL; }
+            if (d.role == PLEX_ROLE_EXPERT && d.expert < 0) { set_error("tensor %d: expert index", i); return PLEX_E_INVAL; }
+            if (d.group < 0) { set_error("tensor %d: negative group", i); return PLEX_E_INVAL; }
+            if ((size_t)d.group >= p.group_names.size()) {
+                p.group_names.resize(d.group + 1);
+                p.group_role.resize(d.group + 1, -1);
+                p.group_experts.resize(d.group + 1, 0);
+            }
+            if (p.group_names[d.group].empty()) { p.group_names[d.group] = T.key; p.group_role[d.group] = d.role; }
+            if (d.role == PLEX_ROLE_EXPERT)
+                p.group_experts[d.group] = std::max(p.group_experts[d.group], d.expert + 1);
+        }
+        p.tensors.push_back(std::move(T));
         total += (uint64_t)d.d0 * (uint64_t)d.d1;
     }
     if (q->n_subset > 0 && q->subset) {
@@ -455,15 +572,14 @@ static plex_status build(const plex_plan_req* q, Plan& p) {
         p.subset.resize(q->n_tensors);
         for (int32_t i = 0; i < q->n_tensors; ++i) p.subset[i] = i;
     }
-    // a1: transition ops.
+    // a1: transition ops, the same decision the group executor takes.
     plex_plan_stats& st = p.stats;
-    st.n_ops = 0;
-    auto add_op = [&](int32_t op, int64_t job) { st.ops[st.n_ops] = op; st.op_jobs[st.n_ops] = job; ++st.n_ops; };
-    if (q->resident_job != q->incoming_job) {
-        if (q->resident_job >= 0) add_op(PLEX_OP_OFFLOAD, q->resident_job);
-        if (q->incoming_job >= 0) add_op(PLEX_OP_ONLOAD, q->incoming_job);
+    {
+        plex_transition t;
+        transition_ops(q->resident_job, q->incoming_job, q->op, &t);
+        st.n_ops = t.n_ops;
+        for (int i = 0; i < 4; ++i) { st.ops[i] = t.ops[i]; st.op_jobs[i] = t.op_jobs[i]; }
     }
-    if (q->op == PLEX_OP_SYNC) add_op(PLEX_OP_SYNC, q->incoming_job);
     st.n_tensors = q->n_tensors;
     st.world = p.world; st.tp = p.tp; st.dp = p.dp; st.ep = p.ep;
     st.total_params = total;
@@ -590,6 +706,34 @@ plex_status plex_plan_dst_tensor(plex_plan_t plan, int32_t rank, int32_t i, plex
     out->arena_offset = D.arena_off;
     out->rows = D.rows;
     out->cols = D.cols;
+    return PLEX_OK;
+}
+
+plex_status plex_plan_group(plex_plan_t plan, int32_t group, char* buf, int32_t cap, int32_t* len, int32_t* role,
+                            int32_t* n_experts) {
+    if (!plan) { set_error("NULL plan"); return PLEX_E_INVAL; }
+    const Plan& p = plan->p;
+    if (group < 0 || group >= (int32_t)p.group_names.size() || p.group_role[group] < 0) {
+        set_error("group %d out of range", group);
+        return PLEX_E_INVAL;
+    }
+    const std::string& n = p.group_names[group];
+    if (len) *len = (int32_t)n.size();
+    if (buf && cap > 0) {
+        const size_t k = std::min<size_t>((size_t)cap - 1, n.size());
+        std::memcpy(buf, n.data(), k);
+        buf[k] = '\0';
+    }
+    if (role) *role = p.group_role[group];
+    if (n_experts) *n_experts = p.group_experts[group];
+    return PLEX_OK;
+}
+
+plex_status plex_transition_decide(int64_t resident, int64_t incoming, int32_t op, plex_transition* out) {
+    if (!out) { set_error("NULL out"); return PLEX_E_INVAL; }
+    if (op != PLEX_OP_NONE && op != PLEX_OP_SYNC) { set_error("op must be PLEX_OP_NONE or PLEX_OP_SYNC"); return PLEX_E_INVAL; }
+    if (op == PLEX_OP_SYNC && incoming < 0) { set_error("SYNC needs an incoming job"); return PLEX_E_INVAL; }
+    transition_ops(resident, incoming, op, out);
     return PLEX_OK;
 }
 

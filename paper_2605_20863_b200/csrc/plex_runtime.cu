@@ -77,6 +77,11 @@ struct DevPlan {
     PackItem* items = nullptr;
     PushItem* push = nullptr;
     PushItem* gather = nullptr;               // NEXT-2 replicated-param all-gather items
+    // PLEX_CTX_SPLIT_PUSH: the push items split by destination (built on first use)
+    PushItem* push_local = nullptr;
+    PushItem* push_remote = nullptr;
+    uint64_t n_push_local = 0, n_push_remote = 0, push_local_elems = 0, push_remote_elems = 0;
+    bool push_split = false;
     unsigned long long* cks = nullptr;        // computed (S1,S2) per segment
     unsigned long long* cks_want = nullptr;   // expected, uploaded at onload
     unsigned long long* cks_in = nullptr;     // recomputed at onload
@@ -220,6 +225,8 @@ static void free_devplan(DevPlan& d) {
     cudaFree(d.items);
     cudaFree(d.push);
     cudaFree(d.gather);
+    cudaFree(d.push_local);
+    cudaFree(d.push_remote);
     cudaFree(d.cks);
     cudaFree(d.cks_want);
     cudaFree(d.cks_in);
@@ -392,6 +399,10 @@ static plex_status finish(plex_ctx_s* c, cudaStream_t caller) {
     CK(cudaStreamSynchronize(c->pack));
     CK(cudaStreamSynchronize(c->copy));
     return timed_collect(c);
+}
+
+void ctx_query(plex_ctx_t c, CtxInfo* o) {
+    *o = CtxInfo{c->staging_bytes, c->n_slots, c->rank, c->world, c->device, c->comm != nullptr};
 }
 
 static plex_status check_common(plex_ctx_s* c, plex_plan_t plan) {
@@ -1089,6 +1100,13 @@ plex_status plex_ctx_set_carry_staging(plex_ctx_t c, void* staging, uint64_t byt
 plex_status plex_ctx_stats(plex_ctx_t c, int32_t which, plex_kernel_stats* out) {
     if (!c || !out || which < 0 || which >= PLEX_NUM_STATS) { set_error("bad stats query"); return PLEX_E_INVAL; }
     *out = c->stats[which];
+    return PLEX_OK;
+}
+
+plex_status plex_ctx_set_flags(plex_ctx_t c, uint32_t value, uint32_t mask) {
+    if (!c) { set_error("NULL ctx"); return PLEX_E_INVAL; }
+    if (mask & ~(PLEX_CTX_TIMING | PLEX_CTX_SPLIT_PUSH)) { set_error("only TIMING / SPLIT_PUSH may change"); return PLEX_E_INVAL; }
+    c->flags = (c->flags & ~mask) | (value & mask);
     return PLEX_OK;
 }
 
@@ -2018,7 +2036,8 @@ plex_status plex_state_wait(plex_ctx_t c, int32_t op, void* caller_stream) {
 
 // ---- a8 - a11: weight sync -------------------------------------------------------------
 static plex_status push_rank(plex_ctx_s* c, const Plan& p, int32_t rank, const void* const* src, int32_t n_src,
-                             void* const* arenas, cudaStream_t s, const PushItem* d_items) {
+                             void* const* arenas, cudaStream_t s, const PushItem* d_items,
+                             const DevPlan* split = nullptr) {
     const size_t nt = p.tensors.size();
     if (!src || (size_t)n_src != nt) { set_error("expected %zu master pointers, got %d", nt, n_src); return PLEX_E_INVAL; }
     const RankPlan& R = p.ranks[rank];
@@ -2031,9 +2050,35 @@ static plex_status push_rank(plex_ctx_s* c, const Plan& p, int32_t rank, const v
     }
     CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, (nt + p.world) * 8, cudaMemcpyHostToDevice, s));
     cudaEvent_t ta = nullptr;
+    if (split) {
+        // diagnostic: local items (HBM only) then remote items (NVLink), each timed
+        if ((st = timed_begin(c, s, &ta))) return st;
+        CK(launch_push(true, split->push_local, split->n_push_local, c->d_ptrs, c->d_ptrs + nt, s));
+        if ((st = timed_end(c, s, ta, PLEX_STAT_PUSH_LOCAL, 6 * split->push_local_elems))) return st;
+        if ((st = timed_begin(c, s, &ta))) return st;
+        CK(launch_push(true, split->push_remote, split->n_push_remote, c->d_ptrs, c->d_ptrs + nt, s));
+        return timed_end(c, s, ta, PLEX_STAT_PUSH_REMOTE, 2 * split->push_remote_elems);
+    }
     if ((st = timed_begin(c, s, &ta))) return st;
     CK(launch_push(true, d_items, R.push.size(), c->d_ptrs, c->d_ptrs + nt, s));
     if ((st = timed_end(c, s, ta, PLEX_STAT_PUSH, R.src_read_bytes + R.src_read_bytes / 2))) return st;
+    return PLEX_OK;
+}
+
+// PLEX_CTX_SPLIT_PUSH tables: this rank's push items partitioned by destination.
+static plex_status split_push(plex_ctx_s* c, const Plan& p, DevPlan* d) {
+    if (d->push_split) return PLEX_OK;
+    std::vector<PushItem> loc, rem;
+    for (const PushItem& it : p.ranks[c->rank].push) {
+        const uint64_t n = (uint64_t)it.rows * it.cols;
+        if ((int32_t)it.dst_rank == c->rank) { loc.push_back(it); d->push_local_elems += n; }
+        else { rem.push_back(it); d->push_remote_elems += n; }
+    }
+    plex_status st;
+    if ((st = upload(&d->push_local, loc)) || (st = upload(&d->push_remote, rem))) return st;
+    d->n_push_local = loc.size();
+    d->n_push_remote = rem.size();
+    d->push_split = true;
     return PLEX_OK;
 }
 
@@ -2146,7 +2191,10 @@ plex_status plex_weight_sync(plex_ctx_t c, plex_plan_t plan, const void* const* 
         NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));
         if ((st = timed_end(c, c->pack, tb, PLEX_STAT_BARRIER, 0))) return st;
     }
-    if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push))) return st;
+    const bool split = (c->flags & PLEX_CTX_SPLIT_PUSH) && c->world > 1;
+    if (split && (st = split_push(c, p, d))) return st;
+    if ((st = push_rank(c, p, c->rank, src_master, n_src, arenas.data(), c->pack, d->push, split ? d : nullptr)))
+        return st;
     if (c->world > 1) NK(ncclAllReduce(d_bar, d_bar, 1, ncclInt32, ncclSum, c->comm, c->pack));   // all pushes landed
     return finish(c, caller);
 }

@@ -27,62 +27,6 @@ KIND_TORCH = {0: torch.bfloat16, 1: torch.float32, 2: torch.float32, 3: torch.fl
 _LAYER = re.compile(r"^(model\.layers\.\d+\.)")
 
 
-# ---------------------------------------------------------------------------
-# R3 roles from parameter names (product side; the oracle has its own reading)
-# ---------------------------------------------------------------------------
-def describe(manifest: Sequence[Tuple[str, Tuple[int, ...]]], head_dim: int = 1):
-    """Return (descs, group_names): plex_tensor_desc fields per tensor and the
-    rollout tensor name of every destination group.
-
-    Column-parallel q/k/v (+bias) fuse into ``qkv_proj`` (split unit =
-    head_dim), gate/up into ``gate_up_proj``; o_proj/down_proj are
-    row-parallel; embed_tokens/lm_head vocab-parallel (column split); experts
-    stack into ``experts.w13_weight`` (gate_e|up_e) and ``experts.w2_weight``;
-    everything else (norms, router) is replicated.
-    """
-    groups: Dict[str, int] = OrderedDict()
-
-    def gid(name: str) -> int:
-        if name not in groups:
-            groups[name] = len(groups)
-        return groups[name]
-
-    descs = []
-    for key, shape in manifest:
-        d0 = int(shape[0])
-        d1 = int(np.prod(shape[1:])) if len(shape) > 1 else 1
-        ndim = len(shape)
-        m = _LAYER.match(key)
-        pre = m.group(1) if m else ""
-        role, slot, expert, unit = L.ROLE_REPLICATED, 0, -1, 1
-        gname = key
-        mm = re.match(r"^(model\.layers\.\d+\.)self_attn\.([qkv])_proj\.(weight|bias)$", key)
-        me = re.match(r"^(model\.layers\.\d+\.)mlp\.experts\.(\d+)\.(gate|up|down)_proj\.weight$", key)
-        if key.endswith("embed_tokens.weight") or key == "lm_head.weight":
-            role = L.ROLE_COL
-        elif mm:
-            role, slot, unit = L.ROLE_COL, "qkv".index(mm.group(2)), head_dim
-            gname = f"{pre}self_attn.qkv_proj.{mm.group(3)}"
-        elif key.endswith("self_attn.o_proj.weight"):
-            role = L.ROLE_ROW
-        elif me:
-            e, which = int(me.group(2)), me.group(3)
-            role, expert = L.ROLE_EXPERT, e
-            if which == "down":
-                gname, slot = f"{pre}mlp.experts.w2_weight", e
-            else:
-                gname, slot = f"{pre}mlp.experts.w13_weight", 2 * e + (0 if which == "gate" else 1)
-        elif re.match(r"^model\.layers\.\d+\.mlp\.(gate|up)_proj\.weight$", key):
-            role, slot = L.ROLE_COL, 0 if ".gate_proj." in key else 1
-            gname = f"{pre}mlp.gate_up_proj.weight"
-        elif re.match(r"^model\.layers\.\d+\.mlp\.down_proj\.weight$", key):
-            role = L.ROLE_ROW
-        descs.append(dict(key=key, d0=d0, d1=d1, ndim=ndim, role=role, group=gid(gname), slot=slot,
-                          expert=expert, unit=unit))
-    names = {v: k for k, v in groups.items()}
-    return descs, names
-
-
 class Plan:
     """Immutable transition plan (plex_transition_plan)."""
 
@@ -94,13 +38,13 @@ class Plan:
                  link_weights: Optional[Sequence[float]] = None, replica_param: bool = False):
         self.manifest = list(manifest)
         self.index = {k: i for i, (k, _) in enumerate(self.manifest)}
-        descs, self.group_names = describe(self.manifest, head_dim)
-        self.descs = descs
-        self._keys = [d["key"].encode() for d in descs]
-        arr = (L.TensorDesc * len(descs))()
-        for i, d in enumerate(descs):
-            arr[i] = L.TensorDesc(self._keys[i], d["d0"], d["d1"], d["ndim"], d["role"], d["group"], d["slot"],
-                                  d["expert"], d["unit"])
+        # keys and shapes only: the library derives every tensor's rollout role,
+        # fusion group and split unit from its key (PLEX_ROLE_AUTO, reading R3)
+        self._keys = [k.encode() for k, _ in self.manifest]
+        arr = (L.TensorDesc * len(self.manifest))()
+        for i, (key, shape) in enumerate(self.manifest):
+            d1 = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+            arr[i] = L.TensorDesc(self._keys[i], int(shape[0]), d1, len(shape), L.ROLE_AUTO, 0, 0, -1, 1)
         self._arr = arr
         sub = None
         n_sub = 0
@@ -112,10 +56,10 @@ class Plan:
         self._lw = None
         if link_weights is not None:
             self._lw = (C.c_float * world)(*[float(x) for x in link_weights])
-        req = L.PlanReq(len(descs), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
+        req = L.PlanReq(len(self.manifest), arr, world, tp, dp, ep, rank_map, slab_layout, kind_mask, n_sub, sub,
                         bucket_bytes, tile_bytes, resident_job, incoming_job, op,
                         (L.PLAN_ELIDE_PARAM if elide_param else 0) | (L.PLAN_REPLICA_PARAM if replica_param else 0),
-                        self._lw)
+                        self._lw, head_dim)
         h = C.c_void_p()
         check(lib.plex_transition_plan(C.byref(req), C.byref(h)))
         self.h = h
@@ -172,6 +116,20 @@ class Plan:
             cache[rank] = [int(np.prod(self.shard_shape(rank, t))) for t in range(len(self.manifest))]
         return cache[rank]
 
+    def group(self, g: int) -> Tuple[str, int, int]:
+        """(rollout tensor name, role, experts stacked) of destination group g,
+        as the library's planner classified it (plex_plan_group)."""
+        cache = self.__dict__.setdefault("_groups", {})
+        if g not in cache:
+            buf = C.create_string_buffer(512)
+            n, role, ne = C.c_int32(), C.c_int32(), C.c_int32()
+            check(lib.plex_plan_group(self.h, g, buf, 512, C.byref(n), C.byref(role), C.byref(ne)))
+            if n.value >= 512:
+                buf = C.create_string_buffer(n.value + 1)
+                check(lib.plex_plan_group(self.h, g, buf, n.value + 1, None, None, None))
+            cache[g] = (buf.value.decode(), role.value, ne.value)
+        return cache[g]
+
     def dst_tensors(self, rank: int) -> List[Tuple[str, int, Tuple[int, ...]]]:
         """(rollout name, arena byte offset, shape) of rank's destination tensors."""
         n = self.rank_info(rank).n_dst_tensors
@@ -179,20 +137,15 @@ class Plan:
         for i in range(n):
             d = L.DstDesc()
             check(lib.plex_plan_dst_tensor(self.h, rank, i, C.byref(d)))
-            name = self.group_names[d.group]
+            name, role, n_exp = self.group(d.group)
             shape: Tuple[int, ...] = (d.rows, d.cols)
-            if name.endswith(("w13_weight", "w2_weight")):
-                per = self.n_experts(name) // self.ep
+            if role == L.ROLE_EXPERT:
+                per = n_exp // self.ep
                 shape = (per, d.rows // per, d.cols)
-            elif self.descs[d.first_tensor]["ndim"] == 1:
+            elif len(self.manifest[d.first_tensor][1]) == 1:
                 shape = (d.rows,)
             out.append((name, d.arena_offset, shape))
         return out
-
-    def n_experts(self, group_name: str) -> int:
-        pre = group_name.rsplit("mlp.experts.", 1)[0]
-        return sum(1 for d in self.descs if d["key"].startswith(pre + "mlp.experts.")
-                   and d["key"].endswith("down_proj.weight"))
 
     def carry(self) -> List[L.CarryDesc]:
         """Carried buckets (NEXT-1 host-link balancing), in the plan's global order."""
@@ -603,6 +556,11 @@ class StateManager:
     def reset_stats(self) -> None:
         check(lib.plex_ctx_reset_stats(self.h))
 
+    def set_split_push(self, on: bool) -> None:
+        """Diagnostic (PLEX_CTX_SPLIT_PUSH): time the sync's local and remote push
+        items as two launches (stats "push_local" / "push_remote")."""
+        check(lib.plex_ctx_set_flags(self.h, L.CTX_SPLIT_PUSH if on else 0, L.CTX_SPLIT_PUSH))
+
 
 # ---- infrastructure (synthetic inputs, verification) ------------------------------
 def synth_fill(t: torch.Tensor, kind: int, seed: int, key: str, index_base: int = 0, special_bits: int = 0,
@@ -663,11 +621,14 @@ class Job:
         """Counter-based synthetic state.  derived_param: the bf16
         params are RNE(master) -- what a mixed-precision optimizer step leaves --
         computed by this library's cast kernel instead of drawn independently."""
+        by_key: Dict[str, list] = {}
+        for (k2, kd), x in self.shards.items():
+            by_key.setdefault(k2, []).append((kd, x))
         for t, (key, shape) in enumerate(self.plan.manifest):
             r0, _ = self.plan.shard_rows(self.rank, t)
             re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
-            for (k2, kd), x in self.shards.items():
-                if k2 == key and not (derived_param and kd == 0):
+            for kd, x in by_key.get(key, ()):
+                if not (derived_param and kd == 0):
                     full = kd == L.KIND_PARAM and self.param_arena is not None
                     synth_fill(x, kd, self.seed, key, 0 if full else r0 * re_, special_bits)
             if derived_param and (key, 0) in self.shards and (key, 1) in self.shards:
@@ -763,3 +724,142 @@ class Job:
 
     def sync(self, arena: torch.Tensor, stream=None) -> None:
         self.mgr.sync(self.plan, self.masters(), arena, stream)
+
+
+# ---- a1: transition decision and the group's residency authority ----------------------
+def transition_decide(resident: Optional[int], incoming: int, sync: bool = False) -> List[Tuple[int, int]]:
+    """PAPER.md:555 op list [(PLEX_OP_*, job)] from the library (plex_transition_decide)."""
+    t = L.Transition()
+    check(lib.plex_transition_decide(-1 if resident is None else resident, incoming,
+                                     L.OP_SYNC if sync else L.OP_NONE, C.byref(t)))
+    return [(t.ops[i], t.op_jobs[i]) for i in range(t.n_ops)]
+
+
+class Group:
+    """The GPU group's resident-job map and transition executor (plex_group_*,
+    PAPER.md:555 ``group_executor_gpu_job`` / ``_handle_job_transition``).
+
+    One per rank process (on its StateManager).  ``add`` registers jobs;
+    ``transition(job, sync=...)`` makes ``job`` the resident one: the library
+    decides the ops (offload the resident job, onload ``job``, optional sync),
+    picks swap / duplex / sequential from what fits, and calls back here only
+    to acquire or release a job's device storage (a5, PyTorch memory).
+    ``hbm_budget`` (bytes, optional) caps the job-state bytes the group may
+    hold on the device at once; an acquire beyond it (or a CUDA OOM) makes the
+    library switch sequentially."""
+
+    def __init__(self, mgr: StateManager, hbm_budget: Optional[int] = None):
+        self.mgr = mgr
+        self.hbm_budget = hbm_budget
+        self.jobs: Dict[int, Job] = {}
+        self._storage_of: Dict[int, Optional[int]] = {}
+        self._cb = L.STORAGE_FN(self._storage)          # kept alive with the group
+        self._cb_error: Optional[BaseException] = None
+        h = C.c_void_p()
+        check(lib.plex_group_create(mgr.h, self._cb, None, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and lib is not None:
+            lib.plex_group_destroy(h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---- registration -----------------------------------------------------------------
+    def _table(self, job: Job):
+        return self.mgr._state_ptrs(job.plan, job.shards, job.rank)
+
+    def add(self, job: Job, resident: bool = False, storage: Optional[int] = None) -> int:
+        """Register ``job``; returns its id.  resident=True: its state is on the
+        device now (at most one such job).  Jobs given the same ``storage`` id
+        share one set of device tensors (in-place swaps): register the one whose
+        shards are allocated first."""
+        jid = len(self.jobs)
+        arr, n = (None, 0)
+        if job.shards and all(v.untyped_storage().nbytes() == v.numel() * v.element_size()
+                              for v in job.slab_shards().values()):
+            arr, n = self._table(job)
+        check(lib.plex_group_add_job(self.h, jid, job.plan.h, job.slab.h if job.slab is not None else None,
+                                     -1 if storage is None else storage, L.GROUP_RESIDENT if resident else 0,
+                                     arr, n))
+        self.jobs[jid] = job
+        self._storage_of[jid] = storage
+        job.group_id = jid
+        return jid
+
+    @property
+    def resident(self) -> Optional[Job]:
+        j = C.c_int64()
+        check(lib.plex_group_resident(self.h, C.byref(j)))
+        return None if j.value < 0 else self.jobs[j.value]
+
+    # ---- a5 storage callback (runs inside plex_group_transition) ------------------------------
+    def _device_bytes(self) -> int:
+        n = 0
+        for jb in self.jobs.values():
+            for v in jb.slab_shards().values():
+                n += v.untyped_storage().nbytes()
+        return n
+
+    def _storage(self, user, jid, acquire, state, n_state):
+        try:
+            job = self.jobs[jid]
+            if acquire:
+                if self.hbm_budget is not None:
+                    need = sum(v.numel() * v.element_size() for v in job.slab_shards().values())
+                    if self._device_bytes() + need > self.hbm_budget:
+                        return 1                                       # does not fit: go sequential
+                try:
+                    job.acquire()
+                except torch.OutOfMemoryError:
+                    return 1
+                arr, n = self._table(job)
+                if n != n_state:
+                    raise ValueError(f"pointer table of {n} entries, library expects {n_state}")
+                for i in range(n):
+                    state[i] = arr[i]
+            else:
+                job.release()
+            return 0
+        except BaseException as e:                                   # never let an exception cross the ABI
+            self._cb_error = e
+            return 2
+
+    # ---- the transition --------------------------------------------------------------------
+    def transition(self, job: Job, sync=None, stream=None) -> dict:
+        """Run (op of) ``job`` on the group: [OFFLOAD resident, ONLOAD job] when
+        they differ, then SYNC job when ``sync`` is given -- one
+        rollout arena (collective sync) or every rank's arena (emulation).
+        Returns {"ops": [(op, job id)], "mode": "swap"|"duplex"|...,
+        "resident_before", "resident_after"}."""
+        jid = job.group_id
+        arenas, n_ar = None, 0
+        if sync is not None:
+            lst = list(sync) if isinstance(sync, (list, tuple)) else [sync]
+            for g, a in enumerate(lst):
+                StateManager._check_arena(job.plan, a, self.mgr.rank if len(lst) == 1 else g)
+            arenas, n_ar = ptr_array([a.data_ptr() for a in lst]), len(lst)
+        t = L.Transition()
+        self._cb_error = None
+        rb = C.c_int64()
+        check(lib.plex_group_resident(self.h, C.byref(rb)))
+        before = self.jobs.get(rb.value) if rb.value >= 0 else None
+        code = lib.plex_group_transition(self.h, jid, L.OP_SYNC if sync is not None else L.OP_NONE, arenas, n_ar,
+                                         _stream_ptr(stream), C.byref(t))
+        if self._cb_error is not None:
+            raise RuntimeError("storage callback failed") from self._cb_error
+        shared = (before is not None and before is not job and self._storage_of.get(before.group_id) is not None
+                  and self._storage_of.get(before.group_id) == self._storage_of.get(jid))
+        if shared and (code == L.OK or code == L.E_CHECKSUM):
+            # mirror the library's in-place swap: the slab now holds the outgoing
+            # state; on success the tensors hold the incoming one
+            before.slab, job.slab = job.slab, before.slab
+            if code == L.OK:
+                before.shards, job.shards = job.shards, before.shards
+                before.param_arena, job.param_arena = job.param_arena, before.param_arena
+        check(code)
+        return {"ops": [(t.ops[i], t.op_jobs[i]) for i in range(t.n_ops)], "mode": L.SWITCH_NAMES[t.mode],
+                "resident_before": t.resident_before, "resident_after": t.resident_after}

@@ -4,7 +4,7 @@ INPUT MODULE. Every element of every synthetic state tensor is a pure function
 of (seed, logical key, kind, flat index i in the *logical, unsharded* tensor),
 so any rank can produce its own shard and the oracle can produce any slice,
 bit-identically.  The CUDA product path implements the same counter-based
-generator independently (paper_2605_20863_b200/csrc/plex_synth.cu); the two
+generator independently (synth_kernel in paper_2605_20863_b200/csrc/plex_kernels.cu); the two
 share no code.  Nothing here is the method's arithmetic: there is no cast, no
 layout, no checksum.
 

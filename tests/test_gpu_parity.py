@@ -219,6 +219,12 @@ def test_weight_sync_world1_collective_entry():
 
 # ---- o10 multiplex trace (emulated 4 ranks, 4 jobs) ----------------------------------------------------
 def test_multiplex_emulated():
+    """configs[4] multiplex trace through the product's residency authority: one
+    plex_group per (emulated) rank decides every switch itself
+    and executes it; the op lists must equal the oracle's transition_ops and
+    the rollout weights / final states the oracle's multiplex_replay.  Jobs
+    release their device storage while suspended (a5) and are re-acquired
+    through the group's storage callback."""
     W = 4
     models = ["toy", "toy-tied", "toy-moe", "mid"]
     layouts = [(2, 2, 1), (1, 4, 1), (2, 2, 2), (2, 2, 1)]
@@ -229,17 +235,28 @@ def test_multiplex_emulated():
     mgrs = [mgr(W, r, bucket=1 << 14) for r in range(W)]
     jobs = [[P.Job(mgrs[r], plans[j], seed=seeds[j], rank=r).alloc().init_synthetic() for r in range(W)]
             for j in range(4)]
-    for j in range(4):                      # every job starts HOST-resident
+    for j in range(4):                      # every job starts HOST-resident, device storage released
         for r in range(W):
             jobs[j][r].suspend()
+    groups = [P.Group(mgrs[r]) for r in range(W)]
+    for r in range(W):
+        for j in range(4):
+            assert groups[r].add(jobs[j][r]) == j
     resident = None
     steps = [0] * 4
-    outs = []
+    outs, modes = [], []
     for j in schedule:
-        ops = O.transition_ops(resident, j)
-        for op, job in ops:
+        want_ops = O.transition_ops(resident, j)
+        for r in range(W):
+            res = groups[r].transition(jobs[j][r])                # the product decides and executes
+            assert res["ops"] == want_ops, (j, r, res)
+            assert res["resident_after"] == j and groups[r].resident is jobs[j][r]
+            modes.append(res["mode"])
+        for jj in range(4):                                       # a5: only the resident job holds HBM
             for r in range(W):
-                (jobs[job][r].suspend() if op == O.OP_OFFLOAD else jobs[job][r].resume())
+                held = all(v.untyped_storage().nbytes() > 0 or v.numel() == 0
+                           for v in jobs[jj][r].slab_shards().values())
+                assert held == (jj == j), (jj, r)
         resident = j
         for r in range(W):
             for t, (key, shape) in enumerate(plans[j].manifest):
@@ -249,10 +266,12 @@ def test_multiplex_emulated():
                     P.synth_mutate(jobs[j][r].shards[(key, kd)], kd, seeds[j], steps[j], key, a * re_)
         steps[j] += 1
         arenas = [mgrs[0].arena(plans[j], g) for g in range(W)]
-        for r in range(W):
-            mgrs[0].sync_rank(plans[j], r, jobs[j][r].masters(), arenas)
+        for r in range(W):                                        # resident already: [SYNC j] only
+            res = groups[r].transition(jobs[j][r], sync=arenas)
+            assert res["ops"] == O.transition_ops(j, j, True) and res["mode"] == "none"
         outs.append([{k: bits_np(v) for k, v in P.StateManager.rollout_views(plans[j], g, arenas[g]).items()}
                      for g in range(W)])
+    assert modes[:W] == ["load"] * W and set(modes[W:]) == {"duplex"}
     # oracle replay
     ojobs = []
     for mo, sd, (tp, dp, ep) in zip(models, seeds, layouts):
@@ -270,13 +289,91 @@ def test_multiplex_emulated():
         for g in range(W):
             for name, x in want[g].items():
                 assert np.array_equal(outs[v][g][name], x), (v, g, name)
-    for j in range(4):
-        if j != resident:
-            for r in range(W):
-                jobs[j][r].resume()
+    for j in range(4):                       # every final state, brought back through the groups
         for r in range(W):
+            groups[r].transition(jobs[j][r])
             for k, x in jobs[j][r].shards.items():
                 assert np.array_equal(bits_np(x), final[j][r][k]), (j, r, k)
+
+
+def test_group_modes_and_failures():
+    """plex_group_transition picks the switch from what fits (R17):
+    LOAD with nothing resident, NONE for the resident job, DUPLEX when the
+    incoming storage can be acquired beside the resident one, SEQUENTIAL under
+    an HBM budget for one job, SWAP for jobs sharing device storage; a corrupted
+    incoming slab leaves no job resident and the outgoing state safe."""
+    man = manifest("mid")
+    hd = MODELS["mid"].head_dim
+    plan = P.Plan(man, head_dim=hd, world=1, tp=1, dp=1, bucket_bytes=1 << 16, tile_bytes=4096)
+    m = mgr(1, 0, bucket=1 << 16)
+    fx, fy = full_state("mid", seed=31, special_bits=3), full_state("mid", seed=32, special_bits=3)
+    segs, size = O.slab_layout(man, 1, 0)
+    x = P.Job(m, plan, seed=31).alloc().init_synthetic(special_bits=3)
+    y = P.Job(m, plan, seed=32).alloc().init_synthetic(special_bits=3)
+    x.suspend()
+    y.suspend()
+    job_bytes = sum(v.numel() * v.element_size() for v in x.slab_shards().values())
+    for budget, mode in ((None, "duplex"), (job_bytes, "sequential")):
+        g = P.Group(m, hbm_budget=budget)
+        ix, iy = g.add(x), g.add(y)
+        assert g.resident is None
+        r = g.transition(x)
+        assert r["mode"] == "load" and r["ops"] == [(L.OP_ONLOAD, ix)] and r["resident_before"] == -1
+        assert g.transition(x)["mode"] == "none"
+        r = g.transition(y)
+        assert r["mode"] == mode and r["ops"] == [(L.OP_OFFLOAD, ix), (L.OP_ONLOAD, iy)], r
+        assert g.resident is y and all(v.untyped_storage().nbytes() == 0 for v in x.slab_shards().values())
+        assert np.array_equal(x.slab.host_bytes(), O.pack_slab(segs, size, fx))
+        for kk, v in y.shards.items():
+            assert np.array_equal(bits_np(v), fy[kk]), kk
+        arena = m.arena(plan)
+        r = g.transition(y, sync=arena)
+        assert r["ops"] == [(L.OP_SYNC, iy)]
+        want = O.weight_sync(master_shards(fy, 1, O.fsdp_rows), 1, 1, 1, O.TP_FAST, hd)[0]
+        for name, v in P.StateManager.rollout_views(plan, 0, arena).items():
+            assert np.array_equal(bits_np(v), want[name]), name
+        g.transition(x)                                           # back, then hand both to the next group
+        x.suspend()
+        g.close()
+        del g
+    # a corrupted incoming slab: E_CHECKSUM, nothing resident, the outgoing state safe in its slab
+    g = P.Group(m)
+    ix, iy = g.add(x), g.add(y)
+    g.transition(x)
+    y.slab.host_bytes()[segs[3].offset] ^= 0x40
+    with pytest.raises(P.PlexError) as e:
+        g.transition(y)
+    assert e.value.code == L.E_CHECKSUM and g.resident is None
+    assert np.array_equal(x.slab.host_bytes(), O.pack_slab(segs, size, fx))
+    g.transition(x)                                               # x comes back intact
+    for kk, v in x.shards.items():
+        assert np.array_equal(bits_np(v), fx[kk]), kk
+    g.close()
+    # SWAP: two jobs sharing one set of device tensors and one slab
+    a = P.Job(m, plan, seed=33, slab=False).alloc()
+    b = P.Job(m, plan, seed=34)
+    b.shards = a.shards
+    b.init_synthetic(special_bits=3)
+    b.suspend(release=False)
+    b.shards = OrderedDict()
+    a.init_synthetic(special_bits=3)
+    fa, fb = full_state("mid", seed=33, special_bits=3), full_state("mid", seed=34, special_bits=3)
+    g = P.Group(m)
+    ia = g.add(a, resident=True, storage=0)
+    ib = g.add(b, storage=0)
+    with pytest.raises(P.PlexError) as e:                        # one resident job per group (R17)
+        g.add(P.Job(m, plan, seed=35).alloc(), resident=True)
+    assert e.value.code == L.E_STATE
+    for k in range(3):
+        inc, out, f_in, f_out = (b, a, fb, fa) if k % 2 == 0 else (a, b, fa, fb)
+        r = g.transition(inc)
+        assert r["mode"] == "swap" and r["ops"] == [(L.OP_OFFLOAD, out.group_id), (L.OP_ONLOAD, inc.group_id)]
+        assert inc.slab is None and out.slab is not None and g.resident is inc
+        for kk, v in inc.shards.items():
+            assert np.array_equal(bits_np(v), f_in[kk]), kk
+        assert np.array_equal(out.slab.host_bytes(), O.pack_slab(segs, size, f_out))
+    g.close()
+    m.close()
 
 
 # ---- NEXT-1 duplex switch --------------------------------------------------------------------------
