@@ -205,9 +205,23 @@ def box_info() -> dict:
     return out
 
 
-def _max_rss_gb(who) -> float:
-    import resource
-    return round(resource.getrusage(who).ru_maxrss * 1024 / 1e9, 2)
+def _hwm_gb() -> float:
+    """This process's own resident high-water mark (VmHWM; getrusage's ru_maxrss
+    would report the bench parent's peak in a spawned child)."""
+    try:
+        for ln in open("/proc/self/status"):
+            if ln.startswith("VmHWM:"):
+                return round(int(ln.split()[1]) * 1024 / 1e9, 2)
+    except OSError:
+        pass
+    return -1.0
+
+
+def _oracle_single_worker(args):
+    """The single-process setting in its own process (its own memory high-water mark)."""
+    model, world, tp, ep, layers = args
+    v, dt, sample = cpu_oracle_sample(model, world, tp, ep, layers)
+    return v, dt, sample, _hwm_gb()
 
 
 def _oracle_rank_worker(args):
@@ -245,7 +259,7 @@ def _oracle_rank_worker(args):
     full = OrderedDict((k, O.rne_bf16(O.gather(v))) for k, v in ms.items())
     O.rollout_tensors(full, tp, dp, ep, r)
     dt = time.perf_counter() - t0
-    return S, dt, _max_rss_gb(0)
+    return S, dt, _hwm_gb()
 
 
 def cpu_oracle_ranks(model: str, W: int, tp: int, ep: int, layers: int) -> dict:
@@ -269,9 +283,11 @@ def cpu_oracle_ranks(model: str, W: int, tp: int, ep: int, layers: int) -> dict:
 def cpu_baseline(a, world: int, tp: int) -> dict:
     """cpu_baseline of the bench line: the oracle, as it stands, on the box's host
     cores -- single process (headline, as the reference arm) plus the per-rank setting."""
-    v, dt, sample = cpu_oracle_sample(a.model, world, tp, a.ep, a.cpu_sample_layers)
+    import multiprocessing as mp
+    with mp.get_context("spawn").Pool(1) as pool:
+        v, dt, sample, hwm = pool.apply(_oracle_single_worker, ((a.model, world, tp, a.ep, a.cpu_sample_layers),))
     out = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
-           "seconds": round(dt, 2), "max_rss_gb": _max_rss_gb(0), "box": box_info()}
+           "seconds": round(dt, 2), "max_rss_gb": hwm, "box": box_info()}
     if a.cpu_ranks > 1:
         try:
             out["per_rank"] = cpu_oracle_ranks(a.model, a.cpu_ranks, min(2, a.cpu_ranks), a.ep, 1)
@@ -557,6 +573,9 @@ def run_plex(a):
         e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
         e2e = {"s": e2e_s, "h2d": info.slab_bytes, "d2h": info.slab_bytes + 16 * info.n_segments}
 
+    executor_desc = (("plex_group_transition (library residency map decides every switch; modes "
+                      f"seen: {sorted(modes_seen)})") if group is not None else "direct calls")
+
     # ---- diagnostic (N>1, outside the timed region): the fused push split into its
     # local (HBM-only) and remote (NVLink) items, timed as two launches so that each
     # gets its own roofline fraction (PLEX_CTX_SPLIT_PUSH)
@@ -596,8 +615,11 @@ def run_plex(a):
     # conservative independent-param state (reading D2').
     variant = None
     if world == 1 and mode == "swap" and not a.no_derived_variant:
+        import gc
+        group.close()
         del group, jobs, job_a, job_b
         group = job_a = job_b = jobs = None
+        gc.collect()
         torch.cuda.empty_cache()
         plan_el = mgr.plan(manifest(a.model), head_dim=shape.head_dim, tp=tp, dp=dp, ep=a.ep, rank_map=rank_map,
                            elide_param=True)
@@ -642,7 +664,9 @@ def run_plex(a):
                    "derive_ms_per_step": round(vst["derive"]["ms"] / vsteps, 3),
                    "note": ("value = state bytes switched (both jobs' full 4-kind state) / step time; the bf16 "
                             "params (1/7 of the bytes) are re-derived on the device, not moved")}
+        vgroup.close()
         del vgroup, vjobs, va, vb
+        gc.collect()
         torch.cuda.empty_cache()
 
     S_total = allsum(float(2 * info.payload_bytes))      # offloaded + onloaded state per switch
@@ -748,8 +772,7 @@ def run_plex(a):
                        "l2": "inputs (state) larger than L2 (126 MB); no flush needed",
                        "plan_ms": round(plan_s * 1e3, 1), "setup_s": round(setup_s, 1),
                        "sync_transport": "nccl" if a.sync_nccl else "nvlink-push",
-                       "executor": ("plex_group_transition (library residency map decides every switch; modes "
-                                    f"seen: {sorted(modes_seen)})") if group is not None else "direct calls",
+                       "executor": executor_desc,
                        "rank_map": ["tp_fast (g = dp*TP + tp)", "dp_fast (g = tp*DP + dp)"][plan.stats().rank_map]},
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
                          "unit": "GB/s", "frac": frac(achieved, peak_hbm), "traffic": traffic,

@@ -334,7 +334,18 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
             c = Cks();
         }
     }
-    if (tid == 0) bulk_wait_all();                 // every bulk store complete before exit
+    if (tid == 0) {
+        bulk_wait_all();                           // every bulk store complete before exit
+        // Self-resetting claim counter (no memset node before each launch): this
+        // CTA's producer made its last claim before it signalled kMetaDone, so
+        // once every CTA has checked in, no claim is outstanding.  ctr[8] counts
+        // finished CTAs; the last one zeroes both for the next launch.
+        __threadfence();
+        if (atomicAdd(ctr + 8, 1u) == gridDim.x - 1) {
+            atomicExch(ctr, 0u);
+            atomicExch(ctr + 8, 0u);
+        }
+    }
 }
 
 __global__ void verify_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
@@ -577,8 +588,6 @@ static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const 
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < 64) attr[dev] = true;
     }
-    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
-    if (e != cudaSuccess) return e;
     const uint32_t cap = (uint32_t)g_num_sms * PackCfg::kCtasPerSm;
     const uint32_t grid = n_items < cap ? n_items : cap;
     // Claim order: item (c * perm) mod n with perm ~ n/3 coprime to n, so the

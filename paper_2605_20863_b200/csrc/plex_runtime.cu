@@ -171,7 +171,7 @@ struct plex_ctx_s {
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
     int* h_flag = nullptr;
     int* d_flag = nullptr;
-    unsigned int* d_ctr = nullptr;      // pack/unpack work counters, one per pipe
+    unsigned int* d_ctr = nullptr;      // pack/unpack work counters, one per pipe (+8: finished CTAs)
     // small device scratch for NCCL barriers and handle exchange
     uint8_t* d_scratch = nullptr;
     uint8_t* h_scratch = nullptr;
@@ -987,6 +987,12 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
         cudaMalloc(&c->d_scratch, 2 * c->scratch_bytes) != cudaSuccess ||
         cudaHostAlloc(&c->h_scratch, 2 * c->scratch_bytes, cudaHostAllocDefault) != cudaSuccess) {
         set_error("ctx scratch allocation failed");
+        return fail(PLEX_E_CUDA);
+    }
+    // pack/unpack claim counters [0, 8) and their finished-CTA counters [8, 16):
+    // zero once here, every launch leaves them zeroed (pack_kernel)
+    if (cudaMemset(c->d_ctr, 0, 64) != cudaSuccess) {
+        set_error("ctx counter init failed");
         return fail(PLEX_E_CUDA);
     }
     if (nccl_id && world > 1) {

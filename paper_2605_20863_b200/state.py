@@ -753,17 +753,26 @@ class Group:
         self.hbm_budget = hbm_budget
         self.jobs: Dict[int, Job] = {}
         self._storage_of: Dict[int, Optional[int]] = {}
-        self._cb = L.STORAGE_FN(self._storage)          # kept alive with the group
+        import weakref
+        me = weakref.ref(self)                          # no group <-> callback reference cycle
+
+        def cb(user, jid, acquire, state, n_state):
+            g = me()
+            return 2 if g is None else g._storage(user, jid, acquire, state, n_state)
+        self._cb = L.STORAGE_FN(cb)                     # kept alive with the group
         self._cb_error: Optional[BaseException] = None
         h = C.c_void_p()
         check(lib.plex_group_create(mgr.h, self._cb, None, C.byref(h)))
         self.h = h
 
     def close(self):
+        """Destroy the library group; the jobs (and their device memory) are
+        released from the group's bookkeeping."""
         h = getattr(self, "h", None)
         if h is not None and h.value and lib is not None:
             lib.plex_group_destroy(h)
             self.h = None
+        self.jobs = {}
 
     def __del__(self):
         self.close()

@@ -131,6 +131,49 @@ def main():
                 print(f"[rank {rank}] sync after swap mismatch {name} iter {it}", flush=True)
                 bad += 1
     del arena, ja, jb
+    # a1 through the library's group executor with the real collectives: three
+    # jobs (one with replicated ZeRO-2 params) time-slicing the group; the op
+    # lists must equal the oracle's transition_ops, every sync the oracle's
+    # weight_sync, every restored state the oracle's shards
+    specs = [("mid", 2 if world % 2 == 0 else 1, 1, False, 51), ("mid-moe", 2 if world % 2 == 0 else 1, world, False, 52),
+             ("toy", 1, 1, True, 53)]
+    group = P.Group(mgr)
+    gjobs, garenas, gwant = [], [], []
+    for model, tp, ep, rep, seed in specs:
+        hd = MODELS[model].head_dim
+        plan = mgr.plan(manifest(model), head_dim=hd, tp=tp, dp=world // tp, ep=ep, replica_param=rep,
+                        tile_bytes=2048)
+        job = P.Job(mgr, plan, seed=seed).alloc().init_synthetic(special_bits=3)
+        job.suspend()                                        # every job starts HOST-resident
+        group.add(job)
+        full = full_state(model, seed=seed, special_bits=3)
+        gjobs.append(job)
+        garenas.append(mgr.arena(plan))
+        gwant.append((full, O.weight_sync(master_shards(full, world, O.fsdp_rows), tp, world // tp, ep, 0, hd)[rank]))
+    resident = None
+    for j in (0, 1, 2, 0, 2, 1, 1):
+        res = group.transition(gjobs[j])
+        if res["ops"] != O.transition_ops(resident, j):
+            print(f"[rank {rank}] group ops {res['ops']} != oracle {O.transition_ops(resident, j)}", flush=True)
+            bad += 1
+        resident = j
+        garenas[j].fill_(0xCD)
+        res = group.transition(gjobs[j], sync=garenas[j])        # collective sync through the executor
+        if res["ops"] != [(O.OP_SYNC, j)]:
+            bad += 1
+        full, want = gwant[j]
+        for name, v in P.StateManager.rollout_views(gjobs[j].plan, rank, garenas[j]).items():
+            if not np.array_equal(bits_np(v), want[name]):
+                print(f"[rank {rank}] group sync mismatch job {j} {name}", flush=True)
+                bad += 1
+        osh = fsdp_shards(full, world, rank, O.fsdp_rows)
+        for (k, kd), v in gjobs[j].shards.items():
+            w = full[(k, kd)] if (kd == 0 and specs[j][3]) else osh[(k, kd)]
+            if not np.array_equal(bits_np(v), w):
+                print(f"[rank {rank}] group restore mismatch job {j} {k}/{kd}", flush=True)
+                bad += 1
+    group.close()
+    del gjobs, garenas
     t = torch.tensor([bad], device=f"cuda:{local}")
     dist.all_reduce(t)
     mgr.close()

@@ -52,3 +52,10 @@ def test_cuda_arm_json_line(extra):
     assert d["config"]["workload"] and d["config"]["switch_mode"] == ("swap" if extra else "duplex")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # every switch was decided and executed by the library's group executor (a1)
+    assert "plex_group_transition" in d["config"]["executor"]
+    assert d["config"]["executor"].endswith(("['swap'])", "['duplex'])"))
+    if extra:                                 # the labelled derived-param (NEXT-2 elision) sub-line
+        dv = d["derived_param"]
+        assert dv["elided"] is True and dv["value"] > 0
+        assert dv["host_link_bytes_per_step"] < dv["state_bytes_switched_per_step"]

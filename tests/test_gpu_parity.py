@@ -271,7 +271,8 @@ def test_multiplex_emulated():
             assert res["ops"] == O.transition_ops(j, j, True) and res["mode"] == "none"
         outs.append([{k: bits_np(v) for k, v in P.StateManager.rollout_views(plans[j], g, arenas[g]).items()}
                      for g in range(W)])
-    assert modes[:W] == ["load"] * W and set(modes[W:]) == {"duplex"}
+    want_modes = ["load"] + ["none" if a == b else "duplex" for a, b in zip(schedule, schedule[1:])]
+    assert modes == [m for m in want_modes for _ in range(W)]
     # oracle replay
     ojobs = []
     for mo, sd, (tp, dp, ep) in zip(models, seeds, layouts):

@@ -85,9 +85,19 @@ class Ctx:
                     f.write(json.dumps(line) + "\n")
 
 
-def timed(c: Ctx, fn, steps: int, warmup: int):
+def timed(c: Ctx, fn, steps: int, warmup: int, min_s: float = 1.5):
+    """CUDA-event time per call (max over ranks) and the clocks sampled during
+    it.  Short calls (a 7 ms sync) are repeated until the timed region lasts
+    >= min_s, so nvidia-smi (200 ms period) records the clocks under load."""
     for _ in range(warmup):
         fn()
+    if min_s > 0 and steps > 0:
+        c.barrier()
+        t0 = time.perf_counter()
+        fn()
+        c.barrier()
+        dt = time.perf_counter() - t0
+        steps = int(c.allmax(float(max(steps, min(2000, int(min_s / max(dt, 1e-5)) + 1)))))
     clocks = Clocks(c.local)
     c.barrier()
     clocks.start()
@@ -98,7 +108,8 @@ def timed(c: Ctx, fn, steps: int, warmup: int):
     e1.record()
     c.barrier()
     clk = clocks.stop()
-    return c.allmax(e0.elapsed_time(e1) / steps), clk
+    clk["timed_calls"] = steps
+    return c.allmax(e0.elapsed_time(e1) / max(1, steps)), clk
 
 
 def scen_duplex(a, c: Ctx):
@@ -520,7 +531,7 @@ def scen_multiplex(a, c: Ctx):
         jobs[resident].suspend()
         res["r"] = None
 
-    ms, clk = timed(c, run_trace, 1, 0)
+    ms, clk = timed(c, run_trace, 1, 0, min_s=0)
     switches = len(schedule) - 1
     c.emit({"scenario": "multiplex", "jobs": models, "n_gpus": c.world, "rounds": a.rounds,
             "visits": len(schedule), "switches": switches, "duplex": a.duplex, "duplex_switches": dup_used["n"],
