@@ -47,7 +47,8 @@ EXPORTS = [
     "plex_weight_sync_from_slab", "plex_weight_sync_rank_from_slab",
     "plex_plan_param_arena", "plex_param_allgather", "plex_param_allgather_rank",
     "plex_slab_checkpoint", "plex_slab_checkpoint_start", "plex_ckpt_wait", "plex_slab_restore", "plex_state_swap",
-    "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne",
+    "plex_synth_fill", "plex_synth_mutate", "plex_checksum", "plex_cast_rne", "plex_diag_pack",
+    "plex_diag_pack_variant",
     "plex_transition_decide", "plex_plan_group", "plex_group_create", "plex_group_destroy", "plex_group_add_job",
     "plex_group_resident", "plex_group_job_slab", "plex_group_transition",
 ]
@@ -179,6 +180,8 @@ def _load() -> C.CDLL:
         "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
         "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),
         "plex_cast_rne": (C.c_int, [VP, VP, U64, VP]),
+        "plex_diag_pack": (C.c_int, [VP, VP, P(VP), I32, I32, I32, VP]),
+        "plex_diag_pack_variant": (C.c_int, [I32]),
         "plex_transition_decide": (C.c_int, [I64, I64, I32, P(Transition)]),
         "plex_plan_group": (C.c_int, [VP, I32, C.c_char_p, I32, P(I32), P(I32), P(I32)]),
         "plex_group_create": (C.c_int, [VP, STORAGE_FN, VP, P(VP)]),

@@ -132,6 +132,25 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
                  "r"(bytes)
                  : "memory");
 }
+// L2 eviction-priority variants (diagnostic variant 1 of the pack kernel):
+// the same bulk copies carrying an L2::evict_first cache policy.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_load_hint(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -207,7 +226,7 @@ using PackCfg = TmaCfg<3, 32, 4, 2>;     // 2 CTAs/SM x 3 stages x 32 KiB (see p
 // latency hides behind the chunks already in flight) and tags every staged
 // chunk with its item geometry.  CTAs that run faster simply take more items,
 // which removes the static round-robin tail.
-template <bool kPack, class Cfg>
+template <bool kPack, class Cfg, int kHint = 0>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     pack_kernel(const PackItem* __restrict__ items, uint32_t n_items, const SegDev* __restrict__ segs,
                 const uint64_t* __restrict__ ptrs, uint8_t* __restrict__ staging, uint64_t bucket_lo,
@@ -234,6 +253,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
     if (tid >= kConsumers) {
         // ---------------- producer: claim items, TMA-load their chunks ----------------
         if (tid != kConsumers) return;
+        const uint64_t pol = kHint ? policy_evict_first() : 0;
         uint32_t q = 0;
         // claim c -> item (c * perm) mod n (perm = 1: slab order; perm coprime
         // to n spreads concurrently processed items across the bucket)
@@ -256,7 +276,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
                 const uint32_t nb = chunk_bulk(g, co, kChunk);
                 if (nb) {
                     mbar_arrive_tx(&full[st], nb);
-                    bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
+                    if (kHint) bulk_load_hint(smem + (size_t)st * kChunk, src + co, nb, &full[st], pol);
+                    else bulk_load(smem + (size_t)st * kChunk, src + co, nb, &full[st]);
                 } else {
                     mbar_arrive(&full[st]);
                 }
@@ -271,6 +292,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         return;
     }
     // ---------------- consumers: checksum + TMA stores ----------------
+    const uint64_t spol = (kHint && tid == 0) ? policy_evict_first() : 0;
     Cks c;
     for (uint32_t q = 0;; ++q) {
         const int st = (int)(q % kStages);
@@ -286,7 +308,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         const uint32_t cend = g.len - co < kChunk ? g.len : co + kChunk;
         const uint32_t dend = g.data < cend ? g.data : cend;            // data end within chunk
         if (tid == 0 && nb) {
-            bulk_store(dst + co, sm, nb);                               // write back while we checksum
+            if (kHint) bulk_store_hint(dst + co, sm, nb, spol);
+            else bulk_store(dst + co, sm, nb);                          // write back while we checksum
             bulk_commit();
         }
         // checksum of the bulk part, read back from shared memory
@@ -574,8 +597,9 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 
 // ---- launchers ----------------------------------------------------------------
 static int g_num_sms = 0;
+static int g_pack_variant = 0;          // diagnostic only (plex_diag_pack_variant)
 
-template <bool kPack>
+template <bool kPack, int kHint>
 static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                                  uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
                                  cudaStream_t s) {
@@ -583,7 +607,7 @@ static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const 
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, PackCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(pack_kernel<kPack, PackCfg, kHint>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)PackCfg::kSmem);
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < 64) attr[dev] = true;
@@ -601,8 +625,8 @@ static cudaError_t launch_pack_t(const PackItem* items, uint32_t n_items, const 
         while (gcd(m, n_items) != 1) m += 2;
         perm = m;
     }
-    pack_kernel<kPack, PackCfg><<<grid, PackCfg::kThreads, PackCfg::kSmem, s>>>(items, n_items, segs, ptrs, staging,
-                                                                                bucket_lo, cks, ctr, perm);
+    pack_kernel<kPack, PackCfg, kHint><<<grid, PackCfg::kThreads, PackCfg::kSmem, s>>>(items, n_items, segs, ptrs,
+                                                                                       staging, bucket_lo, cks, ctr, perm);
     return cudaGetLastError();
 }
 
@@ -616,9 +640,14 @@ cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, cons
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
     }
-    return pack ? launch_pack_t<true>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s)
-                : launch_pack_t<false>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s);
+    if (g_pack_variant == 1)
+        return pack ? launch_pack_t<true, 1>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s)
+                    : launch_pack_t<false, 1>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s);
+    return pack ? launch_pack_t<true, 0>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s)
+                : launch_pack_t<false, 0>(items, n_items, segs, ptrs, staging, bucket_lo, cks, ctr, s);
 }
+
+void set_pack_variant(int v) { g_pack_variant = v; }
 
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
                           cudaStream_t s) {

@@ -35,6 +35,7 @@ namespace plex {
 cudaError_t launch_pack(bool pack, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                         uint8_t* staging, uint64_t bucket_lo, unsigned long long* cks, unsigned int* ctr,
                         cudaStream_t s);
+void set_pack_variant(int v);
 cudaError_t launch_verify(const unsigned long long* got, const unsigned long long* want, uint32_t n, int* bad,
                           cudaStream_t s);
 cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
@@ -2358,6 +2359,32 @@ plex_status plex_synth_mutate(void* buf, int32_t kind, uint64_t job_seed, uint64
     if ((!buf && count) || !key || kind < 0 || kind >= PLEX_NUM_KINDS) { set_error("bad mutate arguments"); return PLEX_E_INVAL; }
     const uint64_t base = stream_base(job_seed, key, kind) ^ ((step + 1) * 0xA24BAED4963EE407ull);
     CK(launch_mutate(buf, kind_esize(kind), base, index_base, count, reinterpret_cast<cudaStream_t>(stream)));
+    return PLEX_OK;
+}
+
+// ---- diagnostics (kernel measurement, not the method) ----------------------------------
+plex_status plex_diag_pack(plex_ctx_t c, plex_plan_t plan, const void* const* state, int32_t n_state, int32_t bucket,
+                           int32_t pack, void* stream) {
+    plex_status st = check_common(c, plan);
+    if (st) return st;
+    const Plan& p = plan->p;
+    const RankPlan& R = p.ranks[c->rank];
+    if (bucket < 0 || bucket >= n_buckets(p, R)) { set_error("bucket %d out of range", bucket); return PLEX_E_INVAL; }
+    DeviceGuard g(c->device);
+    DevPlan* d;
+    if ((st = fill_state_ptrs(c, p, state, n_state)) || (st = get_devplan(c, p, &d))) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, sizeof(uint64_t) * PLEX_NUM_KINDS * p.tensors.size(),
+                       cudaMemcpyHostToDevice, s));
+    const uint64_t i0 = R.bucket_item_start[bucket], i1 = R.bucket_item_start[bucket + 1];
+    CK(launch_pack(pack != 0, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, c->staging,
+                   (uint64_t)bucket * p.bucket, pack ? d->cks : d->cks_in, c->d_ctr, s));
+    return PLEX_OK;
+}
+
+plex_status plex_diag_pack_variant(int32_t variant) {
+    if (variant < 0 || variant > 1) { set_error("pack variant %d unknown", variant); return PLEX_E_INVAL; }
+    set_pack_variant(variant);
     return PLEX_OK;
 }
 

@@ -517,6 +517,11 @@ class StateManager:
             out[name] = arena[off:off + 2 * n].view(torch.bfloat16).view(shape)
         return out
 
+    def diag_pack(self, plan: Plan, shards, bucket: int, pack: bool = True, stream=None) -> None:
+        """Diagnostic: one K1/K2 launch over one bucket, no copies (plex_diag_pack)."""
+        arr, n = self._state_ptrs(plan, shards, self.rank)
+        check(lib.plex_diag_pack(self.h, plan.h, arr, n, bucket, 1 if pack else 0, _stream_ptr(stream)))
+
     def enable_carry(self, plan: Plan) -> None:
         """Give the ctx carry staging (4 bucket slots) if `plan` carries buckets."""
         if not plan.carry():
@@ -582,6 +587,11 @@ def checksum(t: torch.Tensor, index_base: int = 0, out: Optional[torch.Tensor] =
     check(lib.plex_checksum(t.data_ptr() if t.numel() else None, t.element_size(), index_base, t.numel(),
                             out.data_ptr(), _stream_ptr(stream)))
     return out
+
+
+def diag_pack_variant(v: int) -> None:
+    """Diagnostic: K1/K2 build for later launches (0 default, 1 L2::evict_first)."""
+    check(lib.plex_diag_pack_variant(v))
 
 
 def cast_rne(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:

@@ -120,3 +120,32 @@ def sample_keys(man: Sequence[Tuple[str, Tuple[int, ...]]], n: int, seed: int = 
     sizes = [int(np.prod(s)) for _, s in man]
     pick.add(int(np.argmax(sizes)))
     return [keys[i] for i in sorted(pick)]
+
+
+def tensor_checksums(seed: int, man, kinds=(0, 1, 2, 3), special_bits: int = 0,
+                     threads: int = 0) -> Dict[Tuple[str, int], Tuple[int, int]]:
+    """The oracle's (S1, S2) of every logical (key, kind) tensor of the initial
+    synthetic state, chunked (R14 additivity) over the host's cores."""
+    tasks = []
+    for k, s in man:
+        n = 1
+        for d in s:
+            n *= d
+        for kd in kinds:
+            for o in range(0, max(n, 1), CHUNK):
+                tasks.append((k, kd, o, min(CHUNK, n - o)))
+
+    def run(t):
+        k, kd, o, c = t
+        if c <= 0:
+            return k, kd, 0, 0
+        a, b = O.checksum(gen_range(seed, k, kd, o, c, special_bits if kd else 0), o)
+        return k, kd, a, b
+
+    out: Dict[Tuple[str, int], List[int]] = {}
+    with ThreadPoolExecutor(threads or workers()) as ex:
+        for k, kd, a, b in ex.map(run, tasks):
+            acc = out.setdefault((k, kd), [0, 0])
+            acc[0] = (acc[0] + a) & M64
+            acc[1] = (acc[1] + b) & M64
+    return {kk: (v[0], v[1]) for kk, v in out.items()}

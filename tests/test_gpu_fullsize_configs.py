@@ -25,7 +25,7 @@ import pytest
 import torch
 
 from oracle import plex_oracle as O
-from plexgen import MODELS, gen_range, manifest
+from plexgen import MODELS, gen_range, manifest, mutation_bits
 
 import _oracle_pool as OP
 
@@ -52,28 +52,32 @@ def _free(*objs):
     torch.cuda.empty_cache()
 
 
-def test_m2_qwen7b_fsdp8_to_tp2dp4_every_rollout_tensor():
-    _need(150)
+def _emulated_sync_every_tensor(model, seed, W, tp, dp, ep, sample_keys, want_rmap=None):
+    """All W source ranks' pushes emulated on one B200, one source rank at a
+    time (its master shard generated, pushed into all W arenas, freed), so only
+    the W arenas + one master shard are resident.  Checks: ledger == O.ledger;
+    (S1, S2) of EVERY rollout tensor of EVERY rank == the oracle's gather -> RNE
+    -> slice/fuse (c1.3); element by element for ``sample_keys`` (each list is
+    one set of keys fused together, e.g. q/k/v) on every rank."""
     torch.cuda.set_device(0)
-    model, seed, W, tp, dp = "qwen2.5-7b", 1, 8, 2, 4
     man = manifest(model)
     hd = MODELS[model].head_dim
-    plan = P.Plan(man, head_dim=hd, world=W, tp=tp, dp=dp, rank_map=L.RANKMAP_AUTO, bucket_bytes=1 << 20)
+    plan = P.Plan(man, head_dim=hd, world=W, tp=tp, dp=dp, ep=ep, rank_map=L.RANKMAP_AUTO, bucket_bytes=1 << 20)
     rmap = plan.stats().rank_map
-    assert rmap == L.RANKMAP_DP_FAST                         # R10: the lighter ledger (5.99 vs 7.33 GB)
-    assert np.array_equal(plan.ledger(), O.ledger(man, W, tp, dp, 1, rmap))
-    mgrs = [P.StateManager(device=0, rank=r, world=W, bucket_bytes=1 << 20, bootstrap=False) for r in range(W)]
-    masters = [P.Job(mgrs[r], plan, seed=seed, rank=r, slab=False).alloc(kinds=(1,)).init_synthetic().masters()
-               for r in range(W)]
+    if want_rmap is not None:
+        assert rmap == want_rmap
+    assert np.array_equal(plan.ledger(), O.ledger(man, W, tp, dp, ep, rmap))
+    mgr = P.StateManager(device=0, rank=0, world=W, bucket_bytes=1 << 20, bootstrap=False)
     arenas = [torch.full((plan.rank_info(g).dst_arena_bytes,), 0xEE, dtype=torch.uint8, device="cuda")
               for g in range(W)]
-    for r in range(W):                                       # every source rank's push into all 8 arenas
-        mgrs[r].sync_rank(plan, r, masters[r], arenas)
-    torch.cuda.synchronize()
-    del masters
-    gc.collect()
-    torch.cuda.empty_cache()
-    want = OP.rollout_checksums(seed, man, tp, dp, 1, rmap, hd)
+    for r in range(W):                                       # source rank r's push into all W arenas
+        job = P.Job(mgr, plan, seed=seed, rank=r, slab=False).alloc(kinds=(1,)).init_synthetic()
+        mgr.sync_rank(plan, r, job.masters(), arenas)
+        torch.cuda.synchronize()
+        del job
+        gc.collect()
+        torch.cuda.empty_cache()
+    want = OP.rollout_checksums(seed, man, tp, dp, ep, rmap, hd)
     views = [P.StateManager.rollout_views(plan, g, arenas[g]) for g in range(W)]
     assert sorted(want) == sorted((g, n) for g in range(W) for n in views[g])
     names = [(g, n) for g in range(W) for n in views[g]]
@@ -83,23 +87,53 @@ def test_m2_qwen7b_fsdp8_to_tp2dp4_every_rollout_tensor():
     got = ck.cpu().numpy().view(np.uint64)
     bad = [names[i] for i in range(len(names)) if tuple(int(v) for v in got[i]) != want[names[i]]]
     assert not bad, bad[:10]
-    # element by element on sampled tensors, every rank
     shapes = dict(man)
-    for key in ("model.layers.0.self_attn.q_proj.weight", "model.layers.27.mlp.down_proj.weight",
-                "lm_head.weight", "model.layers.13.self_attn.o_proj.weight"):
-        full = {key: gen_range(seed, key, 1, 0, int(np.prod(shapes[key]))).reshape(shapes[key])}
-        if ".q_proj." in key:
-            for n in "kv":
-                k2 = key.replace(".q_proj.", f".{n}_proj.")
-                full[k2] = gen_range(seed, k2, 1, 0, int(np.prod(shapes[k2]))).reshape(shapes[k2])
+    n_cmp = 0
+    for keys in sample_keys:                                 # element by element, every rank
+        full = {k: gen_range(seed, k, 1, 0, int(np.prod(shapes[k]))).reshape(shapes[k]) for k in keys}
         cast = {k: O.rne_bf16(v) for k, v in full.items()}
         for g in range(W):
-            for name, x in O.rollout_tensors(cast, tp, dp, 1, g, rmap, hd).items():
+            for name, x in O.rollout_tensors(cast, tp, dp, ep, g, rmap, hd).items():
                 assert np.array_equal(bits_np(views[g][name]), x), (g, name)
+                n_cmp += 1
+    assert n_cmp > 0
     del views, arenas
-    for m in mgrs:
-        m.close()
+    mgr.close()
     _free()
+    return len(names)
+
+
+def test_m2_qwen7b_fsdp8_to_tp2dp4_every_rollout_tensor():
+    """configs[1]: Qwen2.5-7B FSDP-8 -> TP-2 x DP-4 with the bench's AUTO rank
+    map (R10 picks DP_FAST: 5.99 vs 7.33 GB over the busiest link)."""
+    _need(150)
+    qkv = [f"model.layers.0.self_attn.{n}_proj.weight" for n in "qkv"]
+    _emulated_sync_every_tensor("qwen2.5-7b", 1, 8, 2, 4, 1,
+                                [qkv, ["model.layers.27.mlp.down_proj.weight"], ["lm_head.weight"],
+                                 ["model.layers.13.self_attn.o_proj.weight"]], want_rmap=L.RANKMAP_DP_FAST)
+
+
+def test_m3_qwen32b_fsdp8_to_tp4dp2_every_rollout_tensor():
+    """configs[2] sync: Qwen2.5-32B FSDP-8 -> TP-4 x DP-2 (Table 1 32B row,
+    PAPER.md:615): 8 arenas (131 GB) + one 16.4 GB master shard at a time."""
+    _need(150)
+    qkv = [f"model.layers.7.self_attn.{n}_proj.weight" for n in "qkv"]
+    gu = [f"model.layers.40.mlp.{n}_proj.weight" for n in ("gate", "up")]
+    _emulated_sync_every_tensor("qwen2.5-32b", 2, 8, 4, 2, 1,
+                                [qkv, gu, ["model.layers.63.mlp.down_proj.weight"],
+                                 ["model.layers.31.self_attn.o_proj.weight"]])
+
+
+def test_m4_qwen3_30b_a3b_fsdp8_to_tp2dp4_ep8_every_rollout_tensor():
+    """configs[3] sync: Qwen3-30B-A3B FSDP-8 -> attention TP-2 x DP-4 + experts
+    EP-8 (Table 1): every rollout tensor (w13 / w2 expert stacks
+    included) against the oracle; attention, router and q/k norms element by
+    element."""
+    _need(150)
+    qkv = [f"model.layers.11.self_attn.{n}_proj.weight" for n in "qkv"]
+    _emulated_sync_every_tensor("qwen3-30b-a3b", 3, 8, 2, 4, 8,
+                                [qkv, ["model.layers.47.self_attn.o_proj.weight"],
+                                 ["model.layers.5.mlp.gate.weight"], ["model.layers.5.self_attn.q_norm.weight"]])
 
 
 def test_m1m2_qwen7b_fsdp1_every_slab_byte():
@@ -177,3 +211,126 @@ def test_m3_qwen32b_optimizer_only_roundtrip_k1():
     _need(150)
     n = _shard_roundtrip("qwen2.5-32b", 2, 8, 0, L.SLAB_KIND_MAJOR, L.KINDMASK_OPTIM, 64)
     assert n == 3 * len(manifest("qwen2.5-32b"))
+
+
+def test_m5_multiplex_trace_fullsize():
+    """configs[4] at full size: 4 jobs shaped Qwen2.5-0.5B / 1.5B / 3B / 7B
+    (seeds 0..3) time-slice one GPU group for R = 5
+    round-robin rounds (20 visits, 19 switches).  FSDP-4 emulated on one B200
+    (one plex_group per rank); rollout TP-1 x DP-4 for 0.5B, TP-2 x DP-2 for the
+    rest.  Every switch is decided and executed by the library's residency
+    authority (op lists == O.transition_ops), every visit mutates
+    the state (o10 reading M1) and syncs it.  Checks:
+      * per visit, element by element on every rank: the fused q/k/v, o_proj
+        and input norm of one layer against the oracle's rollout of the
+        mutated masters (init XOR every mask so far, the multiplex_replay
+        closed form pinned in tests/test_oracle_multiplex.py);
+      * at the end, EVERY (key, kind) of every job: each job is brought back
+        through its group, its masks are XOR-ed out again, and the R14
+        checksum (additive over the 4 shards) equals the oracle's checksum of
+        the regenerated initial state -- any byte the 19 switches lost or
+        moved fails it."""
+    _need(150)
+    torch.cuda.set_device(0)
+    W = 4
+    models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
+    seeds = [0, 1, 2, 3]
+    rounds = 5
+    schedule = list(range(4)) * rounds
+    mgrs = [P.StateManager(device=0, rank=r, world=W, bucket_bytes=256 << 20, n_slots=2, bootstrap=False)
+            for r in range(W)]
+    plans, jobs = [], []
+    for mo in models:
+        tp = 1 if mo == "qwen2.5-0.5b" else 2
+        plans.append(P.Plan(manifest(mo), head_dim=MODELS[mo].head_dim, world=W, tp=tp, dp=W // tp,
+                            bucket_bytes=256 << 20))
+    groups = [P.Group(mgrs[r]) for r in range(W)]
+    for j, mo in enumerate(models):                        # every job starts HOST-resident
+        row = []
+        for r in range(W):
+            jb = P.Job(mgrs[r], plans[j], seed=seeds[j], rank=r).alloc().init_synthetic()
+            jb.suspend()
+            row.append(jb)
+        jobs.append(row)
+        torch.cuda.synchronize()
+        _free()
+        for r in range(W):
+            assert groups[r].add(jobs[j][r]) == j
+    resident, steps, modes = None, [0] * 4, []
+
+    def mutate(j, step):
+        for r in range(W):
+            for t, (key, shape) in enumerate(plans[j].manifest):
+                a, _ = plans[j].shard_rows(r, t)
+                re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+                for kd in range(4):
+                    P.synth_mutate(jobs[j][r].shards[(key, kd)], kd, seeds[j], step, key, a * re_)
+
+    rng = np.random.default_rng(5)
+    for v, j in enumerate(schedule):
+        want_ops = O.transition_ops(resident, j)
+        for r in range(W):
+            res = groups[r].transition(jobs[j][r])
+            assert res["ops"] == want_ops, (v, j, r, res)
+            assert res["resident_after"] == j
+            modes.append(res["mode"])
+        resident = j
+        mutate(j, steps[j])
+        steps[j] += 1
+        arenas = [mgrs[0].arena(plans[j], g) for g in range(W)]
+        for r in range(W):
+            res = groups[r].transition(jobs[j][r], sync=arenas)
+            assert res["ops"] == O.transition_ops(j, j, True) and res["mode"] == "none"
+        torch.cuda.synchronize()
+        # oracle: one layer's q/k/v + o_proj + input norm after every mask so far
+        mo = models[j]
+        man = dict(manifest(mo))
+        layer = int(rng.integers(MODELS[mo].layers))
+        keys = [f"model.layers.{layer}.self_attn.{n}_proj.weight" for n in "qkvo"] + \
+            [f"model.layers.{layer}.input_layernorm.weight"]
+        cast = {}
+        for k in keys:
+            n = int(np.prod(man[k]))
+            x = gen_range(seeds[j], k, 1, 0, n)
+            idx = np.arange(n, dtype=np.uint64)
+            for s in range(steps[j]):
+                x = x ^ mutation_bits(seeds[j], s, k, 1, idx)
+            cast[k] = O.rne_bf16(x).reshape(man[k])
+        tp = plans[j].stats().tp
+        for g in range(W):
+            views = P.StateManager.rollout_views(plans[j], g, arenas[g])
+            for name, x in O.rollout_tensors(cast, tp, W // tp, 1, g, L.RANKMAP_TP_FAST,
+                                             MODELS[mo].head_dim).items():
+                assert np.array_equal(bits_np(views[name]), x), (v, j, g, name)
+        del arenas, views
+        _free()
+    want_modes = ["load"] + ["none" if a == b else ("duplex", "sequential") for a, b in zip(schedule, schedule[1:])]
+    for i, m in enumerate(modes):
+        w = want_modes[i // W]
+        assert m == w if isinstance(w, str) else m in w, (i, m, w)
+    # every byte of every job: undo the masks, R14 per (key, kind) == oracle of the initial state
+    for j, mo in enumerate(models):
+        for r in range(W):
+            groups[r].transition(jobs[j][r])
+        for s in range(steps[j]):
+            mutate(j, s)                                   # XOR is an involution
+        man = manifest(mo)
+        names = [(k, kd) for k, _ in man for kd in range(4)]
+        ck = torch.zeros((W, len(names), 2), dtype=torch.int64, device="cuda")
+        for r in range(W):
+            for i, (k, kd) in enumerate(names):
+                t = plans[j].index[k]
+                a, _ = plans[j].shard_rows(r, t)
+                shape = dict(man)[k]
+                re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+                P.checksum(jobs[j][r].shards[(k, kd)], a * re_, out=ck[r, i])
+        got = ck.cpu().numpy().view(np.uint64).astype(object).sum(axis=0)
+        want = OP.tensor_checksums(seeds[j], man)
+        bad = [names[i] for i in range(len(names))
+               if (int(got[i][0]) & OP.M64, int(got[i][1]) & OP.M64) != want[names[i]]]
+        assert not bad, (mo, bad[:10])
+    for g in groups:
+        g.close()
+    for m in mgrs:
+        m.close()
+    _free()

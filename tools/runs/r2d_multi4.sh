@@ -5,7 +5,7 @@ set -x
 mkdir -p gpurun_out
 nvidia-smi topo -m > gpurun_out/r2d_topo.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2d_build.log 2>&1
-timeout 1500 python -m pytest tests/test_gpu_multi.py -q -m gpu -k "collective" > gpurun_out/r2d_pytest_multi.log 2>&1
+timeout 2400 python -m pytest tests/test_gpu_multi.py -v -m gpu --durations=0 > gpurun_out/r2d_pytest_multi.log 2>&1
 echo pytest_rc=$?
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 timeout 900 $TR --nproc-per-node 2 --master-port 29511 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/r2d_bench_n2.log 2>&1
