@@ -723,6 +723,9 @@ def run_plex(a):
         t_hbm = allmax(hbm_b / (peak_hbm * 1e9) * 1e3)
         t_nvl = allmax(float(max(info.send_bytes, info.recv_bytes)) / 770e9 * 1e3)
         if not st["nccl"]["launches"]:
+            # the single-resource "push" row (all 6 B/element over HBM) does not
+            # describe a kernel that also stores over NVLink: push_fused replaces it
+            rl.pop("push", None)
             t_push = allmax(st["push"]["ms"] / a.steps)
             bound = "nvlink" if t_nvl >= t_hbm else "hbm"
             rl["push_fused"] = {"bound": bound, "lower_bound_ms": round(max(t_hbm, t_nvl), 3),
