@@ -44,6 +44,9 @@ def raw(rep):
                 u = units[i]
                 if m.startswith("dram__bytes"):
                     f *= UNIT.get(u, 1)
+                elif m == "gpu__time_duration.sum":            # always microseconds
+                    f *= {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(u, 1.0)
+                    u = "us"
                 d[m] = f
                 d[m + ".unit"] = u
         res.append(d)

@@ -38,16 +38,20 @@ from plexgen import MODELS, manifest  # noqa: E402
 
 
 def bucket_payload(plan, bucket_bytes):
+    """Per bucket: data bytes, bf16 (PARAM) data bytes, number of segments touching it."""
     nb = plan.rank_info(0).n_buckets
-    pay = [0] * nb
+    pay, bf16, nseg = [0] * nb, [0] * nb, [0] * nb
     for s in plan.segments(0):
         lo, hi = s.slab_offset, s.slab_offset + s.nbytes
         while lo < hi:
             b = lo // bucket_bytes
             e = min(hi, (b + 1) * bucket_bytes)
             pay[b] += e - lo
+            if s.kind == 0:
+                bf16[b] += e - lo
+            nseg[b] += 1
             lo = e
-    return pay
+    return pay, bf16, nseg
 
 
 def main():
@@ -64,7 +68,7 @@ def main():
     mgr = P.StateManager(device=0, bucket_bytes=B, n_slots=2, bootstrap=False, duplex=False)
     plan = mgr.plan(manifest(a.model), head_dim=MODELS[a.model].head_dim, tp=1, dp=1)
     job = P.Job(mgr, plan, seed=1, slab=False).alloc().init_synthetic()
-    pay = bucket_payload(plan, B)
+    pay, bf16, nseg = bucket_payload(plan, B)
     full = [k for k in range(len(pay)) if pay[k] > 0.9 * B]          # the full buckets (ragged tail excluded)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     hbm = float(peaks["hbm_gbs"])
@@ -89,6 +93,8 @@ def main():
     def run(pack: bool, mode: str):
         ev = []
         n_launch = len(full) * a.reps
+        mgr.diag_pack(plan, job.shards, full[0], pack, s_k)              # pointer table, untimed
+        torch.cuda.synchronize()
         if "dma" in mode:
             per = (a.gap_ms if "gap" in mode else 0.75) * n_launch + 50.0
             dma(int(per / 40.0) + 2)                                     # ~40 ms per 2 GiB copy
@@ -101,16 +107,22 @@ def main():
                         torch.cuda._sleep(int(a.gap_ms * cyc_per_ms))
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(s_k)
-                    mgr.diag_pack(plan, job.shards, k, pack, s_k)
+                    mgr.diag_pack(plan, job.shards, k, pack, s_k, upload=False)
                     e1.record(s_k)
-                    ev.append((e0, e1, 2 * pay[k]))
+                    ev.append((e0, e1, 2 * pay[k], k))
         torch.cuda.synchronize()
-        ms = [x.elapsed_time(y) for x, y, _ in ev]
-        byt = sum(b for _, _, b in ev)
+        ms = [x.elapsed_time(y) for x, y, _, _ in ev]
+        byt = sum(b for _, _, b, _ in ev)
         t = sum(ms)
+        per_b = {}
+        for (_, _, b, k), m in zip(ev, ms):
+            per_b.setdefault(k, []).append(m)
+        buckets = [{"bucket": k, "us": round(1e3 * sum(v) / len(v), 1),
+                    "frac": round(2 * pay[k] / (sum(v) / len(v) * 1e-3) / 1e9 / hbm, 4),
+                    "bf16_share": round(bf16[k] / pay[k], 3), "segments": nseg[k]} for k, v in sorted(per_b.items())]
         return {"launches": len(ms), "avg_us": round(1e3 * t / len(ms), 1), "GBs": round(byt / (t * 1e-3) / 1e9, 1),
                 "frac": round(byt / (t * 1e-3) / 1e9 / hbm, 4), "min_us": round(1e3 * min(ms), 1),
-                "max_us": round(1e3 * max(ms), 1)}
+                "max_us": round(1e3 * max(ms), 1), "per_bucket": buckets}
 
     def torch_copy(mode: str):
         n = 8
