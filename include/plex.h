@@ -646,12 +646,13 @@ PLEX_API plex_status plex_cast_rne(const void* src_f32, void* dst_bf16, uint64_t
  * pointers, as plex_state_offload) and staging slot 0, on `stream`, with no
  * copy, no checksum verification and no residency change: the kernel as the
  * bucket pipeline launches it, timed on its own by tools/pack_insitu.py.  The
- * pointer table is uploaded first (a small H2D on `stream`) unless mode bit 1
+ * bucket's staging bytes start `staging_offset` bytes into the ctx's staging
+ * buffer (256-B aligned; E_INVAL past its end).  The pointer table is uploaded first (a small H2D on `stream`) unless mode bit 1
  * is set (the previous diag call on this ctx uploaded the same table).  The
  * staging bytes (pack) or the state bytes (unpack) are overwritten.  E_INVAL
  * for a bucket out of range. */
 PLEX_API plex_status plex_diag_pack(plex_ctx_t ctx, plex_plan_t plan, const void* const* state, int32_t n_state,
-                                    int32_t bucket, int32_t mode, void* stream);
+                                    int32_t bucket, int32_t mode, uint64_t staging_offset, void* stream);
 /* Select the K1/K2 build for every later launch in this process: 0 = default,
  * 1 = the same kernel with L2::evict_first cache policies on its bulk copies
  * (measurement of L2 residency effects).  E_INVAL for another value. */

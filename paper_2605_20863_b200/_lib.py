@@ -180,7 +180,7 @@ def _load() -> C.CDLL:
         "plex_synth_mutate": (C.c_int, [VP, I32, U64, U64, C.c_char_p, U64, U64, VP]),
         "plex_checksum": (C.c_int, [VP, I32, U64, U64, VP, VP]),
         "plex_cast_rne": (C.c_int, [VP, VP, U64, VP]),
-        "plex_diag_pack": (C.c_int, [VP, VP, P(VP), I32, I32, I32, VP]),
+        "plex_diag_pack": (C.c_int, [VP, VP, P(VP), I32, I32, I32, U64, VP]),
         "plex_diag_pack_variant": (C.c_int, [I32]),
         "plex_transition_decide": (C.c_int, [I64, I64, I32, P(Transition)]),
         "plex_plan_group": (C.c_int, [VP, I32, C.c_char_p, I32, P(I32), P(I32), P(I32)]),

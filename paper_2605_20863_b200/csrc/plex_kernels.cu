@@ -204,9 +204,9 @@ __device__ __forceinline__ uint32_t chunk_bulk(const ItemGeo& g, uint32_t co, ui
 struct StageMeta {
     ItemGeo g;
     uint32_t co;        // chunk offset within the item
-    uint32_t flags;     // kMetaLast: last chunk of its item; kMetaDone: no more work
+    uint32_t flags;     // kMetaDone: no more work
 };
-constexpr uint32_t kMetaLast = 1u, kMetaDone = 2u;
+constexpr uint32_t kMetaDone = 2u;
 
 template <int STAGES, int CHUNK_KB, int CWARPS, int CTAS>
 struct TmaCfg {
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
                 if (q >= (uint32_t)kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
                 meta[st].g = g;
                 meta[st].co = co;
-                meta[st].flags = (g.len - co <= kChunk) ? kMetaLast : 0u;
+                meta[st].flags = 0u;
                 const uint32_t nb = chunk_bulk(g, co, kChunk);
                 if (nb) {
                     mbar_arrive_tx(&full[st], nb);
@@ -292,8 +292,28 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         return;
     }
     // ---------------- consumers: checksum + TMA stores ----------------
+    // Each warp keeps one running (S1, S2) for the segment of the items it is
+    // folding and adds it to the segment's global pair only when the segment
+    // changes (R14 is additive over any partition) or at the end: a bucket
+    // inside one large tensor (embed / lm_head) would otherwise send every
+    // item's atomics to the same two addresses, and those serialise in L2
+    // (+40 % kernel time on such buckets, profiles/r02f_pack_insitu.jsonl).
     const uint64_t spol = (kHint && tid == 0) ? policy_evict_first() : 0;
     Cks c;
+    uint32_t cseg = 0xFFFFFFFFu;                    // segment c belongs to (warp-uniform)
+    auto flush = [&]() {
+        if (cseg == 0xFFFFFFFFu) return;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
+            c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
+        }
+        if (lane == 0) {
+            atomicAdd(cks + 2 * cseg, c.s1);
+            atomicAdd(cks + 2 * cseg + 1, c.s2);
+        }
+        c = Cks();
+    };
     for (uint32_t q = 0;; ++q) {
         const int st = (int)(q % kStages);
         mbar_wait(&full[st], (q / kStages) & 1);
@@ -301,6 +321,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
         if (flags & kMetaDone) break;
         const ItemGeo g = meta[st].g;
         const uint32_t co = meta[st].co;
+        if (co < g.data && g.seg != cseg) {          // this chunk carries data of another segment
+            flush();
+            cseg = g.seg;
+        }
         const uint8_t* src = kPack ? g.tens : g.buf;
         uint8_t* dst = kPack ? g.buf : g.tens;
         const uint8_t* sm = smem + (size_t)st * kChunk;
@@ -342,21 +366,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kCtasPerSm)
             if (nb) bulk_wait_read_all();                               // the bulk store has read stage st
             mbar_arrive(&empty[st]);
         }
-        if (flags & kMetaLast) {                                        // item complete: fold its checksum
-            if (g.data) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    c.s1 += __shfl_xor_sync(0xffffffffu, c.s1, o);
-                    c.s2 += __shfl_xor_sync(0xffffffffu, c.s2, o);
-                }
-                if (lane == 0) {
-                    atomicAdd(cks + 2 * g.seg, c.s1);
-                    atomicAdd(cks + 2 * g.seg + 1, c.s2);
-                }
-            }
-            c = Cks();
-        }
     }
+    flush();
     if (tid == 0) {
         bulk_wait_all();                           // every bulk store complete before exit
         // Self-resetting claim counter (no memset node before each launch): this

@@ -2364,13 +2364,17 @@ plex_status plex_synth_mutate(void* buf, int32_t kind, uint64_t job_seed, uint64
 
 // ---- diagnostics (kernel measurement, not the method) ----------------------------------
 plex_status plex_diag_pack(plex_ctx_t c, plex_plan_t plan, const void* const* state, int32_t n_state, int32_t bucket,
-                           int32_t mode, void* stream) {
+                           int32_t mode, uint64_t staging_offset, void* stream) {
     const bool pack = (mode & 1) != 0, upload = (mode & 2) == 0;
     plex_status st = check_common(c, plan);
     if (st) return st;
     const Plan& p = plan->p;
     const RankPlan& R = p.ranks[c->rank];
     if (bucket < 0 || bucket >= n_buckets(p, R)) { set_error("bucket %d out of range", bucket); return PLEX_E_INVAL; }
+    if ((staging_offset & 255) || staging_offset + p.bucket > c->staging_bytes) {
+        set_error("staging offset %llu: not 256-B aligned or past the staging buffer", (unsigned long long)staging_offset);
+        return PLEX_E_INVAL;
+    }
     DeviceGuard g(c->device);
     DevPlan* d;
     if ((st = fill_state_ptrs(c, p, state, n_state)) || (st = get_devplan(c, p, &d))) return st;
@@ -2379,7 +2383,7 @@ plex_status plex_diag_pack(plex_ctx_t c, plex_plan_t plan, const void* const* st
         CK(cudaMemcpyAsync(c->d_ptrs, c->h_ptrs, sizeof(uint64_t) * PLEX_NUM_KINDS * p.tensors.size(),
                            cudaMemcpyHostToDevice, s));
     const uint64_t i0 = R.bucket_item_start[bucket], i1 = R.bucket_item_start[bucket + 1];
-    CK(launch_pack(pack, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, c->staging,
+    CK(launch_pack(pack, d->items + i0, (uint32_t)(i1 - i0), d->segs, c->d_ptrs, c->staging + staging_offset,
                    (uint64_t)bucket * p.bucket, pack ? d->cks : d->cks_in, c->d_ctr, s));
     return PLEX_OK;
 }

@@ -517,12 +517,13 @@ class StateManager:
             out[name] = arena[off:off + 2 * n].view(torch.bfloat16).view(shape)
         return out
 
-    def diag_pack(self, plan: Plan, shards, bucket: int, pack: bool = True, stream=None, upload: bool = True) -> None:
+    def diag_pack(self, plan: Plan, shards, bucket: int, pack: bool = True, stream=None, upload: bool = True,
+                  staging_offset: int = 0) -> None:
         """Diagnostic: one K1/K2 launch over one bucket, no copies (plex_diag_pack);
         upload=False reuses the pointer table the previous diag call uploaded."""
         arr, n = self._state_ptrs(plan, shards, self.rank)
         check(lib.plex_diag_pack(self.h, plan.h, arr, n, bucket, (1 if pack else 0) | (0 if upload else 2),
-                                 _stream_ptr(stream)))
+                                 staging_offset, _stream_ptr(stream)))
 
     def enable_carry(self, plan: Plan) -> None:
         """Give the ctx carry staging (4 bucket slots) if `plan` carries buckets."""

@@ -62,10 +62,11 @@ def main():
     ap.add_argument("--gap-ms", type=float, default=5.0)
     ap.add_argument("--variants", default="0,1")
     ap.add_argument("--out", default="")
+    ap.add_argument("--shift-sweep", action="store_true", help="staging-offset sweep (gap mode) only")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     B = a.bucket_mb << 20
-    mgr = P.StateManager(device=0, bucket_bytes=B, n_slots=2, bootstrap=False, duplex=False)
+    mgr = P.StateManager(device=0, bucket_bytes=B, n_slots=2, bootstrap=False)           # 8 GiB staging
     plan = mgr.plan(manifest(a.model), head_dim=MODELS[a.model].head_dim, tp=1, dp=1)
     job = P.Job(mgr, plan, seed=1, slab=False).alloc().init_synthetic()
     pay, bf16, nseg = bucket_payload(plan, B)
@@ -146,6 +147,53 @@ def main():
         return {"avg_us": round(1e3 * sum(ms) / n, 1), "GBs": round(4 * 2 ** 30 / (sum(ms) / n * 1e-3) / 1e9, 1)}
 
     out = []
+    if a.shift_sweep:
+        # staging-offset sweep in gap mode: single-tensor buckets vs normal ones, and torch's
+        # copy of the same tensor bytes into the same staging addresses
+        single = [k for k in full if nseg[k] <= 5]
+        normal = [k for k in full if nseg[k] > 20][:2]
+        stg = mgr.staging
+        emb = job.shards[("model.embed_tokens.weight", 1)].view(torch.uint8).reshape(-1)[:B]
+        for off in [0, 64 << 10, 256 << 10, 1 << 20, (2 << 20) + (64 << 10), (6 << 20) + (192 << 10),
+                    (33 << 20) + (320 << 10), (1 << 30) + (2 << 20), 2 << 30, (3 << 30) + (4 << 10)]:
+            res = {}
+            for k in single + normal:
+                mgr.diag_pack(plan, job.shards, k, True, s_k, staging_offset=off)
+                torch.cuda.synchronize()
+                ts = []
+                with torch.cuda.stream(s_k):
+                    for _ in range(3):
+                        torch.cuda._sleep(int(a.gap_ms * cyc_per_ms))
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(s_k)
+                        mgr.diag_pack(plan, job.shards, k, True, s_k, upload=False, staging_offset=off)
+                        e1.record(s_k)
+                        ts.append((e0, e1))
+                torch.cuda.synchronize()
+                res[k] = round(1e3 * sum(x.elapsed_time(y) for x, y in ts) / 3, 1)
+            ts = []
+            with torch.cuda.stream(s_k):
+                for _ in range(3):
+                    torch.cuda._sleep(int(a.gap_ms * cyc_per_ms))
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(s_k)
+                    stg[off:off + B].copy_(emb)
+                    e1.record(s_k)
+                    ts.append((e0, e1))
+            torch.cuda.synchronize()
+            r = {"tool": "pack_insitu", "sweep": "staging_offset", "offset": off,
+                 "pack_us": {str(k): v for k, v in res.items()},
+                 "segments": {str(k): nseg[k] for k in res},
+                 "torch_copy_embed_to_staging_us": round(1e3 * sum(x.elapsed_time(y) for x, y in ts) / 3, 1),
+                 "addr_delta_embed_minus_staging": int(emb.data_ptr()) - int(stg.data_ptr()) - off}
+            print(json.dumps(r), flush=True)
+            out.append(r)
+        if a.out:
+            with open(a.out, "a") as f:
+                for r in out:
+                    f.write(json.dumps(r) + "\n")
+        mgr.close()
+        return
     for v in [int(x) for x in a.variants.split(",")]:
         diag_pack_variant(v)
         run(True, "b2b")                                                # warm-up
