@@ -1,4 +1,6 @@
-"""N>1 host logic on CPU with the gloo backend (world 2 and 3): the NCCL-id
+"""N>1 host logic on CPU with the gloo backend (world 2, 3 and 8 -- 8 is the
+bench's M2 launch: Qwen2.5-7B FSDP-8 -> TP-2 x DP-4, AUTO rank map, 2 GiB
+buckets, link-weight balancing): the NCCL-id
 bootstrap broadcast, plan determinism across ranks (every rank builds the same
 plan from the same request, PAPER.md:555/576 plans must agree for the
 collective sync), and ledger symmetry (what r sends g is what g receives)."""
@@ -29,10 +31,13 @@ def _worker(rank, world, port, q):
         nid = bootstrap_nccl_id(rank)
         ids = [None] * world
         dist.all_gather_object(ids, nid)
-        model = "qwen2.5-7b" if world == 2 else "mid-moe"
-        tp = 2 if world == 2 else 1
-        ep = 1 if world == 2 else 1
-        plan = Plan(manifest(model), head_dim=MODELS[model].head_dim, world=world, tp=tp, dp=world // tp, ep=ep)
+        from paper_2605_20863_b200 import _lib as L
+        big = world in (2, 8)
+        model = "qwen2.5-7b" if big else "mid-moe"
+        tp = 2 if big else 1
+        ep = 1
+        plan = Plan(manifest(model), head_dim=MODELS[model].head_dim, world=world, tp=tp, dp=world // tp, ep=ep,
+                    rank_map=L.RANKMAP_AUTO if world == 8 else L.RANKMAP_TP_FAST)
         dig = [plan_digest(plan, g) for g in range(world)]
         digs = [None] * world
         dist.all_gather_object(digs, dig)
@@ -46,7 +51,8 @@ def _worker(rank, world, port, q):
         w = torch.tensor([10.0 + 5.0 * rank])
         ws = [torch.zeros(1) for _ in range(world)]
         dist.all_gather(ws, w)
-        cp = Plan(manifest(model), world=world, bucket_bytes=(1 << 30) if world == 2 else (1 << 14), link_weights=[float(x) for x in ws])
+        cp = Plan(manifest(model), world=world, bucket_bytes={2: 1 << 30, 8: 2 << 30}.get(world, 1 << 14),
+                  link_weights=[float(x) for x in ws])
         carry = [(c.owner, c.bucket, c.carrier, c.slab_offset, c.bytes, c.carry_offset) for c in cp.carry()]
         carries = [None] * world
         dist.all_gather_object(carries, carry)
@@ -66,7 +72,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_gloo_multi_rank_host_logic(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
