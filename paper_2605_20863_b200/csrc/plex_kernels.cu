@@ -482,54 +482,80 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
 // param = RNE(master) and checksum what was written.  The master shard of
 // tensor t sits at pointer slot ptr_slot + n_tensors (kind 1 vs kind 0).
 template <bool kCheck>
-__global__ void __launch_bounds__(kThreads) derive_kernel(const PackItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads) derive_kernel(const PackItem* __restrict__ items, uint32_t n_items,
                                                           const SegDev* __restrict__ segs,
                                                           const uint64_t* __restrict__ ptrs, uint32_t n_tensors,
                                                           unsigned long long* __restrict__ cks, int* __restrict__ bad) {
-    const PackItem it = items[blockIdx.x];
-    const SegDev s = segs[it.seg];
-    const uint64_t o0 = it.slab_lo - s.slab_off;
-    if (o0 >= s.bytes) return;                                  // padding only
-    const uint64_t nbytes = (s.bytes - o0 < it.len ? s.bytes - o0 : it.len);
-    const uint64_t n = nbytes / 2;                              // bf16 elements
-    uint16_t* param = reinterpret_cast<uint16_t*>(ptrs[s.ptr_slot] + o0);
-    const uint32_t* master = reinterpret_cast<const uint32_t*>(ptrs[s.ptr_slot + n_tensors] + 2 * o0);
-    const uint64_t ib = s.index_base + o0 / 2;
+    // Grid-stride over the items; the block keeps one running (S1, S2) while
+    // its items stay in one segment and adds it to the segment's pair when the
+    // segment changes (as K1/K2: a bf16 embed / lm_head segment spans ~16 k
+    // items, whose per-item atomics would serialise on one L2 address).
     Cks c;
+    uint32_t cseg = 0xFFFFFFFFu;
     int miss = 0;
-    const bool vec = ((reinterpret_cast<uintptr_t>(param) & 15) == 0) && ((reinterpret_cast<uintptr_t>(master) & 15) == 0);
-    const uint64_t nv = vec ? n / 8 : 0;
-    for (uint64_t v = threadIdx.x; v < nv; v += kThreads) {
-        const uint4 r = rne_8(ld_stream(master + 8 * v), ld_stream(master + 8 * v + 4));
-        if (kCheck) {
-            const uint4 x = ld_stream(param + 8 * v);
-            miss |= (x.x != r.x) | (x.y != r.y) | (x.z != r.z) | (x.w != r.w);
-            c.add_vec(x, 2, ib + 8 * v);
-        } else {
-            st_v4(param + 8 * v, r);
-            c.add_vec(r, 2, ib + 8 * v);
+    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x) {
+        const PackItem it = items[i];
+        const SegDev s = segs[it.seg];
+        const uint64_t o0 = it.slab_lo - s.slab_off;
+        if (o0 >= s.bytes) continue;                                // padding only (block-uniform)
+        if (it.seg != cseg) {
+            if (cseg != 0xFFFFFFFFu) {
+                block_reduce_add(c, cks + 2 * cseg);
+                __syncthreads();                                    // shared partials reused by the next flush
+            }
+            c = Cks();
+            cseg = it.seg;
+        }
+        const uint64_t nbytes = (s.bytes - o0 < it.len ? s.bytes - o0 : it.len);
+        const uint64_t n = nbytes / 2;                              // bf16 elements
+        uint16_t* param = reinterpret_cast<uint16_t*>(ptrs[s.ptr_slot] + o0);
+        const uint32_t* master = reinterpret_cast<const uint32_t*>(ptrs[s.ptr_slot + n_tensors] + 2 * o0);
+        const uint64_t ib = s.index_base + o0 / 2;
+        const bool vec =
+            ((reinterpret_cast<uintptr_t>(param) & 15) == 0) && ((reinterpret_cast<uintptr_t>(master) & 15) == 0);
+        const uint64_t nv = vec ? n / 8 : 0;
+        for (uint64_t v = threadIdx.x; v < nv; v += kThreads) {
+            const uint4 r = rne_8(ld_stream(master + 8 * v), ld_stream(master + 8 * v + 4));
+            if (kCheck) {
+                const uint4 x = ld_stream(param + 8 * v);
+                miss |= (x.x != r.x) | (x.y != r.y) | (x.z != r.z) | (x.w != r.w);
+                c.add_vec(x, 2, ib + 8 * v);
+            } else {
+                st_v4(param + 8 * v, r);
+                c.add_vec(r, 2, ib + 8 * v);
+            }
+        }
+        for (uint64_t e = nv * 8 + threadIdx.x; e < n; e += kThreads) {
+            const uint32_t r = rne_bf16(master[e]);
+            uint32_t b = r;
+            if (kCheck) {
+                b = param[e];
+                miss |= (b != r);
+            } else {
+                param[e] = (uint16_t)r;
+            }
+            c.add_elem(b, ib + e);
         }
     }
-    for (uint64_t e = nv * 8 + threadIdx.x; e < n; e += kThreads) {
-        const uint32_t r = rne_bf16(master[e]);
-        uint32_t b = r;
-        if (kCheck) {
-            b = param[e];
-            miss |= (b != r);
-        } else {
-            param[e] = (uint16_t)r;
-        }
-        c.add_elem(b, ib + e);
-    }
+    if (cseg != 0xFFFFFFFFu) block_reduce_add(c, cks + 2 * cseg);
     if (kCheck && __syncthreads_or(miss) && threadIdx.x == 0) atomicAdd(bad, 1);
-    block_reduce_add(c, cks + 2 * it.seg);
 }
+
+static int g_num_sms = 0;
 
 cudaError_t launch_derive(bool check, const PackItem* items, uint32_t n_items, const SegDev* segs, const uint64_t* ptrs,
                           uint32_t n_tensors, unsigned long long* cks, int* bad, cudaStream_t s) {
     if (!n_items) return cudaSuccess;
-    if (check) derive_kernel<true><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, n_tensors, cks, bad);
-    else derive_kernel<false><<<n_items, kThreads, 0, s>>>(items, segs, ptrs, n_tensors, cks, bad);
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    const uint32_t cap = (uint32_t)g_num_sms * 8u;                 // 8 x 256 threads resident per SM
+    const uint32_t grid = n_items < cap ? n_items : cap;
+    if (check) derive_kernel<true><<<grid, kThreads, 0, s>>>(items, n_items, segs, ptrs, n_tensors, cks, bad);
+    else derive_kernel<false><<<grid, kThreads, 0, s>>>(items, n_items, segs, ptrs, n_tensors, cks, bad);
     return cudaGetLastError();
 }
 
@@ -607,7 +633,6 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint8_t* __res
 }
 
 // ---- launchers ----------------------------------------------------------------
-static int g_num_sms = 0;
 static int g_pack_variant = 0;          // diagnostic only (plex_diag_pack_variant)
 
 template <bool kPack, int kHint>

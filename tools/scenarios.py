@@ -31,6 +31,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -493,8 +494,18 @@ def scen_sync(a, c: Ctx):
 
 
 def scen_multiplex(a, c: Ctx):
+    """configs[4]: 4 jobs shaped 0.5B / 1.5B / 3B / 7B
+    (seeds 0..3) time-slice the GPU group round-robin for --rounds rounds
+    (default 5: 20 visits, 19 switches).  Every visit goes through the
+    library's residency authority (plex_group_transition: it decides the
+    ops and picks duplex / sequential from what fits), then one
+    simulated training step (synth_mutate) and the weight sync through the
+    group.  Full-size parity of the same trace: tests/test_gpu_fullsize_configs.py
+    ::test_m5_multiplex_trace_fullsize."""
+    from paper_2605_20863_b200.state import synth_mutate
     models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
     mgr = P.StateManager(device=c.local, rank=c.rank, world=c.world, bucket_bytes=a.bucket_mb << 20, timing=True)
+    group = P.Group(mgr)
     plans, jobs, arenas = [], [], []
     for j, mo in enumerate(models):
         tp = 1 if mo == "qwen2.5-0.5b" or c.world == 1 else 2
@@ -502,41 +513,41 @@ def scen_multiplex(a, c: Ctx):
         plans.append(pl)
         jb = P.Job(mgr, pl, seed=j).alloc().init_synthetic()
         jb.suspend()
+        group.add(jb)
         jobs.append(jb)
         arenas.append(mgr.arena(pl))
     schedule = list(range(4)) * a.rounds
-    res = {"r": None}
-    from paper_2605_20863_b200.state import synth_mutate  # noqa: F401  (mutation = simulated train step)
+    steps = [0] * 4
+    modes: dict = {}
+    ms_switch = []
 
-    sizes = [pl.rank_info(c.rank).payload_bytes for pl in plans]
-    dup_used = {"n": 0}
+    def mutate(j):
+        for t, (key, shape) in enumerate(plans[j].manifest):
+            a0, _ = plans[j].shard_rows(c.rank, t)
+            re_ = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+            for kd in range(4):
+                synth_mutate(jobs[j].shards[(key, kd)], kd, j, steps[j], key, a0 * re_)
+        steps[j] += 1
 
     def run_trace():
-        resident = res["r"]
         for j in schedule:
-            if resident is not None and resident != j:
-                # duplex needs both jobs on the device during the switch
-                free = torch.cuda.mem_get_info(c.local)[0]
-                dup = a.duplex and c.allmin(1.0 if sizes[j] + (2 << 30) < free else 0.0) > 0.5
-                if dup:
-                    jobs[resident].switch_to(jobs[j])
-                    dup_used["n"] += 1
-                else:
-                    jobs[resident].suspend()
-                    jobs[j].resume()
-            elif resident is None:
-                jobs[j].resume()
-            resident = j
-            jobs[j].sync(arenas[j])
-        jobs[resident].suspend()
-        res["r"] = None
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = group.transition(jobs[j])                       # the library decides and executes
+            e1.record()
+            modes[res["mode"]] = modes.get(res["mode"], 0) + 1
+            mutate(j)                                             # simulated training step
+            group.transition(jobs[j], sync=arenas[j])             # [SYNC j]
+            torch.cuda.synchronize()
+            ms_switch.append(e0.elapsed_time(e1))
 
     ms, clk = timed(c, run_trace, 1, 0, min_s=0)
-    switches = len(schedule) - 1
     c.emit({"scenario": "multiplex", "jobs": models, "n_gpus": c.world, "rounds": a.rounds,
-            "visits": len(schedule), "switches": switches, "duplex": a.duplex, "duplex_switches": dup_used["n"],
-            "trace_ms": round(ms, 1),
-            "ms_per_visit": round(ms / len(schedule), 1), "clocks": clk}, a.out)
+            "visits": len(schedule), "switches": len(schedule) - 1, "executor": "plex_group_transition",
+            "modes": modes, "trace_ms": round(ms, 1), "ms_per_visit": round(ms / len(schedule), 1),
+            "switch_ms_max_rank_sum": round(c.allmax(float(sum(ms_switch))), 1),
+            "state_gb_per_rank": [round(pl.rank_info(c.rank).payload_bytes / 1e9, 2) for pl in plans],
+            "clocks": clk}, a.out)
 
 
 def scen_zero2(a, c: Ctx):
