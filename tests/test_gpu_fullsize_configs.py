@@ -235,6 +235,7 @@ def test_m5_multiplex_trace_fullsize():
     _need(150)
     torch.cuda.set_device(0)
     W = 8 if torch.cuda.get_device_properties(0).total_memory >= 185e9 else 4
+    print(f"M5 trace: FSDP-{W} emulated, device total_memory {torch.cuda.get_device_properties(0).total_memory}")
     models = ["qwen2.5-0.5b", "qwen2.5-1.5b", "qwen2.5-3b", "qwen2.5-7b"]
     seeds = [0, 1, 2, 3]
     rounds = 5
