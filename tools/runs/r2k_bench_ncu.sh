@@ -15,3 +15,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:pack
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:push_kernel -c 1 -o gpurun_out/r02k_push $C3 > gpurun_out/r02k_ncu_push.log 2>&1; echo push_rc=$?
 grep '^{' gpurun_out/r2k_bench.log | tail -1 | cut -c1-400
 grep -o '"roofline": {[^}]*}' gpurun_out/r2k_bench.log
+# M5 at D1's FSDP-8 (8 emulated ranks)
+timeout 1500 python -m pytest tests/test_gpu_fullsize_configs.py -q -s -m gpu -k m5_ > gpurun_out/r2k_pytest_m5_w8.log 2>&1
+echo m5_rc=$?
+tail -5 gpurun_out/r2k_pytest_m5_w8.log
+grep "M5 trace" gpurun_out/r2k_pytest_m5_w8.log

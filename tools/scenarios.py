@@ -198,7 +198,8 @@ def scen_elide(a, c: Ctx):
 def scen_hrrs(a, c: Ctx):
     """NEXT-4: drain one queue of RLVR requests from 4 jobs time-slicing the
     GPU group, FCFS vs HRRS (Alg. 1 / Eq. 3-4) ordering.  Context switches and
-    weight syncs are real (this library); a request's compute phase is modeled
+    weight syncs are real, decided and executed by the group's residency
+    authority (plex_group_transition); a request's compute phase is modeled
     as a host-side wait of its Table-2 duration scaled by
     --time-scale.  HRRS gets C_setup = T_offload + T_load as measured by the
     library on the first switches (Setup.from_stats)."""
@@ -229,6 +230,9 @@ def scen_hrrs(a, c: Ctx):
     reqs.sort(key=lambda r: r.arrival)
 
     def run(policy: str, setup: Setup):
+        group = P.Group(mgr)              # the residency authority executes every switch the order causes
+        for jb in jobs:                   # every job starts HOST-resident
+            group.add(jb)
         resident = None
         t0 = time.perf_counter()
         pending = list(reqs)
@@ -248,17 +252,15 @@ def scen_hrrs(a, c: Ctx):
             r = pending[pick]
             pending.remove(r)
             waits.append(now - r.arrival)
-            if r.job != resident:
-                if resident is None:
-                    jobs[r.job].resume()
-                else:
-                    jobs[resident].switch_to(jobs[r.job])
-                resident = r.job
+            # the group compares the request's job with its resident
+            # job and prepends [OFFLOAD, ONLOAD] itself when they differ
+            res = group.transition(jobs[r.job], sync=arenas[r.job] if r.name == "sync" else None)
+            if res["mode"] not in ("none",):
                 switches += 1
-            if r.name == "sync":
-                jobs[r.job].sync(arenas[r.job])
+            resident = r.job
             torch.cuda.synchronize()
             time.sleep(r.exec_time)                       # the request's own compute phase (modeled)
+        group.close()                                     # park the resident job for the next run
         jobs[resident].suspend()
         return time.perf_counter() - t0, switches, sum(waits) / len(waits)
 
