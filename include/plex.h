@@ -650,7 +650,8 @@ PLEX_API plex_status plex_cast_rne(const void* src_f32, void* dst_bf16, uint64_t
  * buffer (256-B aligned; E_INVAL past its end).  The pointer table is uploaded first (a small H2D on `stream`) unless mode bit 1
  * is set (the previous diag call on this ctx uploaded the same table).  The
  * staging bytes (pack) or the state bytes (unpack) are overwritten.  E_INVAL
- * for a bucket out of range. */
+ * for a bucket out of range; E_STATE while an async prefetch/drain is in
+ * flight on the ctx (it shares the staging ring and work counters). */
 PLEX_API plex_status plex_diag_pack(plex_ctx_t ctx, plex_plan_t plan, const void* const* state, int32_t n_state,
                                     int32_t bucket, int32_t mode, uint64_t staging_offset, void* stream);
 /* Select the K1/K2 build for every later launch in this process: 0 = default,

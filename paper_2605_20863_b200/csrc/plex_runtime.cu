@@ -2367,7 +2367,7 @@ plex_status plex_diag_pack(plex_ctx_t c, plex_plan_t plan, const void* const* st
                            int32_t mode, uint64_t staging_offset, void* stream) {
     const bool pack = (mode & 1) != 0, upload = (mode & 2) == 0;
     plex_status st = check_common(c, plan);
-    if (st) return st;
+    if (st || (st = check_no_async(c))) return st;              // shares the staging ring and counters
     const Plan& p = plan->p;
     const RankPlan& R = p.ranks[c->rank];
     if (bucket < 0 || bucket >= n_buckets(p, R)) { set_error("bucket %d out of range", bucket); return PLEX_E_INVAL; }
