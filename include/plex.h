@@ -19,10 +19,13 @@
  *    slab's residency untouched; a failed onload leaves the slab untouched and
  *    its residency HOST (destination contents unspecified); a failed sync
  *    leaves the sources untouched (destination unspecified).
- *  - Device memory for state, rollout tensors and staging is the CALLER's
- *    (PyTorch's).  The library allocates only: pinned host slabs, small device
- *    metadata tables (segment/work-item tables, pointer tables), events, and
- *    NCCL internals.  Streams are the caller's (cudaStream_t passed as void*).
+ *  - Device memory is always the CALLER's (PyTorch's): state, rollout
+ *    tensors, staging, and a device workspace handed to plex_ctx_create in
+ *    which the library keeps its metadata tables (segment / work-item tables,
+ *    pointer tables, checksum accumulators, handshake flags).  The library
+ *    never calls cudaMalloc (NCCL internals excepted); it allocates pinned
+ *    host memory (slabs, small mirrors) and events.  Streams are the
+ *    caller's (cudaStream_t passed as void*).
  *  - Plans are immutable after creation and may be shared read-only.  Calls
  *    on one (job, rank) state are serialised by the caller (WPG-serial
  *    semantics).
@@ -355,13 +358,23 @@ PLEX_API plex_status plex_plan_param_arena(plex_plan_t plan, int32_t t, uint64_t
 PLEX_API plex_status plex_nccl_unique_id(void* out128);
 /* device: CUDA ordinal.  staging: caller-owned device buffer of
  * staging_bytes >= n_slots * bucket_bytes of every plan used with this ctx.
+ * workspace: caller-owned device buffer (256-B aligned, >= 1 MiB) holding the
+ * library's device metadata for the ctx's lifetime: per plan used with the
+ * ctx about 32 B per segment + 16 B per 64 KiB slab work item + 40 B per push
+ * item + 48 B per segment of checksums (a Qwen2.5-7B FSDP-1 plan: ~75 MB);
+ * freed when the plan is destroyed.  A call that would overflow it fails with
+ * PLEX_E_TIER_FULL (nothing moved).  E_INVAL for a NULL / misaligned / too
+ * small workspace.
  * pack_stream / copy_stream: caller-owned cudaStream_t (side streams).
  * nccl_id: 128 B from plex_nccl_unique_id, or NULL when world == 1 (or for a
  * ctx used only for single-process per-rank emulation).  Collective over
  * `world` ranks when nccl_id != NULL. */
-PLEX_API plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, int32_t n_slots,
-                            void* pack_stream, void* copy_stream, const void* nccl_id,
-                            int32_t rank, int32_t world, uint32_t flags, plex_ctx_t* out);
+PLEX_API plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, void* workspace,
+                                     uint64_t workspace_bytes, int32_t n_slots, void* pack_stream, void* copy_stream,
+                                     const void* nccl_id, int32_t rank, int32_t world, uint32_t flags,
+                                     plex_ctx_t* out);
+/* Device workspace bytes in use now and at most since creation. */
+PLEX_API plex_status plex_ctx_workspace(plex_ctx_t ctx, uint64_t* in_use, uint64_t* high_water);
 PLEX_API plex_status plex_ctx_destroy(plex_ctx_t ctx);
 /* NEXT-1 host-link balancing: caller-owned device buffer of >= 4 x bucket
  * bytes (256-B aligned) used to stage carried buckets (plans built with

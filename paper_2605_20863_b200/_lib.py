@@ -38,7 +38,7 @@ EXPORTS = [
     "plex_last_error", "plex_version", "plex_transition_plan", "plex_plan_destroy", "plex_plan_query",
     "plex_plan_rank_info", "plex_plan_segment", "plex_plan_dst_tensor", "plex_plan_shard_rows", "plex_plan_ledger",
     "plex_plan_n_carry", "plex_plan_carry", "plex_ctx_set_carry_staging", "plex_slab_carry",
-    "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
+    "plex_nccl_unique_id", "plex_ctx_create", "plex_ctx_workspace", "plex_ctx_destroy", "plex_ctx_stats", "plex_ctx_reset_stats",
     "plex_ctx_trace", "plex_ctx_set_flags",
     "plex_slab_create", "plex_slab_destroy", "plex_slab_info", "plex_slab_elided", "plex_slab_checksums",
     "plex_slab_spill", "plex_slab_fill",
@@ -144,7 +144,8 @@ def _load() -> C.CDLL:
         "plex_ctx_set_carry_staging": (C.c_int, [VP, VP, U64]),
         "plex_slab_carry": (C.c_int, [VP, P(VP), P(U64)]),
         "plex_nccl_unique_id": (C.c_int, [VP]),
-        "plex_ctx_create": (C.c_int, [I32, VP, U64, I32, VP, VP, VP, I32, I32, U32, P(VP)]),
+        "plex_ctx_create": (C.c_int, [I32, VP, U64, VP, U64, I32, VP, VP, VP, I32, I32, U32, P(VP)]),
+        "plex_ctx_workspace": (C.c_int, [VP, P(U64), P(U64)]),
         "plex_ctx_destroy": (C.c_int, [VP]),
         "plex_ctx_stats": (C.c_int, [VP, I32, P(KernelStats)]),
         "plex_ctx_reset_stats": (C.c_int, [VP]),

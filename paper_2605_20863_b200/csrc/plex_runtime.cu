@@ -114,6 +114,20 @@ struct Timed {
 
 struct AsyncState;   // an in-flight plex_state_drain / plex_state_prefetch
 
+constexpr uint64_t kMinWorkspace = 1ull << 20;
+
+// Device metadata lives in the caller's workspace (plex_ctx_create): the
+// library never calls cudaMalloc (SURVEY §8(b) ownership).  A first-fit free
+// list over [base, base + bytes), 256-B granules, coalescing on free.
+struct DevHeap {
+    uint8_t* base = nullptr;
+    uint64_t bytes = 0;
+    std::map<uint64_t, uint64_t> free_;      // offset -> size
+    std::map<uint64_t, uint64_t> used;       // offset -> size
+    uint64_t in_use = 0, high_water = 0;
+    std::mutex mu;
+};
+
 }  // namespace plex
 
 using namespace plex;
@@ -185,6 +199,7 @@ struct plex_ctx_s {
     cudaIpcMemHandle_t my_handle[4]{};
     std::map<uint64_t, DevPlan> dev;    // plan id -> device tables
     cudaEvent_t ev_sync[6] = {};        // NCCL baseline: rpack / nccl / runpack x 2
+    DevHeap heap;                       // caller's device workspace: every device table above
 };
 
 struct plex_ckpt_s {                   // a background checkpoint (plex_slab_checkpoint_start)
@@ -221,30 +236,87 @@ namespace plex {
 static std::mutex g_ctx_mu;
 static std::set<plex_ctx_s*> g_ctxs;
 
-static void free_devplan(DevPlan& d) {
-    cudaFree(d.segs);
-    cudaFree(d.items);
-    cudaFree(d.push);
-    cudaFree(d.gather);
-    cudaFree(d.push_local);
-    cudaFree(d.push_remote);
-    cudaFree(d.cks);
-    cudaFree(d.cks_want);
-    cudaFree(d.cks_in);
-    cudaFree(d.items_el);
-    cudaFree(d.local);
-    cudaFree(d.rpack);
-    cudaFree(d.runpack);
+static plex_status dev_alloc(plex_ctx_s* c, uint64_t n, void** out) {
+    *out = nullptr;
+    if (!n) return PLEX_OK;
+    DevHeap& h = c->heap;
+    const uint64_t need = (n + 255) & ~255ull;
+    std::lock_guard<std::mutex> lk(h.mu);
+    for (auto it = h.free_.begin(); it != h.free_.end(); ++it) {
+        if (it->second < need) continue;
+        const uint64_t off = it->first, sz = it->second;
+        h.free_.erase(it);
+        if (sz > need) h.free_[off + need] = sz - need;
+        h.used[off] = need;
+        h.in_use += need;
+        h.high_water = std::max(h.high_water, h.in_use);
+        *out = h.base + off;
+        return PLEX_OK;
+    }
+    set_error("device metadata workspace exhausted: %llu B requested, %llu of %llu B in use "
+              "(pass a larger workspace to plex_ctx_create)", (unsigned long long)need,
+              (unsigned long long)h.in_use, (unsigned long long)h.bytes);
+    return PLEX_E_TIER_FULL;
+}
+
+template <class T>
+static plex_status dev_alloc_t(plex_ctx_s* c, uint64_t n, T** out) {
+    void* p = nullptr;
+    plex_status s = dev_alloc(c, n, &p);
+    *out = reinterpret_cast<T*>(p);
+    return s;
+}
+
+static void dev_free(plex_ctx_s* c, const void* p) {
+    if (!p) return;
+    DevHeap& h = c->heap;
+    std::lock_guard<std::mutex> lk(h.mu);
+    const uint64_t off = reinterpret_cast<const uint8_t*>(p) - h.base;
+    auto u = h.used.find(off);
+    if (u == h.used.end()) return;
+    uint64_t o = off, sz = u->second;
+    h.in_use -= sz;
+    h.used.erase(u);
+    auto nx = h.free_.lower_bound(o);
+    if (nx != h.free_.end() && o + sz == nx->first) {          // merge with the next free block
+        sz += nx->second;
+        nx = h.free_.erase(nx);
+    }
+    if (nx != h.free_.begin()) {                                 // ... and the previous one
+        auto pv = std::prev(nx);
+        if (pv->first + pv->second == o) {
+            pv->second += sz;
+            return;
+        }
+    }
+    h.free_[o] = sz;
+}
+
+// Every stream the ctx launches kernels or copies on has drained (cudaFree used
+// to imply this; a workspace block may be handed out again right after a free).
+static void quiesce(plex_ctx_s* c) {
+    for (cudaStream_t s2 : {c->pack, c->copy, c->copy2, c->kasync, c->copy3, c->ckern, c->cstream, c->ccopy})
+        if (s2) cudaStreamSynchronize(s2);
+}
+
+static void free_devplan(plex_ctx_s* c, DevPlan& d) {
+    quiesce(c);
+    for (const void* p : {(const void*)d.segs, (const void*)d.items, (const void*)d.push, (const void*)d.gather,
+                          (const void*)d.push_local, (const void*)d.push_remote, (const void*)d.cks,
+                          (const void*)d.cks_want, (const void*)d.cks_in, (const void*)d.items_el,
+                          (const void*)d.local, (const void*)d.rpack, (const void*)d.runpack})
+        dev_free(c, p);
     cudaFreeHost(d.h_cks_out);
     cudaFreeHost(d.h_cks_want);
     d = DevPlan{};
 }
 
 template <class T>
-static plex_status upload(T** dptr, const std::vector<T>& v) {
+static plex_status upload(plex_ctx_s* c, T** dptr, const std::vector<T>& v) {
     *dptr = nullptr;
     if (v.empty()) return PLEX_OK;
-    CK(cudaMalloc(dptr, sizeof(T) * v.size()));
+    plex_status s = dev_alloc_t(c, sizeof(T) * v.size(), dptr);
+    if (s) return s;
     CK(cudaMemcpy(*dptr, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
     return PLEX_OK;
 }
@@ -255,19 +327,22 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     const RankPlan& R = p.ranks[c->rank];
     DevPlan d;
     plex_status s;
-    if ((s = upload(&d.segs, R.segs)) || (s = upload(&d.items, R.items)) || (s = upload(&d.push, R.push)) ||
-        (s = upload(&d.items_el, R.items_el)) || (s = upload(&d.gather, R.gather))) {
-        free_devplan(d);
+    if ((s = upload(c, &d.segs, R.segs)) || (s = upload(c, &d.items, R.items)) || (s = upload(c, &d.push, R.push)) ||
+        (s = upload(c, &d.items_el, R.items_el)) || (s = upload(c, &d.gather, R.gather))) {
+        free_devplan(c, d);
         return s;
     }
     const size_t nck = std::max<size_t>(1, 2 * R.segs.size());
-    if (cudaMalloc(&d.cks, nck * 8) != cudaSuccess || cudaMalloc(&d.cks_want, nck * 8) != cudaSuccess ||
-        cudaMalloc(&d.cks_in, nck * 8) != cudaSuccess ||
-        cudaHostAlloc(&d.h_cks_out, nck * 8, cudaHostAllocDefault) != cudaSuccess ||
+    if ((s = dev_alloc_t(c, nck * 8, &d.cks)) || (s = dev_alloc_t(c, nck * 8, &d.cks_want)) ||
+        (s = dev_alloc_t(c, nck * 8, &d.cks_in))) {
+        free_devplan(c, d);
+        return s;
+    }
+    if (cudaHostAlloc(&d.h_cks_out, nck * 8, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&d.h_cks_want, nck * 8, cudaHostAllocDefault) != cudaSuccess) {
         (void)cudaGetLastError();
-        free_devplan(d);
-        set_error("cudaMalloc of checksum tables failed");
+        free_devplan(c, d);
+        set_error("cudaHostAlloc of checksum mirrors failed");
         return PLEX_E_CUDA;
     }
     const int32_t nb = n_buckets(p, R);
@@ -299,20 +374,22 @@ static plex_status get_devplan(plex_ctx_s* c, const Plan& p, DevPlan** out) {
     return PLEX_OK;
 }
 
-static plex_status ensure_table(uint64_t** h, uint64_t** d, size_t* capp, size_t n) {
+static plex_status ensure_table(plex_ctx_s* c, uint64_t** h, uint64_t** d, size_t* capp, size_t n) {
     if (n <= *capp) return PLEX_OK;
     size_t cap = std::max<size_t>(n, 2 * *capp);
+    if (*d) quiesce(c);
     cudaFreeHost(*h);
-    cudaFree(*d);
+    dev_free(c, *d);
     *h = nullptr;
     *d = nullptr;
     *capp = 0;
     CK(cudaHostAlloc(h, cap * 8, cudaHostAllocDefault));
-    CK(cudaMalloc(d, cap * 8));
+    plex_status s = dev_alloc_t(c, cap * 8, d);
+    if (s) return s;
     *capp = cap;
     return PLEX_OK;
 }
-static plex_status ensure_ptrs(plex_ctx_s* c, size_t n) { return ensure_table(&c->h_ptrs, &c->d_ptrs, &c->ptr_cap, n); }
+static plex_status ensure_ptrs(plex_ctx_s* c, size_t n) { return ensure_table(c, &c->h_ptrs, &c->d_ptrs, &c->ptr_cap, n); }
 
 // ---- timing ------------------------------------------------------------------
 static plex_status timed_begin(plex_ctx_s* c, cudaStream_t s, cudaEvent_t* a) {
@@ -427,8 +504,8 @@ static plex_status fill_state_ptrs(plex_ctx_s* c, const Plan& p, const void* con
         return PLEX_E_INVAL;
     }
     plex_status s = table == 0   ? ensure_ptrs(c, PLEX_NUM_KINDS * nt)
-                    : table == 1 ? ensure_table(&c->h_ptrs2, &c->d_ptrs2, &c->ptr_cap2, PLEX_NUM_KINDS * nt)
-                                 : ensure_table(&c->h_ptrs3, &c->d_ptrs3, &c->ptr_cap3, PLEX_NUM_KINDS * nt);
+                    : table == 1 ? ensure_table(c, &c->h_ptrs2, &c->d_ptrs2, &c->ptr_cap2, PLEX_NUM_KINDS * nt)
+                                 : ensure_table(c, &c->h_ptrs3, &c->d_ptrs3, &c->ptr_cap3, PLEX_NUM_KINDS * nt);
     if (s) return s;
     uint64_t* h = table == 0 ? c->h_ptrs : table == 1 ? c->h_ptrs2 : c->h_ptrs3;
     const RankPlan& R = p.ranks[c->rank];
@@ -546,7 +623,8 @@ static plex_status carry_ready(plex_ctx_s* c, const Plan& p) {
     if (!(c->flags & PLEX_CTX_CARRY_NCCL)) {
         if (!c->cflags) {
             void* f = nullptr;
-            CK(cudaMalloc(&f, 4096));
+            plex_status sa = dev_alloc(c, 4096, &f);                // exported to the peers over CUDA IPC
+            if (sa) return sa;
             CK(cudaMemset(f, 0, 4096));
             c->cflags = reinterpret_cast<unsigned long long*>(f);
             c->cerr = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(f) + 2048);
@@ -938,9 +1016,9 @@ plex_status plex_nccl_unique_id(void* out128) {
     return PLEX_OK;
 }
 
-plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, int32_t n_slots, void* pack_stream,
-                            void* copy_stream, const void* nccl_id, int32_t rank, int32_t world, uint32_t flags,
-                            plex_ctx_t* out) {
+plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_bytes, void* workspace,
+                            uint64_t workspace_bytes, int32_t n_slots, void* pack_stream, void* copy_stream,
+                            const void* nccl_id, int32_t rank, int32_t world, uint32_t flags, plex_ctx_t* out) {
     if (!out) { set_error("NULL out"); return PLEX_E_INVAL; }
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world || n_slots < 1 || n_slots > 64 || !staging || !staging_bytes) {
@@ -948,8 +1026,16 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
         return PLEX_E_INVAL;
     }
     if (reinterpret_cast<uintptr_t>(staging) % 256) { set_error("staging must be 256-B aligned"); return PLEX_E_INVAL; }
+    if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256 || workspace_bytes < kMinWorkspace) {
+        set_error("workspace must be a 256-B aligned device buffer of >= %llu bytes",
+                  (unsigned long long)kMinWorkspace);
+        return PLEX_E_INVAL;
+    }
     DeviceGuard g(device);
     auto* c = new plex_ctx_s();
+    c->heap.base = reinterpret_cast<uint8_t*>(workspace);
+    c->heap.bytes = workspace_bytes & ~255ull;
+    c->heap.free_[0] = c->heap.bytes;
     c->device = device;
     c->staging = reinterpret_cast<uint8_t*>(staging);
     c->staging_bytes = staging_bytes;
@@ -983,11 +1069,15 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
             return fail(PLEX_E_CUDA);
         }
     c->scratch_bytes = 256 * (size_t)world + 256;
-    if (cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&c->d_flag, 64) != cudaSuccess ||
-        cudaMalloc(&c->d_ctr, 64) != cudaSuccess ||
-        cudaMalloc(&c->d_scratch, 2 * c->scratch_bytes) != cudaSuccess ||
+    {
+        plex_status sa;
+        if ((sa = dev_alloc_t(c, 64, &c->d_flag)) || (sa = dev_alloc_t(c, 64, &c->d_ctr)) ||
+            (sa = dev_alloc_t(c, 2 * c->scratch_bytes, &c->d_scratch)))
+            return fail(sa);
+    }
+    if (cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&c->h_scratch, 2 * c->scratch_bytes, cudaHostAllocDefault) != cudaSuccess) {
-        set_error("ctx scratch allocation failed");
+        set_error("ctx pinned scratch allocation failed");
         return fail(PLEX_E_CUDA);
     }
     // pack/unpack claim counters [0, 8) and their finished-CTA counters [8, 16):
@@ -1014,6 +1104,14 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
     return PLEX_OK;
 }
 
+plex_status plex_ctx_workspace(plex_ctx_t c, uint64_t* in_use, uint64_t* high_water) {
+    if (!c || !in_use || !high_water) { set_error("NULL argument"); return PLEX_E_INVAL; }
+    std::lock_guard<std::mutex> lk(c->heap.mu);
+    *in_use = c->heap.in_use;
+    *high_water = c->heap.high_water;
+    return PLEX_OK;
+}
+
 plex_status plex_ctx_destroy(plex_ctx_t c) {
     if (!c) return PLEX_OK;
     {
@@ -1033,7 +1131,7 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     for (auto& a : c->async) {
         if (a) { a->slab->busy = false; async_free(a); a = nullptr; }
     }
-    for (auto& kv : c->dev) free_devplan(kv.second);
+    for (auto& kv : c->dev) free_devplan(c, kv.second);
     for (auto& kv : c->peers)
         if (kv.second.second) cudaIpcCloseMemHandle(kv.second.second);
     if (c->comm) ncclCommDestroy(c->comm);
@@ -1045,9 +1143,7 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     if (c->ev_pack_done) cudaEventDestroy(c->ev_pack_done);
     if (c->ev_copy_done) cudaEventDestroy(c->ev_copy_done);
     cudaFreeHost(c->h_ptrs);
-    cudaFree(c->d_ptrs);
     cudaFreeHost(c->h_ptrs2);
-    cudaFree(c->d_ptrs2);
     for (cudaEvent_t e : c->ev_pack2) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy2) cudaEventDestroy(e);
     if (c->copy2) cudaStreamDestroy(c->copy2);
@@ -1064,13 +1160,8 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     for (cudaEvent_t e : c->ev_pack3) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy3) cudaEventDestroy(e);
     cudaFreeHost(c->h_ptrs3);
-    cudaFree(c->d_ptrs3);
     cudaFreeHost(c->h_flag);
-    cudaFree(c->d_flag);
-    cudaFree(c->d_ctr);
-    cudaFree(c->d_scratch);
     cudaFreeHost(c->h_scratch);
-    if (c->cflags) cudaFree(c->cflags);
     if (c->h_cerr) cudaFreeHost(c->h_cerr);
     delete c;
     return PLEX_OK;
@@ -1085,8 +1176,7 @@ plex_status plex_plan_destroy(plex_plan_t plan) {
             auto it = c->dev.find(key);
             if (it == c->dev.end()) continue;
             DeviceGuard g(c->device);
-            cudaStreamSynchronize(c->pack);
-            free_devplan(it->second);
+            free_devplan(c, it->second);                  // drains the ctx's streams first
             c->dev.erase(it);
         }
     }
@@ -2082,7 +2172,7 @@ static plex_status split_push(plex_ctx_s* c, const Plan& p, DevPlan* d) {
         else { rem.push_back(it); d->push_remote_elems += n; }
     }
     plex_status st;
-    if ((st = upload(&d->push_local, loc)) || (st = upload(&d->push_remote, rem))) return st;
+    if ((st = upload(c, &d->push_local, loc)) || (st = upload(c, &d->push_remote, rem))) return st;
     d->n_push_local = loc.size();
     d->n_push_remote = rem.size();
     d->push_split = true;
@@ -2101,7 +2191,7 @@ plex_status plex_weight_sync_rank(plex_ctx_t c, plex_plan_t plan, int32_t rank, 
     auto it = c->dev.find(key);
     if (it == c->dev.end()) {
         DevPlan d;
-        plex_status s = upload(&d.push, p.ranks[rank].push);
+        plex_status s = upload(c, &d.push, p.ranks[rank].push);
         if (s) return s;
         it = c->dev.emplace(key, d).first;
     }
@@ -2242,7 +2332,7 @@ plex_status plex_param_allgather_rank(plex_ctx_t c, plex_plan_t plan, int32_t ra
     auto it = c->dev.find(key);
     if (it == c->dev.end()) {
         DevPlan d;
-        if ((st = upload(&d.gather, p.ranks[rank].gather))) return st;
+        if ((st = upload(c, &d.gather, p.ranks[rank].gather))) return st;
         it = c->dev.emplace(key, d).first;
     }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -2500,12 +2590,14 @@ static plex_status build_nccl_sched(plex_ctx_s* c, const Plan& p, DevPlan* d, ui
         rp.insert(rp.end(), rp_r[k].begin(), rp_r[k].end());
         ru.insert(ru.end(), ru_r[k].begin(), ru_r[k].end());
     }
-    cudaFree(d->local);
-    cudaFree(d->rpack);
-    cudaFree(d->runpack);
+    if (d->local || d->rpack || d->runpack) quiesce(c);
+    dev_free(c, d->local);
+    dev_free(c, d->rpack);
+    dev_free(c, d->runpack);
     d->local = d->rpack = d->runpack = nullptr;
     plex_status st;
-    if ((st = upload(&d->local, local)) || (st = upload(&d->rpack, rp)) || (st = upload(&d->runpack, ru))) return st;
+    if ((st = upload(c, &d->local, local)) || (st = upload(c, &d->rpack, rp)) || (st = upload(c, &d->runpack, ru)))
+        return st;
     d->n_local = local.size();
     d->local_bytes = local_bytes;
     d->rounds = R;

@@ -321,7 +321,8 @@ class StateManager:
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, bucket_bytes: int = 2 << 30,
                  n_slots: int = 2, timing: bool = False, sync_nccl: bool = False, bootstrap: bool = True,
-                 nccl_id: Optional[bytes] = None, duplex: bool = True, carry_nccl: bool = False):
+                 nccl_id: Optional[bytes] = None, duplex: bool = True, carry_nccl: bool = False,
+                 workspace_bytes: int = 256 << 20):
         if not torch.cuda.is_available():
             raise RuntimeError("StateManager needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -342,7 +343,10 @@ class StateManager:
         flags = ((L.CTX_TIMING if timing else 0) | (L.CTX_SYNC_NCCL if sync_nccl else 0)
                  | (L.CTX_CARRY_NCCL if carry_nccl else 0))
         h = C.c_void_p()
-        check(lib.plex_ctx_create(device, self.staging.data_ptr(), self.staging.numel(), n_slots,
+        # the library's device metadata tables live here (it never calls cudaMalloc)
+        self.workspace = torch.empty(workspace_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+        check(lib.plex_ctx_create(device, self.staging.data_ptr(), self.staging.numel(), self.workspace.data_ptr(),
+                                  self.workspace.numel(), n_slots,
                                   self.pack_stream.cuda_stream, self.copy_stream.cuda_stream,
                                   idbuf, rank, world, flags, C.byref(h)))
         self.h = h
@@ -533,6 +537,12 @@ class StateManager:
         if getattr(self, "carry_staging", None) is None or self.carry_staging.numel() < need:
             self.carry_staging = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
             check(lib.plex_ctx_set_carry_staging(self.h, self.carry_staging.data_ptr(), self.carry_staging.numel()))
+
+    def workspace_usage(self) -> Tuple[int, int]:
+        """(bytes in use, high-water mark) of the device metadata workspace."""
+        a, b = C.c_uint64(), C.c_uint64()
+        check(lib.plex_ctx_workspace(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stats(self) -> Dict[str, dict]:
         out = {}

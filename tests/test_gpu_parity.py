@@ -995,3 +995,41 @@ def test_swap_with_replica_params_world1():
         P._lib.check(P._lib.lib.plex_param_allgather(m.h, plain.h, a.param_arena.data_ptr(), None))
     assert e.value.code == L.E_INVAL
     m.close()
+
+
+def test_workspace_is_the_callers_and_bounded():
+    """SURVEY §8(b) ownership: the library keeps every device table in the
+    workspace the caller hands to plex_ctx_create (it never calls cudaMalloc).
+    Too small a workspace is refused at creation; a plan whose tables do not
+    fit fails with E_TIER_FULL before anything moves; destroying the plan
+    gives its tables back."""
+    import gc
+    with pytest.raises(P.PlexError) as e:
+        P.StateManager(device=0, bucket_bytes=4096, bootstrap=False, workspace_bytes=4096)
+    assert e.value.code == L.E_INVAL
+    man = [("w", (4096, 16384))]                              # 64 M elements; 4 KiB buckets -> 230 k work items
+    small = P.StateManager(device=0, bucket_bytes=4096, bootstrap=False, workspace_bytes=1 << 20)
+    plan = small.plan(man)
+    job = P.Job(small, plan, seed=3).alloc().init_synthetic()
+    before = {k: P.checksum(v).cpu() for k, v in job.shards.items()}
+    with pytest.raises(P.PlexError) as e:
+        job.suspend(release=False)
+    assert e.value.code == L.E_TIER_FULL and "workspace" in str(e.value)
+    assert job.slab.residency == L.RES_DEVICE                 # nothing moved
+    assert all(torch.equal(P.checksum(v).cpu(), before[k]) for k, v in job.shards.items())
+    big = P.StateManager(device=0, bucket_bytes=4096, bootstrap=False, workspace_bytes=64 << 20)
+    base, _ = big.workspace_usage()
+    plan2 = big.plan(man)
+    job2 = P.Job(big, plan2, seed=3).alloc().init_synthetic()
+    job2.suspend()
+    job2.resume()                                              # checksum-verified round trip
+    assert all(torch.equal(P.checksum(v).cpu(), before[k]) for k, v in job2.shards.items())
+    used, hw = big.workspace_usage()
+    assert used > base and hw >= used
+    del job2, plan2
+    gc.collect()
+    assert big.workspace_usage()[0] < used                     # the plan's tables went back
+    del job, plan
+    gc.collect()
+    small.close()
+    big.close()
