@@ -111,7 +111,7 @@ def main():
             groups.setdefault(k, []).append(d)
         for k, ds in groups.items():
             rd = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in ds]
-            traffic[k] = {"dram_bytes_per_launch": sum(rd) / len(rd), "source": f"gpurun_out/{tag}_{which}.ncu-rep",
+            traffic[k] = {"dram_bytes_per_launch": sum(rd) / len(rd), "source": f"profiles/{tag}_ncu_summary.md (capture gpurun_out/{tag}_{which}.ncu-rep, not committed)",
                           "duration_us": sum(d.get("gpu__time_duration.sum", 0) for d in ds) / len(ds),
                           "launches": len(ds)}
     json.dump(traffic, open(traffic_path, "w"), indent=1)
