@@ -100,15 +100,6 @@ def test_fullsize_qwen05_one_gpu():
 
 
 @pytest.mark.slow
-def test_fullsize_qwen7b_one_gpu():
-    """bench.py's N=1 workload: the whole Qwen2.5-7B state on one B200."""
-    if torch.cuda.get_device_properties(0).total_memory < 150e9:
-        pytest.skip("needs a 180 GB B200")
-    _fullsize("qwen2.5-7b", 1, ["lm_head.weight", "model.layers.0.self_attn.q_proj.weight",
-                                "model.layers.27.mlp.down_proj.weight", "model.norm.weight"])
-
-
-@pytest.mark.slow
 def test_fullsize_qwen05_every_byte():
     """configs[0] checked exhaustively: every byte of the
     0.5B slab and every element of every rollout tensor against the oracle's
