@@ -361,7 +361,7 @@ PLEX_API plex_status plex_nccl_unique_id(void* out128);
  * workspace: caller-owned device buffer (256-B aligned, >= 1 MiB) holding the
  * library's device metadata for the ctx's lifetime: per plan used with the
  * ctx about 32 B per segment + 16 B per 64 KiB slab work item + 40 B per push
- * item + 48 B per segment of checksums (a Qwen2.5-7B FSDP-1 plan: ~75 MB);
+ * item + 48 B per segment of checksums (a Qwen2.5-7B FSDP-1 plan: ~45 MB, ~71 MB with elision);
  * freed when the plan is destroyed.  A call that would overflow it fails with
  * PLEX_E_TIER_FULL (nothing moved).  E_INVAL for a NULL / misaligned / too
  * small workspace.
