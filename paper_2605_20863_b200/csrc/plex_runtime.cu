@@ -115,6 +115,17 @@ struct Timed {
 struct AsyncState;   // an in-flight plex_state_drain / plex_state_prefetch
 
 constexpr uint64_t kMinWorkspace = 1ull << 20;
+constexpr uint64_t kSwapPieces = 4;     // copies per bucket in the in-place swap (at most)
+// Measurement knob: PLEX_SWAP_PIECES=1 restores whole-bucket copies (A/B of the
+// piecewise swap on one box); read once.
+static uint64_t swap_pieces() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("PLEX_SWAP_PIECES");
+        const long x = e ? std::strtol(e, nullptr, 10) : (long)kSwapPieces;
+        return (uint64_t)std::min<long>((long)kSwapPieces, std::max<long>(1, x));
+    }();
+    return v;
+}
 
 // Device metadata lives in the caller's workspace (plex_ctx_create): the
 // library never calls cudaMalloc (SURVEY §8(b) ownership).  A first-fit free
@@ -184,6 +195,7 @@ struct plex_ctx_s {
     uint64_t cepoch = 0;
     std::vector<std::vector<unsigned long long>> carry_in_last;   // [owner][onload slot] last seq written
     std::vector<cudaEvent_t> ev_pack2, ev_copy2;
+    std::vector<cudaEvent_t> ev_piece;  // in-place swap: H2D piece j of in-ring slot s done
     int* h_flag = nullptr;
     int* d_flag = nullptr;
     unsigned int* d_ctr = nullptr;      // pack/unpack work counters, one per pipe (+8: finished CTAs)
@@ -1145,6 +1157,7 @@ plex_status plex_ctx_destroy(plex_ctx_t c) {
     cudaFreeHost(c->h_ptrs);
     cudaFreeHost(c->h_ptrs2);
     for (cudaEvent_t e : c->ev_pack2) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_piece) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_copy2) cudaEventDestroy(e);
     if (c->copy2) cudaStreamDestroy(c->copy2);
     if (c->kasync) cudaStreamDestroy(c->kasync);
@@ -1729,6 +1742,10 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
             CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
         }
     }
+    if (c->ev_piece.empty()) {
+        c->ev_piece.resize((size_t)c->n_slots * kSwapPieces);
+        for (auto& e : c->ev_piece) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
             c->d_ctr, c->d_flag + 2, c->h_flag + 2};
     // Both halves' kernels share the pack stream.  The two rings run at the
@@ -1810,6 +1827,10 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
             CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
         }
     }
+    if (c->ev_piece.empty()) {
+        c->ev_piece.resize((size_t)c->n_slots * kSwapPieces);
+        for (auto& e : c->ev_piece) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
             c->d_ctr, c->d_flag + 2, c->h_flag + 2};
     Pipe pi{c->staging + (uint64_t)c->n_slots * p.bucket, c->n_slots, c->ev_pack2.data(), c->ev_copy2.data(), c->pack,
@@ -1866,11 +1887,19 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
         const uint64_t lo = base + (uint64_t)k * p.bucket;
         const uint64_t len = std::min<uint64_t>(p.bucket, R.slab_bytes - lo);
         const uint64_t i0 = hi.bstart[k], i1 = hi.bstart[k + 1];
-        // H2D B_k
+        // H2D B_k, in pieces: A_k's D2H may overwrite a slab range as soon as
+        // B_k's piece of it has been read, so the first and last buckets (which
+        // run one direction alone) shrink to one piece each
+        const uint64_t np = std::min<uint64_t>(swap_pieces(), std::max<uint64_t>(1, len / 4096));
+        const uint64_t ps = ((len + np - 1) / np + 255) & ~255ull;
         if (k >= c->n_slots) CK(cudaStreamWaitEvent(pi.copy, pi.ev_k[si_slot], 0));
-        if ((st = tbeg(c, pi, pi.copy, &ta))) return st;
-        CK(cudaMemcpyAsync(si, slab->host + lo, len, cudaMemcpyHostToDevice, pi.copy));
-        if ((st = tend(c, pi, pi.copy, ta, PLEX_STAT_H2D, len))) return st;
+        for (uint64_t j = 0; j * ps < len; ++j) {
+            const uint64_t o = j * ps, n = std::min(ps, len - o);
+            if ((st = tbeg(c, pi, pi.copy, &ta))) return st;
+            CK(cudaMemcpyAsync(si + o, slab->host + lo + o, n, cudaMemcpyHostToDevice, pi.copy));
+            if ((st = tend(c, pi, pi.copy, ta, PLEX_STAT_H2D, n))) return st;
+            CK(cudaEventRecord(c->ev_piece[(size_t)si_slot * kSwapPieces + j], pi.copy));
+        }
         CK(cudaEventRecord(pi.ev_c[si_slot], pi.copy));
         // pack A_k
         if (oseq >= c->n_slots) CK(cudaStreamWaitEvent(po.kern, po.ev_c[so_slot], 0));
@@ -1886,12 +1915,15 @@ plex_status plex_state_swap(plex_ctx_t c, plex_plan_t plan, void* const* state, 
                        pi.ctr, pi.kern));
         if ((st = tend(c, pi, pi.kern, ta, PLEX_STAT_UNPACK, 2 * hi.payload[k]))) return st;
         CK(cudaEventRecord(pi.ev_k[si_slot], pi.kern));
-        // D2H A_k (after H2D B_k read this slab range)
+        // D2H A_k, piece j after H2D B_k has read that piece of the slab range
         CK(cudaStreamWaitEvent(po.copy, po.ev_k[so_slot], 0));
-        CK(cudaStreamWaitEvent(po.copy, pi.ev_c[si_slot], 0));
-        if ((st = tbeg(c, po, po.copy, &ta))) return st;
-        CK(cudaMemcpyAsync(slab->host + lo, so, len, cudaMemcpyDeviceToHost, po.copy));
-        if ((st = tend(c, po, po.copy, ta, PLEX_STAT_D2H, len))) return st;
+        for (uint64_t j = 0; j * ps < len; ++j) {
+            const uint64_t o = j * ps, n = std::min(ps, len - o);
+            CK(cudaStreamWaitEvent(po.copy, c->ev_piece[(size_t)si_slot * kSwapPieces + j], 0));
+            if ((st = tbeg(c, po, po.copy, &ta))) return st;
+            CK(cudaMemcpyAsync(slab->host + lo + o, so + o, n, cudaMemcpyDeviceToHost, po.copy));
+            if ((st = tend(c, po, po.copy, ta, PLEX_STAT_D2H, n))) return st;
+        }
         CK(cudaEventRecord(po.ev_c[so_slot], po.copy));
     }
     // on_end re-derives B's params (elided) after every A pack on the same stream
