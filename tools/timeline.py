@@ -94,6 +94,10 @@ def main():
                    "busy_frac_of_span": round(busy(v) / span, 3)}
     if "d2h" in iv and "h2d" in iv:
         summ["d2h_h2d_overlap_ms"] = round(overlap(iv["d2h"], iv["h2d"]), 2)
+        # one direction alone at the ends: before the first D2H starts / after the last H2D ends
+        summ["head_ms_before_first_d2h"] = round(min(x for x, _ in iv["d2h"]), 2)
+        summ["tail_ms_after_last_h2d"] = round(span - max(y for _, y in iv["h2d"]), 2)
+        summ["swap_pieces_env"] = os.environ.get("PLEX_SWAP_PIECES", "default")
     kern = iv.get("pack", []) + iv.get("unpack", [])
     copies = iv.get("d2h", []) + iv.get("h2d", [])
     if kern and copies:
