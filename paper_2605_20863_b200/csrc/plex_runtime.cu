@@ -115,13 +115,14 @@ struct Timed {
 struct AsyncState;   // an in-flight plex_state_drain / plex_state_prefetch
 
 constexpr uint64_t kMinWorkspace = 1ull << 20;
-constexpr uint64_t kSwapPieces = 4;     // copies per bucket in the in-place swap (at most)
-// Measurement knob: PLEX_SWAP_PIECES=1 restores whole-bucket copies (A/B of the
-// piecewise swap on one box); read once.
+constexpr uint64_t kSwapPieces = 16;    // copies per bucket in the in-place swap (at most)
+constexpr uint64_t kSwapPiecesDefault = 4;
+// Measurement knob: PLEX_SWAP_PIECES=n (1..16; 1 = whole-bucket copies) for
+// A/B runs of the piecewise swap on one box; read once.
 static uint64_t swap_pieces() {
     static const uint64_t v = [] {
         const char* e = std::getenv("PLEX_SWAP_PIECES");
-        const long x = e ? std::strtol(e, nullptr, 10) : (long)kSwapPieces;
+        const long x = e ? std::strtol(e, nullptr, 10) : (long)kSwapPiecesDefault;
         return (uint64_t)std::min<long>((long)kSwapPieces, std::max<long>(1, x));
     }();
     return v;
