@@ -1743,10 +1743,6 @@ plex_status plex_state_switch(plex_ctx_t c, plex_plan_t plan_out, const void* co
             CK(cudaEventCreateWithFlags(&c->ev_copy2[i], cudaEventDisableTiming));
         }
     }
-    if (c->ev_piece.empty()) {
-        c->ev_piece.resize((size_t)c->n_slots * kSwapPieces);
-        for (auto& e : c->ev_piece) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
     Pipe po{c->staging, c->n_slots, c->ev_pack.data(), c->ev_copy.data(), c->pack, c->copy, c->h_ptrs, c->d_ptrs,
             c->d_ctr, c->d_flag + 2, c->h_flag + 2};
     // Both halves' kernels share the pack stream.  The two rings run at the
