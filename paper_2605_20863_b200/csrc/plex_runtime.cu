@@ -116,7 +116,7 @@ struct AsyncState;   // an in-flight plex_state_drain / plex_state_prefetch
 
 constexpr uint64_t kMinWorkspace = 1ull << 20;
 constexpr uint64_t kSwapPieces = 16;    // copies per bucket in the in-place swap (at most)
-constexpr uint64_t kSwapPiecesDefault = 4;
+constexpr uint64_t kSwapPiecesDefault = 8;   // sweep 2 / 4 / 8 / 16: profiles/r02r_*
 // Measurement knob: PLEX_SWAP_PIECES=n (1..16; 1 = whole-bucket copies) for
 // A/B runs of the piecewise swap on one box; read once.
 static uint64_t swap_pieces() {
