@@ -28,6 +28,7 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include "plex_heap.h"
 #include "plex_internal.h"
 
 namespace plex {
@@ -129,14 +130,11 @@ static uint64_t swap_pieces() {
 }
 
 // Device metadata lives in the caller's workspace (plex_ctx_create): the
-// library never calls cudaMalloc (SURVEY §8(b) ownership).  A first-fit free
-// list over [base, base + bytes), 256-B granules, coalescing on free.
+// library never calls cudaMalloc (SURVEY §8(b) ownership).  OffsetHeap
+// (plex_heap.h) hands out 256-B aligned offsets into [base, base + bytes).
 struct DevHeap {
     uint8_t* base = nullptr;
-    uint64_t bytes = 0;
-    std::map<uint64_t, uint64_t> free_;      // offset -> size
-    std::map<uint64_t, uint64_t> used;       // offset -> size
-    uint64_t in_use = 0, high_water = 0;
+    OffsetHeap h;
     std::mutex mu;
 };
 
@@ -253,23 +251,16 @@ static plex_status dev_alloc(plex_ctx_s* c, uint64_t n, void** out) {
     *out = nullptr;
     if (!n) return PLEX_OK;
     DevHeap& h = c->heap;
-    const uint64_t need = (n + 255) & ~255ull;
     std::lock_guard<std::mutex> lk(h.mu);
-    for (auto it = h.free_.begin(); it != h.free_.end(); ++it) {
-        if (it->second < need) continue;
-        const uint64_t off = it->first, sz = it->second;
-        h.free_.erase(it);
-        if (sz > need) h.free_[off + need] = sz - need;
-        h.used[off] = need;
-        h.in_use += need;
-        h.high_water = std::max(h.high_water, h.in_use);
-        *out = h.base + off;
-        return PLEX_OK;
+    const uint64_t off = h.h.alloc(n);
+    if (off == OffsetHeap::kNone) {
+        set_error("device metadata workspace exhausted: %llu B requested, %llu of %llu B in use "
+                  "(pass a larger workspace to plex_ctx_create)", (unsigned long long)n,
+                  (unsigned long long)h.h.in_use(), (unsigned long long)h.h.bytes());
+        return PLEX_E_TIER_FULL;
     }
-    set_error("device metadata workspace exhausted: %llu B requested, %llu of %llu B in use "
-              "(pass a larger workspace to plex_ctx_create)", (unsigned long long)need,
-              (unsigned long long)h.in_use, (unsigned long long)h.bytes);
-    return PLEX_E_TIER_FULL;
+    *out = h.base + off;
+    return PLEX_OK;
 }
 
 template <class T>
@@ -284,25 +275,7 @@ static void dev_free(plex_ctx_s* c, const void* p) {
     if (!p) return;
     DevHeap& h = c->heap;
     std::lock_guard<std::mutex> lk(h.mu);
-    const uint64_t off = reinterpret_cast<const uint8_t*>(p) - h.base;
-    auto u = h.used.find(off);
-    if (u == h.used.end()) return;
-    uint64_t o = off, sz = u->second;
-    h.in_use -= sz;
-    h.used.erase(u);
-    auto nx = h.free_.lower_bound(o);
-    if (nx != h.free_.end() && o + sz == nx->first) {          // merge with the next free block
-        sz += nx->second;
-        nx = h.free_.erase(nx);
-    }
-    if (nx != h.free_.begin()) {                                 // ... and the previous one
-        auto pv = std::prev(nx);
-        if (pv->first + pv->second == o) {
-            pv->second += sz;
-            return;
-        }
-    }
-    h.free_[o] = sz;
+    h.h.free((uint64_t)(reinterpret_cast<const uint8_t*>(p) - h.base));
 }
 
 // Every stream the ctx launches kernels or copies on has drained (cudaFree used
@@ -1047,8 +1020,7 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
     DeviceGuard g(device);
     auto* c = new plex_ctx_s();
     c->heap.base = reinterpret_cast<uint8_t*>(workspace);
-    c->heap.bytes = workspace_bytes & ~255ull;
-    c->heap.free_[0] = c->heap.bytes;
+    c->heap.h.reset(workspace_bytes);
     c->device = device;
     c->staging = reinterpret_cast<uint8_t*>(staging);
     c->staging_bytes = staging_bytes;
@@ -1120,8 +1092,8 @@ plex_status plex_ctx_create(int32_t device, void* staging, uint64_t staging_byte
 plex_status plex_ctx_workspace(plex_ctx_t c, uint64_t* in_use, uint64_t* high_water) {
     if (!c || !in_use || !high_water) { set_error("NULL argument"); return PLEX_E_INVAL; }
     std::lock_guard<std::mutex> lk(c->heap.mu);
-    *in_use = c->heap.in_use;
-    *high_water = c->heap.high_water;
+    *in_use = c->heap.h.in_use();
+    *high_water = c->heap.h.high_water();
     return PLEX_OK;
 }
 
