@@ -423,6 +423,49 @@ def scen_optim(a, c: Ctx):
     _ = shape
 
 
+def scen_m2rank(a, c: Ctx):
+    """configs[1] per-GPU workload at k GPUs: each process is rank c.rank of the
+    M2 plan (Qwen2.5-7B FSDP-8 -> TP-2 x DP-4, AUTO rank map) and switches the
+    GPU between two such jobs through the group executor (duplex: offload A ||
+    onload B, 13.33 GB each way per GPU).  k = WORLD_SIZE GPUs switch at once,
+    sharing the box's host memory system as 8 ranks of a real 8-GPU box would
+    share theirs.  The M2 sync is not run here (it needs all 8 ranks' peers);
+    its NVLink bound from the plan's ledger is reported next to it."""
+    W = 8
+    model = "qwen2.5-7b"
+    mgr = P.StateManager(device=c.local, rank=c.rank, world=W, bucket_bytes=a.bucket_mb << 20, bootstrap=False,
+                         timing=True)
+    plan = mgr.plan(manifest(model), head_dim=MODELS[model].head_dim, world=W, tp=2, dp=4, rank_map=L.RANKMAP_AUTO)
+    ja = P.Job(mgr, plan, seed=1).alloc().init_synthetic()
+    jb = P.Job(mgr, plan, seed=2).alloc().init_synthetic()
+    jb.suspend()
+    group = P.Group(mgr)
+    group.add(ja, resident=True)
+    group.add(jb)
+    modes = {}
+    cur = {"j": ja}
+
+    def step():
+        nxt = jb if cur["j"] is ja else ja
+        res = group.transition(nxt)
+        modes[res["mode"]] = modes.get(res["mode"], 0) + 1
+        cur["j"] = nxt
+
+    ms, clk = timed(c, step, a.steps, a.warmup, min_s=0)
+    S = plan.rank_info(c.rank).payload_bytes
+    st = mgr.stats()
+    d2h = st["d2h"]["bytes"] / (st["d2h"]["ms"] * 1e-3) / 1e9
+    h2d = st["h2d"]["bytes"] / (st["h2d"]["ms"] * 1e-3) / 1e9
+    led = plan.ledger()
+    nv = max(max(int(led[r].sum() - led[r, r]), int(led[:, r].sum() - led[r, r])) for r in range(W))
+    c.emit({"scenario": "m2rank", "model": model, "plan": "FSDP-8 -> TP-2xDP-4 (AUTO rank map)", "k_gpus": c.world,
+            "state_bytes_per_gpu": S, "switch_ms_max_rank": round(ms, 2), "modes": modes,
+            "GBs_per_gpu_each_way": round(S / (ms * 1e-3) / 1e9, 2),
+            "rank0_copy_engine_GBs": {"d2h": round(d2h, 2), "h2d": round(h2d, 2)},
+            "m2_sync_nvlink_bound_ms": round(nv / 770e9 * 1e3, 2), "m2_sync_busiest_link_bytes": nv,
+            "clocks": clk}, a.out)
+
+
 def scen_moe(a, c: Ctx):
     model = "qwen3-30b-a3b"
     shape = MODELS[model]
@@ -644,7 +687,8 @@ def scen_carry(a, c: Ctx):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync", "zero2", "carry"])
+    ap.add_argument("--scenario", required=True, choices=["duplex", "elide", "optim", "moe", "multiplex", "hrrs", "overlap", "nvme", "sync", "zero2", "carry",
+                             "m2rank"])
     ap.add_argument("--spill-dir", default="/tmp")
     ap.add_argument("--io-threads", type=int, default=8)
     ap.add_argument("--time-scale", type=float, default=0.005)
@@ -664,7 +708,7 @@ def main():
     if not a.model:
         a.model = {"duplex": "qwen2.5-7b", "elide": "qwen2.5-7b", "optim": "qwen2.5-32b", "zero2": "qwen2.5-7b", "carry": "qwen2.5-7b"}.get(a.scenario, "")
     {"duplex": scen_duplex, "elide": scen_elide, "optim": scen_optim, "moe": scen_moe,
-     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "overlap": scen_overlap, "nvme": scen_nvme,
+     "multiplex": scen_multiplex, "hrrs": scen_hrrs, "m2rank": scen_m2rank, "overlap": scen_overlap, "nvme": scen_nvme,
      "sync": scen_sync, "zero2": scen_zero2, "carry": scen_carry}[a.scenario](a, c)
     c.barrier()
     if c.world > 1:
