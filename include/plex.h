@@ -483,7 +483,9 @@ PLEX_API plex_status plex_state_switch(plex_ctx_t ctx, plex_plan_t plan_out, con
  * plex_state_switch), but only ONE device copy and ONE pinned slab exist: per
  * bucket, the outgoing pack reads a tensor range before the incoming unpack
  * overwrites it (same kernel stream) and the outgoing D2H overwrites a slab
- * range only after the incoming H2D has read it.  Staging >= 2 x n_slots x
+ * range only after the incoming H2D has read it (both copies of a bucket run
+ * in up to 8 pieces, each D2H piece waiting only for its own H2D piece, so
+ * the head and tail buckets overlap too).  Staging >= 2 x n_slots x
  * bucket.  Blocking, caller-stream ordered.  With PLEX_PLAN_ELIDE_PARAM: an
  * elided incoming slab and a derivable outgoing job both walk the shifted
  * grid (no param byte moves); an elided incoming slab and a non-derivable
