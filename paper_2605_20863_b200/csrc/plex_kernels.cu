@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "plex_internal.h"
 
@@ -409,10 +410,13 @@ __device__ __forceinline__ uint4 rne_8(const uint4& a, const uint4& b) {
 // send segment.  kCast = false is K5 of the NCCL baseline: a bf16 -> bf16
 // rectangle copy from a receive segment into the arena.
 template <bool kCast>
-__global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restrict__ items, uint64_t n_items,
                                                         const uint64_t* __restrict__ src_ptrs,
                                                         const uint64_t* __restrict__ dst_arenas) {
-    const PushItem it = items[blockIdx.x];
+  // one item per CTA (grid = items), or grid-stride over the items with a
+  // persistent grid (PLEX_PUSH_PERSISTENT measurement variant)
+  for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
+    const PushItem it = items[ii];
     constexpr int kSrcEs = kCast ? 4 : 2;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(src_ptrs[it.tensor]) + (uint64_t)it.src_elem * kSrcEs;
     uint16_t* dst = reinterpret_cast<uint16_t*>(dst_arenas[it.dst_rank]) + it.dst_elem;
@@ -474,6 +478,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restri
                                     : reinterpret_cast<const uint16_t*>(src)[si];
         }
     }
+  }
 }
 
 // ---- NEXT-2: derived-param check / re-derivation -------------------------------
@@ -693,14 +698,36 @@ cudaError_t launch_verify(const unsigned long long* got, const unsigned long lon
     return cudaGetLastError();
 }
 
+static int push_persistent() {
+    static const int v = [] {
+        const char* e = std::getenv("PLEX_PUSH_PERSISTENT");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    return v;
+}
+
 cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
                         const uint64_t* dst_arenas, cudaStream_t s) {
-    // grid.x limit is 2^31-1; chunk very long item lists
+    if (!n_items) return cudaSuccess;
+    if (push_persistent()) {
+        if (!g_num_sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+            if (g_num_sms <= 0) g_num_sms = 148;
+        }
+        const uint64_t cap = (uint64_t)g_num_sms * 8;               // 8 x 256 threads resident per SM
+        const uint32_t grid = (uint32_t)(n_items < cap ? n_items : cap);
+        if (cast) push_kernel<true><<<grid, kThreads, 0, s>>>(items, n_items, src_ptrs, dst_arenas);
+        else push_kernel<false><<<grid, kThreads, 0, s>>>(items, n_items, src_ptrs, dst_arenas);
+        return cudaGetLastError();
+    }
+    // one CTA per item; grid.x limit is 2^31-1: chunk very long item lists
     const uint64_t kMax = 1ull << 30;
     for (uint64_t o = 0; o < n_items; o += kMax) {
         const uint64_t n = n_items - o < kMax ? n_items - o : kMax;
-        if (cast) push_kernel<true><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
-        else push_kernel<false><<<(uint32_t)n, kThreads, 0, s>>>(items + o, src_ptrs, dst_arenas);
+        if (cast) push_kernel<true><<<(uint32_t)n, kThreads, 0, s>>>(items + o, n, src_ptrs, dst_arenas);
+        else push_kernel<false><<<(uint32_t)n, kThreads, 0, s>>>(items + o, n, src_ptrs, dst_arenas);
     }
     return cudaGetLastError();
 }
