@@ -413,8 +413,8 @@ template <bool kCast>
 __global__ void __launch_bounds__(kThreads) push_kernel(const PushItem* __restrict__ items, uint64_t n_items,
                                                         const uint64_t* __restrict__ src_ptrs,
                                                         const uint64_t* __restrict__ dst_arenas) {
-  // one item per CTA (grid = items), or grid-stride over the items with a
-  // persistent grid (PLEX_PUSH_PERSISTENT measurement variant)
+  // one item per CTA (the launch uses grid = items; the loop form also
+  // covers a grid smaller than the item list)
   for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
     const PushItem it = items[ii];
     constexpr int kSrcEs = kCast ? 4 : 2;
@@ -698,30 +698,13 @@ cudaError_t launch_verify(const unsigned long long* got, const unsigned long lon
     return cudaGetLastError();
 }
 
-static int push_persistent() {
-    static const int v = [] {
-        const char* e = std::getenv("PLEX_PUSH_PERSISTENT");
-        return e && e[0] == '1' ? 1 : 0;
-    }();
-    return v;
-}
-
+// One CTA per item: a persistent grid-stride variant (148 x 8 CTAs) measured
+// 0.82 vs 0.92 of the peer copy at 7B TP-2 x DP-2 and 0.88 vs 1.06 of HBM at
+// 32B TP-4 (profiles/r02aa_push_persistent_ab.jsonl): the block scheduler's
+// dynamic placement of 64 KiB items beats a static stride.
 cudaError_t launch_push(bool cast, const PushItem* items, uint64_t n_items, const uint64_t* src_ptrs,
                         const uint64_t* dst_arenas, cudaStream_t s) {
     if (!n_items) return cudaSuccess;
-    if (push_persistent()) {
-        if (!g_num_sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-            if (g_num_sms <= 0) g_num_sms = 148;
-        }
-        const uint64_t cap = (uint64_t)g_num_sms * 8;               // 8 x 256 threads resident per SM
-        const uint32_t grid = (uint32_t)(n_items < cap ? n_items : cap);
-        if (cast) push_kernel<true><<<grid, kThreads, 0, s>>>(items, n_items, src_ptrs, dst_arenas);
-        else push_kernel<false><<<grid, kThreads, 0, s>>>(items, n_items, src_ptrs, dst_arenas);
-        return cudaGetLastError();
-    }
     // one CTA per item; grid.x limit is 2^31-1: chunk very long item lists
     const uint64_t kMax = 1ull << 30;
     for (uint64_t o = 0; o < n_items; o += kMax) {
